@@ -1,0 +1,756 @@
+// capi.cpp — the extern "C" boundary (include/groot.h) over the device path.
+//
+// Host-side pieces that are inherently sequential live here: the CSA
+// multiplier generator (input source, src/circuitgen.cpp:66-133), the ASCII
+// AIGER parser (src/aig.cpp:47-88), Glorot init (src/gnn.cpp:113-138) and the
+// ASG1 model format (src/gnn.cpp:330-372). Everything on the data path —
+// features, CSR, batch, partition, regrow, materialize, forward, classify —
+// runs in the CUDA kernels of graph_build.cu / forward.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace groot {
+
+std::atomic<uint64_t> g_launches{0};
+static cudaStream_t g_stream = nullptr;
+static thread_local std::string g_error;
+
+cudaStream_t stream() { return g_stream; }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    GROOT_CUDA(cudaGetDevice(&dev));
+    GROOT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+// graph_build.cu / forward.cu
+groot_graph* encode(uint32_t, uint32_t, const uint32_t*, uint32_t, const uint32_t*, const uint8_t*);
+groot_graph* batch(const groot_graph*, uint32_t);
+groot_graph* graph_from_host(uint32_t, const uint64_t*, const uint32_t*, const uint8_t*, const uint8_t*, uint64_t,
+                             const uint32_t*);
+void graph_copy_out(const groot_graph*, uint64_t*, uint32_t*, uint8_t*, uint8_t*, uint32_t*, uint32_t*);
+groot_assignment* topo_chunks(const groot_graph*, uint32_t);
+groot_assignment* assignment_from_host(uint32_t, const uint32_t*);
+groot_assignment* load_assignment(const char*, uint32_t);
+uint64_t edge_cut(const groot_graph*, const groot_assignment*);
+groot_parts* regrow(const groot_graph*, const groot_assignment*, int);
+groot_graph* materialize(const groot_graph*, const groot_parts*, uint32_t);
+groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<uint64_t>&);
+void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
+void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
+void forward_naive_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
+void spmm_mean_device(groot_graph*, const float*, uint32_t, float*);
+void spmm_csr_device(uint32_t, const uint32_t*, const uint32_t*, const float*, const float*, uint32_t, float*);
+void model_upload(groot_model*);
+void classify_rows(groot_graph*, uint32_t);
+uint32_t hd_threshold();
+
+// ---------------------------------------------------------------------------
+// CSA multiplier generator (src/circuitgen.cpp:13-133). Nodes are created in
+// the reference's order so every downstream array is bit-identical.
+// ---------------------------------------------------------------------------
+namespace {
+
+enum : uint8_t { kPo = 0, kMaj = 1, kXor = 2, kAnd = 3, kPi = 4 };
+constexpr uint32_t kNone = 0xFFFFFFFFu;  // "no literal" in a column slot
+
+struct Csa {
+  uint32_t w;
+  uint32_t inputs;
+  std::vector<uint32_t> ands;    // (left, right) literal pairs
+  std::vector<uint8_t> labels;   // const + PIs + ANDs (+ POs at the end)
+  std::vector<uint32_t> outs;
+
+  explicit Csa(uint32_t width) : w(width), inputs(2 * width) {
+    labels.assign(1 + inputs, kAnd);
+    std::fill(labels.begin() + 1, labels.end(), kPi);
+  }
+  uint32_t node(uint32_t l, uint32_t r, uint8_t cls) {
+    const uint32_t v = 1 + inputs + static_cast<uint32_t>(ands.size() >> 1);
+    ands.push_back(l);
+    ands.push_back(r);
+    labels.push_back(cls);
+    return v << 1;
+  }
+  // Column reduction: 1 input passes, 2 -> half adder, 3 -> full adder.
+  // Returns sum; carry written to *carry (kNone when none).
+  uint32_t reduce(const uint32_t* in, int cnt, uint32_t* carry) {
+    if (cnt == 1) { *carry = kNone; return in[0]; }
+    const uint32_t a = in[0], b = in[1];
+    if (cnt == 2) {  // gen_half_adder
+      const uint32_t c = node(a, b, kMaj);
+      const uint32_t nr = node(a ^ 1, b ^ 1, kAnd);
+      *carry = c;
+      return node(c ^ 1, nr ^ 1, kXor);
+    }
+    const uint32_t cin = in[2];  // gen_full_adder
+    const uint32_t c1 = node(a, b, kAnd);
+    const uint32_t n1 = node(a ^ 1, b ^ 1, kAnd);
+    const uint32_t x1 = node(c1 ^ 1, n1 ^ 1, kAnd);
+    const uint32_t c2 = node(x1, cin, kAnd);
+    const uint32_t n2 = node(x1 ^ 1, cin ^ 1, kAnd);
+    const uint32_t s = node(c2 ^ 1, n2 ^ 1, kXor);
+    const uint32_t mj = node(c1 ^ 1, c2 ^ 1, kMaj);
+    *carry = mj ^ 1;
+    return s;
+  }
+  void build() {
+    auto pp = [&](uint32_t i, uint32_t j) { return node(2 * (i + 1), 2 * (w + j + 1), kAnd); };
+    std::vector<uint32_t> sums(2 * w, kNone), carries(2 * w, kNone), m(2 * w, 0);
+    m[0] = pp(0, 0);
+    for (uint32_t j = 1; j < w; ++j) sums[j] = pp(0, j);
+    std::vector<uint32_t> ns(2 * w), nc(2 * w);
+    for (uint32_t i = 1; i < w; ++i) {
+      std::fill(ns.begin(), ns.end(), kNone);
+      std::fill(nc.begin(), nc.end(), kNone);
+      for (uint32_t j = 0; j < w; ++j) {
+        const uint32_t c = i + j;
+        uint32_t in[3];
+        int cnt = 0;
+        if (sums[c] != kNone) in[cnt++] = sums[c];
+        in[cnt++] = pp(i, j);
+        if (carries[c] != kNone) in[cnt++] = carries[c];
+        uint32_t carry;
+        const uint32_t s = reduce(in, cnt, &carry);
+        (j == 0 ? m[i] : ns[c]) = s;
+        if (carry != kNone) nc[c + 1] = carry;
+      }
+      sums.swap(ns);
+      carries.swap(nc);
+    }
+    uint32_t ripple = kNone;
+    for (uint32_t c = w; c < 2 * w; ++c) {
+      uint32_t in[3];
+      int cnt = 0;
+      if (sums[c] != kNone) in[cnt++] = sums[c];
+      if (carries[c] != kNone) in[cnt++] = carries[c];
+      if (ripple != kNone) in[cnt++] = ripple;
+      if (cnt == 0) fail(GROOT_ERUNTIME, "gen_csa_multiplier: empty column");
+      m[c] = reduce(in, cnt, &ripple);
+    }
+    outs = m;
+    labels.insert(labels.end(), outs.size(), kPo);
+  }
+};
+
+// Closed-form sizes: w^2 partial products; rows 1..w-1 reduce w columns each
+// (column j=0 of row i and the top column are half adders when the carry or
+// sum slot is empty). Counting by construction keeps it exact.
+void csa_counts(uint32_t w, uint32_t* na) {
+  Csa c(w);
+  c.build();
+  *na = static_cast<uint32_t>(c.ands.size() / 2);
+}
+
+// ---------------------------------------------------------------------------
+// ASCII AIGER (src/aig.cpp:47-88) — same validation order and messages.
+// ---------------------------------------------------------------------------
+struct ParsedAig {
+  uint32_t inputs = 0;
+  std::vector<uint32_t> ands, outs;
+};
+
+ParsedAig parse_aiger_text(const char* text, size_t len) {
+  std::istringstream in(std::string(text, len));
+  auto num = [&](const char* what) {
+    uint64_t v;
+    if (!(in >> v)) fail(GROOT_ERUNTIME, std::string("AIGER: missing or bad ") + what);
+    return v;
+  };
+  std::string magic;
+  if (!(in >> magic)) fail(GROOT_ERUNTIME, "AIGER: empty input");
+  if (magic != "aag") fail(GROOT_ERUNTIME, "AIGER: expected ASCII header 'aag', got '" + magic + "'");
+  const uint64_t M = num("M"), I = num("I"), L = num("L"), O = num("O"), A = num("A");
+  if (L != 0) fail(GROOT_ERUNTIME, "AIGER: latches unsupported (sequential circuit)");
+  if (M != I + A) fail(GROOT_ERUNTIME, "AIGER: non-contiguous variable numbering (M != I + A)");
+  if (1 + M + O >= 0xFFFFFFFFull) fail(GROOT_ERUNTIME, "AIGER: too many nodes");
+  ParsedAig p;
+  p.inputs = static_cast<uint32_t>(I);
+  for (uint64_t k = 0; k < I; ++k)
+    if (num("input literal") != 2 * (k + 1)) fail(GROOT_ERUNTIME, "AIGER: inputs must be the literals 2..2I in order");
+  auto lit = [&](uint64_t l, const char* what) {
+    if (l > 2 * M + 1) fail(GROOT_ERUNTIME, std::string("AIGER: ") + what + " literal out of range");
+    return static_cast<uint32_t>(l);
+  };
+  std::vector<uint64_t> olits(O);
+  for (uint64_t k = 0; k < O; ++k) olits[k] = num("output literal");
+  p.ands.reserve(2 * A);
+  for (uint64_t k = 0; k < A; ++k) {
+    const uint64_t lhs = num("AND lhs");
+    if (lhs != 2 * (I + 1 + k)) fail(GROOT_ERUNTIME, "AIGER: AND definitions must appear in ascending index order");
+    const uint32_t l = lit(num("AND rhs0"), "AND rhs0");
+    const uint32_t r = lit(num("AND rhs1"), "AND rhs1");
+    const uint64_t own = lhs >> 1;
+    if ((l >> 1) >= own || (r >> 1) >= own) fail(GROOT_ERUNTIME, "AIGER: fanin index >= own index (cycle)");
+    p.ands.push_back(l);
+    p.ands.push_back(r);
+  }
+  for (uint64_t v : olits) p.outs.push_back(lit(v, "output"));
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// Model: init_model (src/gnn.cpp:113-138), ASG1 I/O (src/gnn.cpp:330-372)
+// ---------------------------------------------------------------------------
+uint64_t param_count(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes) {
+  uint64_t c = 0;
+  uint32_t in = in_dim;
+  for (uint32_t l = 0; l < depth; ++l) {
+    c += 2ull * in * hidden + hidden;
+    in = hidden;
+  }
+  return c + static_cast<uint64_t>(in) * classes + classes;
+}
+
+void init_params(uint64_t seed, uint32_t in_dim, uint32_t hidden, uint32_t classes, uint32_t depth, double* out) {
+  if (depth < 1) fail(GROOT_EINVAL, "init_model: depth must be >= 1");
+  std::mt19937_64 rng(seed);
+  double* q = out;
+  auto glorot = [&](uint32_t rows, uint32_t cols) {
+    const double lim = std::sqrt(6.0 / (rows + cols));
+    std::uniform_real_distribution<double> dist(-lim, lim);
+    for (uint64_t i = 0; i < static_cast<uint64_t>(rows) * cols; ++i) *q++ = dist(rng);
+  };
+  uint32_t in = in_dim;
+  for (uint32_t l = 0; l < depth; ++l) {
+    glorot(in, hidden);
+    glorot(in, hidden);
+    for (uint32_t o = 0; o < hidden; ++o) *q++ = 0.0;
+    in = hidden;
+  }
+  glorot(in, classes);
+  for (uint32_t o = 0; o < classes; ++o) *q++ = 0.0;
+}
+
+groot_model* model_create(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes, const double* prm) {
+  if (depth < 1 || depth > 64) fail(GROOT_EINVAL, "model: depth must be in 1..64");
+  if (in_dim != 4 || hidden != 32) fail(GROOT_EINVAL, "model: the device path supports in_dim 4 and hidden 32");
+  if (classes < 1 || classes > 8) fail(GROOT_EINVAL, "model: classes must be in 1..8");
+  auto* m = new groot_model;
+  m->depth = depth;
+  m->in_dim = in_dim;
+  m->hidden = hidden;
+  m->classes = classes;
+  m->params.assign(prm, prm + param_count(depth, in_dim, hidden, classes));
+  try {
+    model_upload(m);
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  return m;
+}
+
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_error = msg; }
+
+static void need(const void* p, const char* what) {
+  if (!p) fail(GROOT_EINVAL, std::string(what) + ": null argument");
+}
+
+}  // namespace groot
+
+using namespace groot;
+
+extern "C" {
+
+const char* groot_last_error(void) { return g_error.c_str(); }
+int groot_version(void) { return 1; }
+
+int groot_set_stream(void* s) {
+  g_stream = static_cast<cudaStream_t>(s);
+  return GROOT_OK;
+}
+void* groot_get_stream(void) { return g_stream; }
+int groot_device_synchronize(void) {
+  return guarded([] { GROOT_CUDA(cudaStreamSynchronize(g_stream)); });
+}
+uint64_t groot_kernel_launches(void) { return g_launches.load(); }
+void groot_reset_kernel_launches(void) { g_launches.store(0); }
+
+// ---- AIG sources ------------------------------------------------------------
+int groot_csa_sizes(uint32_t width, uint32_t* ni, uint32_t* na, uint32_t* no) {
+  return guarded([&] {
+    if (width < 2) fail(GROOT_EINVAL, "gen_csa_multiplier: width must be >= 2");
+    need(ni, "groot_csa_sizes");
+    csa_counts(width, na);
+    *ni = 2 * width;
+    *no = 2 * width;
+  });
+}
+
+int groot_gen_csa(uint32_t width, uint32_t* and_lits, uint32_t* out_lits, uint8_t* labels) {
+  return guarded([&] {
+    if (width < 2) fail(GROOT_EINVAL, "gen_csa_multiplier: width must be >= 2");
+    Csa c(width);
+    c.build();
+    if (and_lits) std::copy(c.ands.begin(), c.ands.end(), and_lits);
+    if (out_lits) std::copy(c.outs.begin(), c.outs.end(), out_lits);
+    if (labels) std::copy(c.labels.begin(), c.labels.end(), labels);
+  });
+}
+
+int groot_aiger_sizes(const char* text, size_t len, uint32_t* ni, uint32_t* na, uint32_t* no) {
+  return guarded([&] {
+    need(text, "groot_aiger_sizes");
+    const ParsedAig p = parse_aiger_text(text, len);
+    *ni = p.inputs;
+    *na = static_cast<uint32_t>(p.ands.size() / 2);
+    *no = static_cast<uint32_t>(p.outs.size());
+  });
+}
+
+int groot_aiger_fill(const char* text, size_t len, uint32_t* and_lits, uint32_t* out_lits) {
+  return guarded([&] {
+    need(text, "groot_aiger_fill");
+    const ParsedAig p = parse_aiger_text(text, len);
+    if (and_lits) std::copy(p.ands.begin(), p.ands.end(), and_lits);
+    if (out_lits) std::copy(p.outs.begin(), p.outs.end(), out_lits);
+  });
+}
+
+// ---- graphs -----------------------------------------------------------------
+int groot_encode(uint32_t ni, uint32_t na, const uint32_t* ands, uint32_t no, const uint32_t* outs,
+                 const uint8_t* labels, groot_graph** out) {
+  return guarded([&] {
+    need(out, "groot_encode");
+    if (na) need(ands, "groot_encode");
+    if (no) need(outs, "groot_encode");
+    *out = encode(ni, na, ands, no, outs, labels);
+  });
+}
+
+int groot_batch(const groot_graph* g, uint32_t copies, groot_graph** out) {
+  return guarded([&] {
+    need(g, "groot_batch");
+    *out = batch(g, copies);
+  });
+}
+
+int groot_graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col, const uint8_t* feat,
+                          const uint8_t* lab, uint64_t ne, const uint32_t* edges, groot_graph** out) {
+  return guarded([&] {
+    need(rp, "groot_graph_from_host");
+    if (rp[n]) need(col, "groot_graph_from_host");
+    *out = graph_from_host(n, rp, col, feat, lab, ne, edges);
+  });
+}
+
+int groot_graph_sizes(const groot_graph* g, uint32_t* n, uint64_t* nnz, uint64_t* ne) {
+  return guarded([&] {
+    need(g, "groot_graph_sizes");
+    if (n) *n = g->n;
+    if (nnz) *nnz = g->nnz;
+    if (ne) *ne = g->ne;
+  });
+}
+
+int groot_graph_copy_out(const groot_graph* g, uint64_t* rp, uint32_t* col, uint8_t* feat, uint8_t* lab,
+                         uint32_t* deg, uint32_t* edges) {
+  return guarded([&] {
+    need(g, "groot_graph_copy_out");
+    graph_copy_out(g, rp, col, feat, lab, deg, edges);
+  });
+}
+
+int groot_graph_device_ptrs(const groot_graph* g, const uint32_t** rp, const uint32_t** col, const uint8_t** feat,
+                            const uint8_t** lab, const uint32_t** edges) {
+  return guarded([&] {
+    need(g, "groot_graph_device_ptrs");
+    if (rp) *rp = g->rp.p;
+    if (col) *col = g->col.p;
+    if (feat) *feat = g->feat.p;
+    if (lab) *lab = g->labels.p;
+    if (edges) *edges = g->edges.p;
+  });
+}
+
+void groot_graph_free(groot_graph* g) { delete g; }
+
+// ---- partition ----------------------------------------------------------------
+int groot_partition_topo_chunks(const groot_graph* g, uint32_t k, groot_assignment** out) {
+  return guarded([&] {
+    need(g, "groot_partition_topo_chunks");
+    *out = topo_chunks(g, k);
+  });
+}
+
+int groot_load_assignment(const char* path, uint32_t n, groot_assignment** out) {
+  return guarded([&] {
+    need(path, "groot_load_assignment");
+    *out = load_assignment(path, n);
+  });
+}
+
+int groot_assignment_from_host(uint32_t n, const uint32_t* part_of, groot_assignment** out) {
+  return guarded([&] {
+    need(part_of, "groot_assignment_from_host");
+    *out = assignment_from_host(n, part_of);
+  });
+}
+
+int groot_assignment_info(const groot_assignment* a, uint32_t* n, uint32_t* k) {
+  return guarded([&] {
+    need(a, "groot_assignment_info");
+    if (n) *n = a->n;
+    if (k) *k = a->k;
+  });
+}
+
+int groot_assignment_copy_out(const groot_assignment* a, uint32_t* part_of) {
+  return guarded([&] {
+    need(a, "groot_assignment_copy_out");
+    a->part_of.download(part_of, a->n);
+    stream_sync();
+  });
+}
+
+void groot_assignment_free(groot_assignment* a) { delete a; }
+
+int groot_crossing_fraction(const groot_graph* g, const groot_assignment* a, double* fraction) {
+  return guarded([&] {
+    need(g, "groot_crossing_fraction");
+    need(a, "groot_crossing_fraction");
+    *fraction = g->ne ? static_cast<double>(edge_cut(g, a)) / static_cast<double>(g->ne) : 0.0;
+  });
+}
+
+int groot_edge_cut(const groot_graph* g, const groot_assignment* a, uint64_t* cut) {
+  return guarded([&] {
+    need(g, "groot_edge_cut");
+    need(a, "groot_edge_cut");
+    *cut = edge_cut(g, a);
+  });
+}
+
+// ---- regrow -----------------------------------------------------------------------
+int groot_regrow(const groot_graph* g, const groot_assignment* a, int with_b, groot_parts** out) {
+  return guarded([&] {
+    need(g, "groot_regrow");
+    need(a, "groot_regrow");
+    *out = regrow(g, a, with_b);
+  });
+}
+
+int groot_parts_count(const groot_parts* p, uint32_t* k) {
+  return guarded([&] {
+    need(p, "groot_parts_count");
+    *k = p->k;
+  });
+}
+
+int groot_parts_sizes(const groot_parts* p, uint32_t part, uint32_t* nc, uint32_t* nb, uint64_t* ne) {
+  return guarded([&] {
+    need(p, "groot_parts_sizes");
+    if (part >= p->k) fail(GROOT_EINVAL, "parts: index out of range");
+    if (nc) *nc = static_cast<uint32_t>(p->core_off[part + 1] - p->core_off[part]);
+    if (nb) *nb = static_cast<uint32_t>(p->bnd_off[part + 1] - p->bnd_off[part]);
+    if (ne) *ne = p->edge_off[part + 1] - p->edge_off[part];
+  });
+}
+
+int groot_parts_copy_out(const groot_parts* p, uint32_t part, uint32_t* core, uint32_t* bnd, uint32_t* edges) {
+  return guarded([&] {
+    need(p, "groot_parts_copy_out");
+    if (part >= p->k) fail(GROOT_EINVAL, "parts: index out of range");
+    const uint64_t c0 = p->core_off[part], c1 = p->core_off[part + 1];
+    const uint64_t b0 = p->bnd_off[part], b1 = p->bnd_off[part + 1];
+    const uint64_t e0 = p->edge_off[part], e1 = p->edge_off[part + 1];
+    if (core && c1 > c0)
+      GROOT_CUDA(cudaMemcpyAsync(core, p->core.p + c0, (c1 - c0) * 4, cudaMemcpyDeviceToHost, stream()));
+    if (bnd && b1 > b0)
+      GROOT_CUDA(cudaMemcpyAsync(bnd, p->bnd.p + b0, (b1 - b0) * 4, cudaMemcpyDeviceToHost, stream()));
+    if (edges && e1 > e0)
+      GROOT_CUDA(cudaMemcpyAsync(edges, p->edges.p + 2 * e0, (e1 - e0) * 8, cudaMemcpyDeviceToHost, stream()));
+    stream_sync();
+  });
+}
+
+int groot_footprint_proxy(const groot_parts* p, uint32_t feature_cols, uint32_t hidden_dim, uint64_t* bytes) {
+  return guarded([&] {
+    need(p, "groot_footprint_proxy");
+    uint64_t best = 0;
+    for (uint32_t q = 0; q < p->k; ++q) {
+      const uint64_t size = (p->core_off[q + 1] - p->core_off[q]) + (p->bnd_off[q + 1] - p->bnd_off[q]);
+      const uint64_t ne = p->edge_off[q + 1] - p->edge_off[q];
+      best = std::max(best, size * (feature_cols + hidden_dim) * 4 + 2 * ne * 8);
+    }
+    *bytes = best;
+  });
+}
+
+int groot_materialize(const groot_graph* g, const groot_parts* p, uint32_t part, groot_graph** out) {
+  return guarded([&] {
+    need(g, "groot_materialize");
+    need(p, "groot_materialize");
+    *out = materialize(g, p, part);
+  });
+}
+
+void groot_parts_free(groot_parts* p) { delete p; }
+
+// ---- model --------------------------------------------------------------------------
+uint64_t groot_param_count(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes) {
+  return param_count(depth, in_dim, hidden, classes);
+}
+
+int groot_init_params(uint64_t seed, uint32_t in_dim, uint32_t hidden, uint32_t classes, uint32_t depth,
+                      double* params) {
+  return guarded([&] {
+    need(params, "groot_init_params");
+    init_params(seed, in_dim, hidden, classes, depth, params);
+  });
+}
+
+int groot_model_create(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes, const double* params,
+                       groot_model** out) {
+  return guarded([&] {
+    need(params, "groot_model_create");
+    *out = model_create(depth, in_dim, hidden, classes, params);
+  });
+}
+
+int groot_model_load(const char* path, groot_model** out) {
+  return guarded([&] {
+    need(path, "groot_model_load");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail(GROOT_ERUNTIME, std::string("cannot open model file: ") + path);
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::string(magic, 4) != "ASG1") fail(GROOT_ERUNTIME, "model file: bad magic or version");
+    uint32_t hdr[4];
+    in.read(reinterpret_cast<char*>(hdr), 16);
+    if (!in || hdr[0] == 0 || hdr[0] > 64) fail(GROOT_ERUNTIME, "model file: bad header");
+    std::vector<double> prm(param_count(hdr[0], hdr[1], hdr[2], hdr[3]));
+    in.read(reinterpret_cast<char*>(prm.data()), static_cast<std::streamsize>(prm.size() * 8));
+    if (!in) fail(GROOT_ERUNTIME, "model file: truncated");
+    *out = model_create(hdr[0], hdr[1], hdr[2], hdr[3], prm.data());
+  });
+}
+
+int groot_model_save(const groot_model* m, const char* path) {
+  return guarded([&] {
+    need(m, "groot_model_save");
+    std::ofstream out(path, std::ios::binary);
+    if (!out) fail(GROOT_ERUNTIME, std::string("cannot write model file: ") + path);
+    out.write("ASG1", 4);
+    const uint32_t hdr[4] = {m->depth, m->in_dim, m->hidden, m->classes};
+    out.write(reinterpret_cast<const char*>(hdr), 16);
+    out.write(reinterpret_cast<const char*>(m->params.data()), static_cast<std::streamsize>(m->params.size() * 8));
+  });
+}
+
+int groot_model_info(const groot_model* m, uint32_t* depth, uint32_t* in_dim, uint32_t* hidden, uint32_t* classes) {
+  return guarded([&] {
+    need(m, "groot_model_info");
+    if (depth) *depth = m->depth;
+    if (in_dim) *in_dim = m->in_dim;
+    if (hidden) *hidden = m->hidden;
+    if (classes) *classes = m->classes;
+  });
+}
+
+int groot_model_params(const groot_model* m, double* params) {
+  return guarded([&] {
+    need(m, "groot_model_params");
+    std::copy(m->params.begin(), m->params.end(), params);
+  });
+}
+
+void groot_model_free(groot_model* m) { delete m; }
+
+// ---- forward / predict -------------------------------------------------------------
+static void finish_confusion(const uint64_t* conf, uint32_t n, uint64_t* confusion, double* accuracy) {
+  if (confusion) std::copy(conf, conf + 25, confusion);
+  if (accuracy) {
+    uint64_t hit = 0;
+    for (int c = 0; c < 5; ++c) hit += conf[c * 5 + c];
+    *accuracy = n ? static_cast<double>(hit) / static_cast<double>(n) : 0.0;
+  }
+}
+
+int groot_forward(const groot_model* m, const groot_graph* g, float* logits_host) {
+  return guarded([&] {
+    need(m, "groot_forward");
+    need(g, "groot_forward");
+    auto* gg = const_cast<groot_graph*>(g);
+    DevBuf<uint8_t> cls(g->n);
+    DevBuf<float> lg(static_cast<size_t>(g->n) * m->classes);
+    forward_device(m, gg, cls.p, lg.p, nullptr);
+    if (logits_host) lg.download(logits_host, static_cast<size_t>(g->n) * m->classes);
+    stream_sync();
+  });
+}
+
+// Debug/differential path: thread-per-row kernels (tests only).
+int groot_debug_forward_naive(const groot_model* m, const groot_graph* g, float* logits_host, uint8_t* labels_host) {
+  return guarded([&] {
+    need(m, "groot_debug_forward_naive");
+    need(g, "groot_debug_forward_naive");
+    auto* gg = const_cast<groot_graph*>(g);
+    DevBuf<uint8_t> cls(g->n);
+    DevBuf<float> lg(static_cast<size_t>(g->n) * m->classes);
+    forward_naive_device(m, gg, cls.p, lg.p, nullptr);
+    if (logits_host) lg.download(logits_host, static_cast<size_t>(g->n) * m->classes);
+    if (labels_host) cls.download(labels_host, g->n);
+    stream_sync();
+  });
+}
+
+int groot_predict_full(const groot_model* m, const groot_graph* g, uint8_t* labels_host, uint64_t* confusion,
+                       double* accuracy) {
+  return guarded([&] {
+    need(m, "groot_predict_full");
+    need(g, "groot_predict_full");
+    auto* gg = const_cast<groot_graph*>(g);
+    DevBuf<uint8_t> cls(g->n);
+    DevBuf<unsigned long long> conf(25);
+    conf.zero();
+    forward_device(m, gg, cls.p, nullptr, conf.p);
+    uint64_t h[25];
+    conf.download(reinterpret_cast<unsigned long long*>(h), 25);
+    if (labels_host) cls.download(labels_host, g->n);
+    stream_sync();
+    finish_confusion(h, g->n, confusion, accuracy);
+  });
+}
+
+int groot_predict_full_dev(const groot_model* m, const groot_graph* g, uint8_t* labels_dev, float* logits_dev,
+                           uint64_t* confusion_dev) {
+  return guarded([&] {
+    need(m, "groot_predict_full_dev");
+    need(g, "groot_predict_full_dev");
+    need(labels_dev, "groot_predict_full_dev");
+    forward_device(m, const_cast<groot_graph*>(g), labels_dev, logits_dev,
+                   reinterpret_cast<unsigned long long*>(confusion_dev));
+  });
+}
+
+int groot_predict(const groot_model* m, const groot_graph* g, const groot_parts* p, uint8_t* labels_host,
+                  uint64_t* confusion, double* accuracy) {
+  return guarded([&] {
+    need(m, "groot_predict");
+    need(g, "groot_predict");
+    need(p, "groot_predict");
+    std::vector<uint64_t> node_off;
+    groot_graph* u = union_of_parts(g, p, node_off);
+    try {
+      DevBuf<uint8_t> cls(u->n), out(g->n);
+      out.zero();
+      forward_device(m, u, cls.p, nullptr, nullptr);
+      scatter_core_labels(p, node_off, cls.p, out.p);
+      std::vector<uint8_t> pred(g->n), truth(g->n);
+      out.download(pred.data(), g->n);
+      g->labels.download(truth.data(), g->n);
+      stream_sync();
+      uint64_t conf[25] = {0};
+      for (uint32_t v = 0; v < g->n; ++v)
+        if (truth[v] < 5 && pred[v] < 5) ++conf[truth[v] * 5 + pred[v]];
+      if (labels_host) std::copy(pred.begin(), pred.end(), labels_host);
+      finish_confusion(conf, g->n, confusion, accuracy);
+    } catch (...) {
+      delete u;
+      throw;
+    }
+    delete u;
+  });
+}
+
+int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uint32_t* ands, uint32_t no,
+                       const uint32_t* outs, const uint8_t* labels, uint32_t copies, uint8_t* labels_out,
+                       uint64_t* confusion, double* accuracy) {
+  return guarded([&] {
+    need(m, "groot_classify_aig");
+    groot_graph* g1 = encode(ni, na, ands, no, outs, labels);
+    groot_graph* g = g1;
+    try {
+      if (copies > 1) {
+        g = batch(g1, copies);
+        delete g1;
+        g1 = nullptr;
+      } else if (copies < 1) {
+        fail(GROOT_EINVAL, "batch: copy count must be >= 1");
+      }
+      DevBuf<uint8_t> cls(g->n);
+      DevBuf<unsigned long long> conf(25);
+      conf.zero();
+      forward_device(m, g, cls.p, nullptr, conf.p);
+      uint64_t h[25];
+      conf.download(reinterpret_cast<unsigned long long*>(h), 25);
+      if (labels_out) cls.download(labels_out, g->n);
+      stream_sync();
+      finish_confusion(h, g->n, confusion, accuracy);
+    } catch (...) {
+      delete g1;
+      if (g != g1) delete g;
+      throw;
+    }
+    if (g != g1) delete g;
+    delete g1;
+  });
+}
+
+// ---- SpMM ------------------------------------------------------------------------------
+int groot_spmm_mean(const groot_graph* g, const float* dense, uint32_t f, float* out) {
+  return guarded([&] {
+    need(g, "groot_spmm_mean");
+    need(dense, "groot_spmm_mean");
+    need(out, "groot_spmm_mean");
+    if (f == 0) fail(GROOT_EINVAL, "spmm: f must be >= 1");
+    DevBuf<float> d(static_cast<size_t>(g->n) * f), o(static_cast<size_t>(g->n) * f);
+    d.upload(dense, static_cast<size_t>(g->n) * f);
+    spmm_mean_device(const_cast<groot_graph*>(g), d.p, f, o.p);
+    o.download(out, static_cast<size_t>(g->n) * f);
+    stream_sync();
+  });
+}
+
+int groot_spmm_mean_dev(const groot_graph* g, const float* dense_dev, uint32_t f, float* out_dev) {
+  return guarded([&] {
+    need(g, "groot_spmm_mean_dev");
+    if (f == 0) fail(GROOT_EINVAL, "spmm: f must be >= 1");
+    spmm_mean_device(const_cast<groot_graph*>(g), dense_dev, f, out_dev);
+  });
+}
+
+int groot_spmm_csr(uint32_t rows, uint32_t cols, const uint64_t* rp, const uint32_t* col, const float* vals,
+                   const float* dense, uint32_t f, float* out) {
+  return guarded([&] {
+    need(rp, "groot_spmm_csr");
+    const uint64_t nnz = rp[rows];
+    if (nnz >= 0xFFFFFFFFull) fail(GROOT_EINVAL, "spmm: nnz must be < 2^32");
+    std::vector<uint32_t> rp32(rows + 1ull);
+    for (uint32_t r = 0; r <= rows; ++r) {
+      if (r && rp[r] < rp[r - 1]) fail(GROOT_EINVAL, "CsrMatrix: row_ptr not monotone");
+      rp32[r] = static_cast<uint32_t>(rp[r]);
+    }
+    for (uint64_t q = 0; q < nnz; ++q)
+      if (col[q] >= cols) fail(GROOT_EINVAL, "CsrMatrix: column index out of range");
+    DevBuf<uint32_t> drp(rows + 1ull), dcol(nnz);
+    DevBuf<float> dval(nnz), dd(static_cast<size_t>(cols) * f), dout(static_cast<size_t>(rows) * f);
+    drp.upload(rp32.data(), rows + 1ull);
+    dcol.upload(col, nnz);
+    if (vals) dval.upload(vals, nnz);
+    dd.upload(dense, static_cast<size_t>(cols) * f);
+    spmm_csr_device(rows, drp.p, dcol.p, vals ? dval.p : nullptr, dd.p, f, dout.p);
+    dout.download(out, static_cast<size_t>(rows) * f);
+    stream_sync();
+  });
+}
+
+}  // extern "C"

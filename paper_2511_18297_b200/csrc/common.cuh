@@ -1,0 +1,164 @@
+// common.cuh — shared host/device plumbing for libgroot_b200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "groot.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libgroot_b200 is built for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace groot {
+
+// Error carried to the C ABI: code is one of GROOT_E*.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const char* msg) {
+  if (!ok) fail(GROOT_EINVAL, msg);
+}
+
+#define GROOT_CUDA(expr)                                                                       \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      ::groot::fail(GROOT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+cudaStream_t stream();
+
+// Launch helper: counts launches (bench evidence) and checks the launch.
+#define GROOT_LAUNCH(kernel, grid, block, smem, ...)                                           \
+  do {                                                                                         \
+    kernel<<<(grid), (block), (smem), ::groot::stream()>>>(__VA_ARGS__);                      \
+    ::groot::g_launches.fetch_add(1, std::memory_order_relaxed);                               \
+    GROOT_CUDA(cudaGetLastError());                                                            \
+  } while (0)
+
+inline void stream_sync() { GROOT_CUDA(cudaStreamSynchronize(stream())); }
+
+// Thread-local message returned by groot_last_error().
+void set_last_error(const std::string& msg);
+
+// Runs f, mapping exceptions to GROOT_* status codes for the C ABI.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GROOT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return GROOT_ERUNTIME;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return GROOT_ERUNTIME;
+  }
+}
+int num_sms();
+
+// Owning device buffer.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) GROOT_CUDA(cudaMalloc(&p, count * sizeof(T) + 16));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void zero() {
+    if (p) GROOT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream()));
+  }
+  void upload(const T* h, size_t count) {
+    if (count) GROOT_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, stream()));
+  }
+  void download(T* h, size_t count) const {
+    if (count) GROOT_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  }
+};
+
+inline unsigned blocks_for(uint64_t items, unsigned threads, unsigned cap = 148u * 16u) {
+  uint64_t b = (items + threads - 1) / threads;
+  if (b == 0) b = 1;
+  return static_cast<unsigned>(b < cap ? b : cap);
+}
+
+// ---- graph-building primitives (graph_build.cu) -----------------------------
+// Symmetric CSR from a forward edge list (build_symmetric_csr, src/encode.cpp:14-31):
+// rows ascending, duplicates kept. rp: u32[n+1], col: u32[2*ne].
+void build_csr(uint32_t n, uint64_t ne, const uint32_t* d_edges, uint32_t* d_rp, uint32_t* d_col);
+// Exclusive prefix sum of u32 counts into u32 offsets (count+1 outputs).
+void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t count);
+void exclusive_scan_u64(const uint64_t* d_in, uint64_t* d_out, uint64_t count);
+
+}  // namespace groot
+
+// ---- opaque handle bodies --------------------------------------------------------
+struct groot_graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t nnz = 0, ne = 0;
+  groot::DevBuf<uint32_t> rp;      // n+1 (u32: nnz < 2^32 enforced)
+  groot::DevBuf<uint32_t> col;     // nnz
+  groot::DevBuf<uint8_t> feat;     // 4n, byte j of node v = feature j (== u32 per node)
+  groot::DevBuf<uint8_t> labels;   // n
+  groot::DevBuf<uint32_t> edges;   // 2*ne (fwd_edges pairs)
+  // Forward-path cache: row classifier output and activation buffers.
+  uint32_t hd_threshold = 0;
+  uint32_t num_hd = 0;
+  groot::DevBuf<uint32_t> hd_rows;  // rows with degree >= hd_threshold, ascending
+  groot::DevBuf<float> hd_mean;     // num_hd x 32 neighbour means (scratch per layer)
+  groot::DevBuf<float> act[2];      // n x 32 ping-pong activations
+};
+
+struct groot_assignment {
+  uint32_t n = 0, k = 0;
+  groot::DevBuf<uint32_t> part_of;
+};
+
+struct groot_parts {
+  uint32_t k = 0;
+  int with_boundary = 1;
+  std::vector<uint64_t> core_off, bnd_off, edge_off;  // host copies, k+1 each
+  groot::DevBuf<uint32_t> core;    // concatenated core_nodes
+  groot::DevBuf<uint32_t> bnd;     // concatenated boundary_nodes
+  groot::DevBuf<uint32_t> edges;   // concatenated local edge pairs
+};
+
+struct groot_model {
+  uint32_t depth = 0, in_dim = 0, hidden = 0, classes = 0;
+  std::vector<double> params;       // fp64, ASG1 order (host copy)
+  groot::DevBuf<float> l0;          // layer 0: Ws[4x32], Wn[4x32], b[32]
+  groot::DevBuf<uint32_t> bimg;     // layers >= 1: 16 KB smem image each (B hi/lo, swizzled)
+  groot::DevBuf<float> bias;        // layers >= 1: 32 each
+  groot::DevBuf<float> naive_w;     // fp32 row-major weights for the naive debug path
+  groot::DevBuf<float> head;        // W_out[32 x classes] then b_out[classes]
+};

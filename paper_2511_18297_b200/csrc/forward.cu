@@ -1,0 +1,777 @@
+// forward.cu — GraphSAGE mean-aggregator forward + classify on sm_100a.
+//
+// Reference: run_forward / predict_full (src/gnn.cpp:37-52, 259-300) over the
+// degree-polarised SpMM (src/spmm.cpp:37-127, inc/spmm.hpp:106-181).
+//
+// Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel does
+//   gather (LD rows)  ->  [h | mean(h_N)] tile in smem (TF32 hi/lo split)
+//   -> tcgen05.mma kind::tf32 (3 products: hi*hi + hi*lo + lo*hi) into TMEM
+//   -> tcgen05.ld epilogue: + bias, ReLU, coalesced store (or, in the last
+//      layer, the 32 -> classes head + first-max argmax + confusion counts).
+// High-degree rows (the row classifier's HD band; the PIs of a multiplier)
+// are aggregated first by a CTA-per-row kernel with a fixed-order reduction.
+// Layer 0 (4 -> 32, inputs in {0,1}^4) is a gather + FFMA kernel.
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace groot {
+
+constexpr int kF = 32;                       // hidden width (tensor-core layers)
+constexpr int kTileM = 128;                  // rows per MMA tile (UMMA M)
+constexpr int kEpiWarps = 4;                 // warps 0..3: TMEM lane quadrants
+constexpr int kProdWarps = 8;                // warps 4..11: gather producers
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 12: TMEM alloc + MMA issue
+constexpr int kThreads = (kMmaWarp + 1) * 32;     // 416
+constexpr int kStages = 2;
+constexpr uint32_t kTileBytes = kTileM * 128;     // 128 rows x 32 fp32
+constexpr uint32_t kStageBytes = 4 * kTileBytes;  // h_hi, h_lo, m_hi, m_lo
+constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
+constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
+constexpr int kMaxClasses = 8;
+constexpr uint32_t kTmemCols = 64;                // two 32-column fp32 accumulators
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBBytes + kEpiBytes +
+                                (kF * kMaxClasses + kMaxClasses + kF) * 4 + 8 * 8 + 4 + 25 * 4 + 1024;
+
+uint32_t hd_threshold() {
+  static uint32_t t = [] {
+    const char* e = std::getenv("GROOT_HD_THRESHOLD");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 128u;
+  }();
+  return t;
+}
+
+struct HdInfo {
+  const uint32_t* rows;  // ascending
+  uint32_t count;
+  uint32_t threshold;
+  const float* mean;  // count x width
+};
+
+__device__ __forceinline__ uint32_t hd_slot(const HdInfo& hd, uint32_t row) {
+  uint32_t lo = 0, hi = hd.count;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (hd.rows[mid] < row) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4scale(float4 a, float s) {
+  return make_float4(a.x * s, a.y * s, a.z * s, a.w * s);
+}
+
+// Mean of neighbour rows for NR rows per 8-lane group (lane j owns columns
+// 4j..4j+3). LD rows: up to 8 neighbours' 128-byte rows are loaded at once per
+// row (coalesced LDG.128 per group), summed in nonzero order, then scaled by
+// 1/deg. HD rows (degree >= threshold) read the precomputed mean. The loop
+// bounds are warp-uniform so shuffles stay convergent.
+template <int NR>
+__device__ __forceinline__ void gather_mean32(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                              const float* __restrict__ H, uint32_t n, const uint32_t (&row)[NR],
+                                              int j, int gbase, const HdInfo& hd, float4 (&m)[NR]) {
+  uint32_t b[NR], d[NR], c[NR];
+  bool is_hd[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    b[q] = 0;
+    d[q] = 0;
+    if (row[q] < n) {
+      b[q] = __ldg(rp + row[q]);
+      d[q] = __ldg(rp + row[q] + 1) - b[q];
+    }
+    is_hd[q] = d[q] >= hd.threshold;
+  }
+  uint32_t dl[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    dl[q] = is_hd[q] ? 0u : d[q];
+    c[q] = (static_cast<uint32_t>(j) < dl[q]) ? __ldg(col + b[q] + j) : 0u;
+  }
+  float4 v[NR][8];
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t ci = __shfl_sync(0xffffffffu, c[q], gbase + t);
+      v[q][t] = (static_cast<uint32_t>(t) < dl[q]) ? ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    float4 acc = v[q][0];
+#pragma unroll
+    for (int t = 1; t < 8; ++t)
+      if (static_cast<uint32_t>(t) < dl[q]) acc = f4add(acc, v[q][t]);
+    m[q] = acc;
+  }
+  // Rows with 8 < degree < threshold: remaining neighbours, 8 at a time.
+  uint32_t dmax = 0;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) dmax = max(dmax, dl[q]);
+  dmax = __reduce_max_sync(0xffffffffu, dmax);
+  for (uint32_t k = 8; k < dmax; k += 8) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const uint32_t cc = (k + j < dl[q]) ? __ldg(col + b[q] + k + j) : 0u;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + t);
+        if (k + t < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j));
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    if (is_hd[q]) {
+      m[q] = ptx::ldg_f4(hd.mean + static_cast<size_t>(hd_slot(hd, row[q])) * kF + 4 * j);
+    } else {
+      const float inv = d[q] > 0 ? 1.0f / static_cast<float>(d[q]) : 0.0f;
+      m[q] = f4scale(m[q], inv);
+    }
+  }
+}
+
+// Store one 16-byte chunk (4 fp32) of a tile row as TF32 hi and lo parts into
+// SWIZZLE_128B K-major layout: chunk j of row i sits at i*128 + ((j ^ (i&7)) << 4).
+__device__ __forceinline__ void store_split(uint8_t* hi_base, uint32_t i, int j, float4 x) {
+  float4 h, l;
+  h.x = ptx::tf32_rna(x.x); l.x = x.x - h.x;
+  h.y = ptx::tf32_rna(x.y); l.y = x.y - h.y;
+  h.z = ptx::tf32_rna(x.z); l.z = x.z - h.z;
+  h.w = ptx::tf32_rna(x.w); l.w = x.w - h.w;
+  const uint32_t off = i * 128u + ((static_cast<uint32_t>(j) ^ (i & 7u)) << 4);
+  *reinterpret_cast<float4*>(hi_base + off) = h;
+  *reinterpret_cast<float4*>(hi_base + kTileBytes + off) = l;
+}
+
+struct LayerArgs {
+  uint32_t n;
+  const uint32_t* rp;
+  const uint32_t* col;
+  const float* hin;      // n x 32
+  float* hout;           // n x 32 (unused in the last layer)
+  const uint32_t* bimg;  // 16 KB swizzled W image (hi/lo)
+  const float* bias;     // 32
+  HdInfo hd;
+  const float* head;     // W_out [32 x classes] row-major, then b_out
+  uint32_t classes;
+  uint8_t* cls;          // last layer: n classes
+  float* logits;         // last layer: n x classes (optional)
+  const uint8_t* labels; // optional (confusion)
+  unsigned long long* confusion;  // optional, 25 counters
+};
+
+template <bool kLast>
+__global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kStages * kStageBytes;
+  uint8_t* sE = sB + kBBytes;
+  float* sHead = reinterpret_cast<float*>(sE + kEpiBytes);
+  float* sBias = sHead + kF * kMaxClasses + kMaxClasses;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + kF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  uint64_t* tfull = bars + 4;
+  uint64_t* tempty = bars + 6;
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 8);
+  uint32_t* sConf = sTmem + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = a.n;
+  const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+
+  for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
+  if (threadIdx.x < kF) sBias[threadIdx.x] = a.bias[threadIdx.x];
+  if (kLast) {
+    for (uint32_t i = threadIdx.x; i < kF * a.classes + a.classes; i += kThreads) sHead[i] = a.head[i];
+    if (threadIdx.x < 25) sConf[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], kProdWarps * 32);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], kEpiWarps * 32);
+    }
+    ptx::mbar_fence_init();
+  }
+  if (warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *sTmem;
+
+  if (warp >= kEpiWarps && warp < kMmaWarp) {
+    // ===== gather producers =====
+    const int pw = warp - kEpiWarps;
+    const int g = lane >> 3, j = lane & 7, gbase = lane & 24;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+      ptx::mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* st = sA + s * kStageBytes;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        uint32_t li[2], row[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          li[q] = pw * 16 + pass * 8 + q * 4 + g;
+          row[q] = t * kTileM + li[q];
+        }
+        float4 m[2];
+        gather_mean32<2>(a.rp, a.col, a.hin, n, row, j, gbase, a.hd, m);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float4 h = row[q] < n ? ptx::ldg_f4(a.hin + static_cast<size_t>(row[q]) * kF + 4 * j)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+          store_split(st, li[q], j, h);                       // K block 0: self features
+          store_split(st + 2 * kTileBytes, li[q], j, m[q]);   // K block 1: neighbour mean
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&full[s]);
+    }
+  } else if (warp == kMmaWarp) {
+    // ===== MMA issuer (one thread) =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
+      const uint32_t a0 = ptx::smem_addr(sA), b0 = ptx::smem_addr(sB);
+      uint32_t it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+        const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::mbar_wait(&tempty[acc], aph ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * kF;
+#pragma unroll
+        for (uint32_t kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint32_t ao = a0 + s * kStageBytes + kb * 2 * kTileBytes + kk * 32;
+            const uint32_t bo = b0 + kb * 8192 + kk * 32;
+            const uint64_t ahi = ptx::umma_desc_sw128(ao), alo = ptx::umma_desc_sw128(ao + kTileBytes);
+            const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
+            ptx::mma_tf32(d, ahi, bhi, idesc, (kb | kk) != 0);
+            ptx::mma_tf32(d, ahi, blo, idesc, 1);
+            ptx::mma_tf32(d, alo, bhi, idesc, 1);
+          }
+        ptx::mma_commit(&empty[s]);
+        ptx::mma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue: TMEM -> registers -> bias/ReLU -> store (or head + argmax) =====
+    const uint32_t q = warp;  // lanes 32q..32q+31 of TMEM
+    uint8_t* ew = sE + q * 4096;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t acc = it & 1, ph = (it >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], ph);
+      ptx::tc_fence_after();
+      float r[32];
+      ptx::tmem_ld_32x32b_x32(tmem_base + acc * kF + ((q * 32u) << 16), r);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + sBias[i], 0.0f);
+      const uint32_t row0 = t * kTileM + q * 32;
+      if (!kLast) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(ew + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+              make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t ri = k * 4 + (lane >> 3), c = lane & 7;
+          const float4 v = *reinterpret_cast<const float4*>(ew + ri * 128 + ((c ^ (ri & 7)) << 4));
+          if (row0 + ri < n) *reinterpret_cast<float4*>(a.hout + static_cast<size_t>(row0 + ri) * kF + 4 * c) = v;
+        }
+        __syncwarp();
+      } else {
+        const uint32_t row = row0 + lane;
+        const uint32_t C = a.classes;
+        float best = 0.f;
+        uint32_t arg = 0;
+        for (uint32_t c = 0; c < C; ++c) {
+          float s = 0.f;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) s = fmaf(r[k], sHead[k * C + c], s);
+          s += sHead[kF * C + c];
+          if (c == 0 || s > best) { best = s; arg = c; }
+          if (a.logits && row < n) a.logits[static_cast<size_t>(row) * C + c] = s;
+        }
+        if (row < n) {
+          a.cls[row] = static_cast<uint8_t>(arg);
+          if (a.confusion && a.labels) {
+            const uint32_t tr = a.labels[row];
+            if (tr < 5 && arg < 5) atomicAdd(&sConf[tr * 5 + arg], 1u);
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (kLast && a.confusion && threadIdx.x < 25 && sConf[threadIdx.x])
+    atomicAdd(&a.confusion[threadIdx.x], static_cast<unsigned long long>(sConf[threadIdx.x]));
+  if (warp == kMmaWarp) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Layer 0: 4 -> 32 from u8 features (one u32 word per node). 8 lanes per row,
+// lane j computes outputs 4j..4j+3. Neighbour feature words are summed as
+// packed byte counters (exact: LD degree < 256), so the mean is exact up to
+// the final 1/deg scaling.
+// ---------------------------------------------------------------------------
+struct Layer0Args {
+  uint32_t n;
+  const uint32_t* rp;
+  const uint32_t* col;
+  const uint32_t* feat;
+  const float* w;  // Ws[4][32], Wn[4][32], b[32]
+  HdInfo hd;       // mean width 4
+  float* hout;
+};
+
+__global__ void __launch_bounds__(256) sage_layer0_kernel(const Layer0Args a) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
+  float4 ws[4], wn[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    ws[k] = ptx::ldg_f4(a.w + k * 32 + 4 * j);
+    wn[k] = ptx::ldg_f4(a.w + 128 + k * 32 + 4 * j);
+  }
+  const float4 bias = ptx::ldg_f4(a.w + 256 + 4 * j);
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; base < a.n; base += warps * 4) {
+    const uint32_t row = base + g;
+    uint32_t b = 0, d = 0;
+    if (row < a.n) {
+      b = __ldg(a.rp + row);
+      d = __ldg(a.rp + row + 1) - b;
+    }
+    const bool is_hd = d >= a.hd.threshold;
+    const uint32_t dl = is_hd ? 0u : d;
+    uint32_t packed = 0;
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
+    for (uint32_t k = 0; k < dmax; k += 8)
+      if (k + j < dl) packed += __ldg(a.feat + __ldg(a.col + b + k + j));
+    packed += __shfl_xor_sync(0xffffffffu, packed, 1);
+    packed += __shfl_xor_sync(0xffffffffu, packed, 2);
+    packed += __shfl_xor_sync(0xffffffffu, packed, 4);
+    float m[4];
+    if (is_hd) {
+      const float4 mm = ptx::ldg_f4(a.hd.mean + static_cast<size_t>(hd_slot(a.hd, row)) * 4);
+      m[0] = mm.x; m[1] = mm.y; m[2] = mm.z; m[3] = mm.w;
+    } else {
+      const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) m[k] = static_cast<float>((packed >> (8 * k)) & 0xFFu) * inv;
+    }
+    if (row >= a.n) continue;
+    const uint32_t x = __ldg(a.feat + row);
+    float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float xk = static_cast<float>((x >> (8 * k)) & 0xFFu);
+      s1.x = fmaf(xk, ws[k].x, s1.x); s1.y = fmaf(xk, ws[k].y, s1.y);
+      s1.z = fmaf(xk, ws[k].z, s1.z); s1.w = fmaf(xk, ws[k].w, s1.w);
+      s2.x = fmaf(m[k], wn[k].x, s2.x); s2.y = fmaf(m[k], wn[k].y, s2.y);
+      s2.z = fmaf(m[k], wn[k].z, s2.z); s2.w = fmaf(m[k], wn[k].w, s2.w);
+    }
+    float4 z;
+    z.x = fmaxf((s1.x + s2.x) + bias.x, 0.f);
+    z.y = fmaxf((s1.y + s2.y) + bias.y, 0.f);
+    z.z = fmaxf((s1.z + s2.z) + bias.z, 0.f);
+    z.w = fmaxf((s1.w + s2.w) + bias.w, 0.f);
+    *reinterpret_cast<float4*>(a.hout + static_cast<size_t>(row) * kF + 4 * j) = z;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// HD rows: CTA per row, 32 groups of 8 lanes stride the neighbour list; fixed
+// order reduction over groups (deterministic). out row = slot (or row id).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) hd_mean32_kernel(const uint32_t* __restrict__ hd_rows, uint32_t count,
+                                                        const uint32_t* __restrict__ rp,
+                                                        const uint32_t* __restrict__ col,
+                                                        const float* __restrict__ H, float* __restrict__ out,
+                                                        int out_by_row) {
+  __shared__ float red[32][kF + 1];
+  const int gid = threadIdx.x >> 3, j = threadIdx.x & 7;
+  for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
+    const uint32_t r = hd_rows[slot], b = rp[r], d = rp[r + 1] - b;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t e = gid;
+    for (; e + 96 < d; e += 128) {
+      const uint32_t c0 = __ldg(col + b + e), c1 = __ldg(col + b + e + 32);
+      const uint32_t c2 = __ldg(col + b + e + 64), c3 = __ldg(col + b + e + 96);
+      const float4 v0 = ptx::ldg_f4(H + static_cast<size_t>(c0) * kF + 4 * j);
+      const float4 v1 = ptx::ldg_f4(H + static_cast<size_t>(c1) * kF + 4 * j);
+      const float4 v2 = ptx::ldg_f4(H + static_cast<size_t>(c2) * kF + 4 * j);
+      const float4 v3 = ptx::ldg_f4(H + static_cast<size_t>(c3) * kF + 4 * j);
+      acc = f4add(f4add(acc, v0), v1);
+      acc = f4add(f4add(acc, v2), v3);
+    }
+    for (; e < d; e += 32) acc = f4add(acc, ptx::ldg_f4(H + static_cast<size_t>(__ldg(col + b + e)) * kF + 4 * j));
+    red[gid][4 * j] = acc.x;
+    red[gid][4 * j + 1] = acc.y;
+    red[gid][4 * j + 2] = acc.z;
+    red[gid][4 * j + 3] = acc.w;
+    __syncthreads();
+    if (threadIdx.x < kF) {
+      float s = 0.f;
+      for (int q = 0; q < 32; ++q) s += red[q][threadIdx.x];
+      const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
+      out[static_cast<size_t>(out_by_row ? r : slot) * kF + threadIdx.x] = s * inv;
+    }
+    __syncthreads();
+  }
+}
+
+// Layer-0 HD rows: exact integer feature counts, mean = count / deg.
+__global__ void __launch_bounds__(256) hd_mean_feat_kernel(const uint32_t* __restrict__ hd_rows, uint32_t count,
+                                                           const uint32_t* __restrict__ rp,
+                                                           const uint32_t* __restrict__ col,
+                                                           const uint32_t* __restrict__ feat, float* __restrict__ out) {
+  __shared__ uint32_t red[8][4];
+  for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
+    const uint32_t r = hd_rows[slot], b = rp[r], d = rp[r + 1] - b;
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) {
+      const uint32_t x = __ldg(feat + __ldg(col + b + e));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] += (x >> (8 * k)) & 0xFFu;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[threadIdx.x >> 5][k] = c[k];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      uint32_t s = 0;
+      for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+      const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
+      out[static_cast<size_t>(slot) * 4 + threadIdx.x] = static_cast<float>(s) * inv;
+    }
+    __syncthreads();
+  }
+}
+
+// Standalone LD aggregation (groot_spmm_mean, f = 32): the same gather as the
+// fused layer, writing the mean rows (HD rows are written by hd_mean32_kernel).
+__global__ void __launch_bounds__(256) spmm_mean32_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+                                                          const uint32_t* __restrict__ col,
+                                                          const float* __restrict__ H, HdInfo hd,
+                                                          float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; base < n; base += warps * 8) {
+    uint32_t row[2] = {base + g, base + 4 + g};
+    float4 m[2];
+    HdInfo none = hd;
+    gather_mean32<2>(rp, col, H, n, row, j, gbase, none, m);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (row[q] < n) {
+        const uint32_t d = __ldg(rp + row[q] + 1) - __ldg(rp + row[q]);
+        if (d < hd.threshold) *reinterpret_cast<float4*>(out + static_cast<size_t>(row[q]) * kF + 4 * j) = m[q];
+      }
+  }
+}
+
+// General CSR SpMM (spmm::execute over CsrMatrix<float>): 8 lanes per row,
+// columns strided by 8, nonzeros accumulated in order. vals == nullptr -> 1/deg.
+__global__ void __launch_bounds__(256) spmm_generic_kernel(uint32_t rows, const uint32_t* __restrict__ rp,
+                                                           const uint32_t* __restrict__ col,
+                                                           const float* __restrict__ vals,
+                                                           const float* __restrict__ dense, uint32_t f,
+                                                           float* __restrict__ out) {
+  const int j = threadIdx.x & 7;
+  const uint32_t groups = gridDim.x * (blockDim.x >> 3);
+  for (uint32_t r = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); r < rows; r += groups) {
+    const uint32_t b = rp[r], e = rp[r + 1];
+    const float inv = e > b ? 1.0f / static_cast<float>(e - b) : 0.0f;
+    for (uint32_t c = j; c < f; c += 8) {
+      float acc = 0.f;
+      for (uint32_t q = b; q < e; ++q) {
+        const float v = vals ? vals[q] : inv;
+        acc += v * dense[static_cast<size_t>(col[q]) * f + c];
+      }
+      out[static_cast<size_t>(r) * f + c] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Naive reference path (debug / differential tests only): thread per row.
+// ---------------------------------------------------------------------------
+__global__ void naive_layer_kernel(uint32_t n, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                   const float* __restrict__ hin, const uint32_t* __restrict__ feat, uint32_t fin,
+                                   const float* __restrict__ ws, const float* __restrict__ wn,
+                                   const float* __restrict__ b, float* __restrict__ hout) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    float h[32], m[32];
+    for (uint32_t k = 0; k < fin; ++k) {
+      h[k] = hin ? hin[static_cast<size_t>(r) * fin + k] : static_cast<float>((feat[r] >> (8 * k)) & 0xFF);
+      m[k] = 0.f;
+    }
+    const uint32_t d = rp[r + 1] - rp[r];
+    for (uint32_t q = rp[r]; q < rp[r + 1]; ++q) {
+      const uint32_t u = col[q];
+      for (uint32_t k = 0; k < fin; ++k)
+        m[k] += hin ? hin[static_cast<size_t>(u) * fin + k] : static_cast<float>((feat[u] >> (8 * k)) & 0xFF);
+    }
+    const float inv = d ? 1.0f / static_cast<float>(d) : 0.0f;
+    for (uint32_t k = 0; k < fin; ++k) m[k] *= inv;
+    for (uint32_t o = 0; o < 32; ++o) {
+      float s1 = 0.f, s2 = 0.f;
+      for (uint32_t k = 0; k < fin; ++k) {
+        s1 = fmaf(h[k], ws[k * 32 + o], s1);
+        s2 = fmaf(m[k], wn[k * 32 + o], s2);
+      }
+      hout[static_cast<size_t>(r) * 32 + o] = fmaxf((s1 + s2) + b[o], 0.f);
+    }
+  }
+}
+
+__global__ void head_kernel(uint32_t n, const float* __restrict__ h, const float* __restrict__ head, uint32_t C,
+                            uint8_t* __restrict__ cls, float* __restrict__ logits, const uint8_t* __restrict__ labels,
+                            unsigned long long* __restrict__ confusion) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    float best = 0.f;
+    uint32_t arg = 0;
+    for (uint32_t c = 0; c < C; ++c) {
+      float s = 0.f;
+      for (int k = 0; k < 32; ++k) s = fmaf(h[static_cast<size_t>(r) * 32 + k], head[k * C + c], s);
+      s += head[32 * C + c];
+      if (c == 0 || s > best) { best = s; arg = c; }
+      if (logits) logits[static_cast<size_t>(r) * C + c] = s;
+    }
+    cls[r] = static_cast<uint8_t>(arg);
+    if (confusion && labels && labels[r] < 5 && arg < 5) atomicAdd(&confusion[labels[r] * 5 + arg], 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row classifier (K10): rows with degree >= threshold, ascending.
+// ---------------------------------------------------------------------------
+__global__ void hd_flag_kernel(uint32_t n, const uint32_t* __restrict__ rp, uint32_t thr, uint8_t* __restrict__ flag) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    flag[v] = (rp[v + 1] - rp[v]) >= thr;
+}
+
+void classify_rows(groot_graph* g, uint32_t thr) {
+  if (g->hd_threshold == thr && (g->num_hd == 0 || g->hd_rows.p)) return;
+  DevBuf<uint8_t> flag(g->n);
+  DevBuf<uint32_t> out(g->n), cnt(1);
+  if (g->n) GROOT_LAUNCH(hd_flag_kernel, blocks_for(g->n, 256), 256, 0, g->n, g->rp.p, thr, flag.p);
+  size_t bytes = 0;
+  cub::CountingInputIterator<uint32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, bytes, it, flag.p, out.p, cnt.p, g->n, stream());
+  DevBuf<uint8_t> tmp(bytes);
+  GROOT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, flag.p, out.p, cnt.p, g->n, stream()));
+  uint32_t num = 0;
+  cnt.download(&num, 1);
+  stream_sync();
+  g->num_hd = num;
+  g->hd_rows.alloc(num);
+  if (num)
+    GROOT_CUDA(cudaMemcpyAsync(g->hd_rows.p, out.p, num * 4ull, cudaMemcpyDeviceToDevice, stream()));
+  g->hd_mean.alloc(static_cast<size_t>(num) * kF);
+  g->hd_threshold = thr;
+  stream_sync();
+}
+
+static void ensure_activations(groot_graph* g) {
+  const size_t need = static_cast<size_t>(g->n) * kF;
+  for (auto& b : g->act)
+    if (b.n < need) b.alloc(need);
+}
+
+static void set_tc_smem() {
+  static bool done = false;
+  if (done) return;
+  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  done = true;
+}
+
+// Full forward + classify on a resident graph. cls: u8[n] device; logits:
+// f32[n*classes] device or null; confusion: u64[25] device or null.
+void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* logits, unsigned long long* confusion) {
+  require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
+  if (g->n == 0) return;
+  set_tc_smem();
+  classify_rows(g, hd_threshold());
+  ensure_activations(g);
+  const uint32_t n = g->n;
+  HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
+  const unsigned sms = static_cast<unsigned>(num_sms());
+  // layer 0
+  if (g->num_hd)
+    GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
+                 g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
+  Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), m->l0.p, hd, g->act[0].p};
+  GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, 32, sms * 8), 256, 0, l0);
+  const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+  for (uint32_t l = 1; l < m->depth; ++l) {
+    const float* hin = g->act[(l - 1) & 1].p;
+    float* hout = g->act[l & 1].p;
+    if (g->num_hd)
+      GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
+                   g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
+    LayerArgs a{};
+    a.n = n;
+    a.rp = g->rp.p;
+    a.col = g->col.p;
+    a.hin = hin;
+    a.hout = hout;
+    a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
+    a.bias = m->bias.p + static_cast<size_t>(l - 1) * kF;
+    a.hd = hd;
+    a.head = m->head.p;
+    a.classes = m->classes;
+    a.cls = cls;
+    a.logits = logits;
+    a.labels = g->labels.p;
+    a.confusion = confusion;
+    const unsigned grid = std::min<uint32_t>(ntiles, sms);
+    if (l + 1 == m->depth) GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a);
+    else GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a);
+  }
+  if (m->depth == 1)
+    GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, g->act[0].p, m->head.p, m->classes, cls, logits,
+                 g->labels.p, confusion);
+}
+
+// Naive path (tests): same math, thread per row, plain loads.
+void forward_naive_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* logits,
+                          unsigned long long* confusion) {
+  ensure_activations(g);
+  const uint32_t n = g->n;
+  if (n == 0) return;
+  const float* w = m->naive_w.p;
+  uint32_t in = m->in_dim;
+  size_t off = 0;
+  for (uint32_t l = 0; l < m->depth; ++l) {
+    const float* ws = w + off;
+    const float* wn = ws + in * 32;
+    const float* b = wn + in * 32;
+    off += 2 * in * 32 + 32;
+    GROOT_LAUNCH(naive_layer_kernel, blocks_for(n, 128), 128, 0, n, g->rp.p, g->col.p,
+                 l ? g->act[(l - 1) & 1].p : nullptr, reinterpret_cast<const uint32_t*>(g->feat.p), in, ws, wn, b,
+                 g->act[l & 1].p);
+    in = 32;
+  }
+  GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, g->act[(m->depth - 1) & 1].p, m->head.p, m->classes, cls,
+               logits, g->labels.p, confusion);
+}
+
+void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out) {
+  if (g->n == 0) return;
+  if (f == kF) {
+    classify_rows(g, hd_threshold());
+    HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
+    const unsigned sms = static_cast<unsigned>(num_sms());
+    if (g->num_hd)
+      GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
+                   g->rp.p, g->col.p, dense, out, 1);
+    GROOT_LAUNCH(spmm_mean32_kernel, blocks_for(g->n, 64, sms * 8), 256, 0, g->n, g->rp.p, g->col.p, dense, hd, out);
+  } else {
+    GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
+                 nullptr, dense, f, out);
+  }
+}
+
+void spmm_csr_device(uint32_t rows, const uint32_t* rp, const uint32_t* col, const float* vals, const float* dense,
+                     uint32_t f, float* out) {
+  if (rows == 0) return;
+  GROOT_LAUNCH(spmm_generic_kernel, blocks_for(rows, 32, num_sms() * 16), 256, 0, rows, rp, col, vals, dense, f, out);
+}
+
+// Host-side TF32 split (round-to-nearest, ties away — same as cvt.rna.tf32.f32).
+static float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// Build device weights: layer 0 fp32, layers >= 1 as swizzled smem images
+// (B operand K-major: row n = output feature, K = input feature).
+void model_upload(groot_model* m) {
+  const uint32_t D = m->depth, H = m->hidden, C = m->classes, I = m->in_dim;
+  const double* p = m->params.data();
+  std::vector<float> l0(2 * I * H + H);
+  for (size_t i = 0; i < l0.size(); ++i) l0[i] = static_cast<float>(p[i]);
+  m->l0.alloc(l0.size());
+  m->l0.upload(l0.data(), l0.size());
+  // naive path: all layers fp32 row-major, then head
+  std::vector<float> nw;
+  size_t off = 0;
+  uint32_t in = I;
+  std::vector<uint32_t> img(static_cast<size_t>(D > 1 ? D - 1 : 0) * (kBBytes / 4), 0);
+  std::vector<float> bias(static_cast<size_t>(D > 1 ? D - 1 : 0) * H);
+  for (uint32_t l = 0; l < D; ++l) {
+    const double* ws = p + off;
+    const double* wn = ws + in * H;
+    const double* b = wn + in * H;
+    for (uint32_t i = 0; i < 2 * in * H + H; ++i) nw.push_back(static_cast<float>(ws[i]));
+    if (l > 0) {
+      uint8_t* base = reinterpret_cast<uint8_t*>(img.data()) + static_cast<size_t>(l - 1) * kBBytes;
+      for (int kb = 0; kb < 2; ++kb) {
+        const double* W = kb ? wn : ws;
+        for (uint32_t nn = 0; nn < 32; ++nn)
+          for (uint32_t k = 0; k < 32; ++k) {
+            const float v = static_cast<float>(W[k * H + nn]);
+            const float hi = tf32_rna_host(v), lo = v - hi;
+            const uint32_t o = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
+            std::memcpy(base + kb * 8192 + o, &hi, 4);
+            std::memcpy(base + kb * 8192 + 4096 + o, &lo, 4);
+          }
+      }
+      for (uint32_t o = 0; o < H; ++o) bias[(l - 1) * H + o] = static_cast<float>(b[o]);
+    }
+    off += 2 * in * H + H;
+    in = H;
+  }
+  std::vector<float> head(H * C + C);
+  for (uint32_t i = 0; i < H * C + C; ++i) head[i] = static_cast<float>(p[off + i]);
+  m->bimg.alloc(img.size());
+  m->bimg.upload(img.data(), img.size());
+  m->bias.alloc(bias.size());
+  m->bias.upload(bias.data(), bias.size());
+  m->head.alloc(head.size());
+  m->head.upload(head.data(), head.size());
+  m->naive_w.alloc(nw.size());
+  m->naive_w.upload(nw.data(), nw.size());
+  stream_sync();
+}
+
+}  // namespace groot
