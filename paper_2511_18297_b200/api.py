@@ -16,6 +16,8 @@ import numpy as np
 from ._lib import GrootError, GrootInvalidArgument, check, lib, ptr  # noqa: F401
 
 NUM_CLASSES = 5
+
+
 NODE_CLASS = {"PO": 0, "MAJ": 1, "XOR": 2, "AND": 3, "PI": 4}  # inc/circuitgen.hpp:15
 
 
@@ -96,14 +98,17 @@ def write_aiger(aig: Aig) -> str:
 # ---------------------------------------------------------------------------
 class EdaGraph:
     """Learning graph in HBM: symmetric CSR, 4-bit features, labels, fwd_edges."""
+    _FREE = "groot_graph_free"
+
 
     def __init__(self, handle):
         self._h = handle
+        self._free = getattr(lib(), self._FREE)  # bound now: module globals vanish at shutdown
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            lib().groot_graph_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     @property
@@ -210,13 +215,16 @@ def batch(g: EdaGraph, copies: int) -> EdaGraph:
 # partition + regrow (inc/partition.hpp)
 # ---------------------------------------------------------------------------
 class PartitionAssignment:
+    _FREE = "groot_assignment_free"
+
     def __init__(self, handle):
         self._h = handle
+        self._free = getattr(lib(), self._FREE)  # bound now: module globals vanish at shutdown
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            lib().groot_assignment_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     @property
@@ -307,14 +315,17 @@ class AugmentedPartition:
 
 class AugmentedPartitions:
     """vector<AugmentedPartition> living in HBM (result of regrow/core_subgraphs)."""
+    _FREE = "groot_parts_free"
+
 
     def __init__(self, handle):
         self._h = handle
+        self._free = getattr(lib(), self._FREE)  # bound now: module globals vanish at shutdown
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            lib().groot_parts_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     @property
@@ -381,14 +392,17 @@ def param_count(depth=4, in_dim=4, hidden=32, classes=NUM_CLASSES) -> int:
 
 class Model:
     """Model (inc/gnn.hpp:26-33) resident on the device (weights split TF32 hi/lo)."""
+    _FREE = "groot_model_free"
+
 
     def __init__(self, handle):
         self._h = handle
+        self._free = getattr(lib(), self._FREE)  # bound now: module globals vanish at shutdown
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            lib().groot_model_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     @property
