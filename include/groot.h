@@ -56,6 +56,14 @@ int groot_device_synchronize(void);
 /* Counter of kernels the library launched since the last reset (bench evidence). */
 uint64_t groot_kernel_launches(void);
 void groot_reset_kernel_launches(void);
+/* Per-kernel CUDA-event timing on the library stream. enable(1) clears and
+ * starts recording; read() returns, per kernel name, the summed milliseconds
+ * and launch count (names: max entries of 48 chars each). */
+int groot_profile_enable(int on);
+int groot_profile_read(uint32_t max, char* names, double* total_ms, uint64_t* launches,
+                       uint32_t* count);
+/* Release cached device blocks held by the library's caching allocator. */
+int groot_empty_cache(void);
 
 /* ---- AIG sources (host; input side of the path) --------------------------
  * gen_csa_multiplier (src/circuitgen.cpp:66-133): deterministic CSA array.

@@ -75,6 +75,7 @@ def _declare(L):
         "ref_plan_execute": (i32, [P, u32, P, P, P, P, u32, P, C.c_uint]),
         "ref_plan_free": (None, [P]),
         "ref_predict_full": (i32, [P, u32, u32, u32, u32, P, P, P, P, P]),
+        "ref_predict_parts": (i32, [P, P, u32, u32, u32, u32, u32, u32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -245,6 +246,15 @@ def predict_full(g: RefGraph, params, depth=4, in_dim=4, hidden=32, classes=5, w
     if st != 0:
         raise ValueError(_err())
     return pred, conf, acc.value, lg
+
+
+def predict_parts(parts: RefParts, first: int, count: int, params, pred=None, depth=4, in_dim=4, hidden=32,
+                  classes=5):
+    """predict (src/gnn.cpp:280-291) over parts [first, first+count), parts in parallel."""
+    st = lib().ref_predict_parts(parts.g.h, parts.h, first, count, depth, in_dim, hidden, classes,
+                                 ptr(np.ascontiguousarray(params, np.float64)), ptr(pred))
+    if st != 0:
+        raise ValueError(_err())
 
 
 def default_workers() -> int:

@@ -316,4 +316,67 @@ int ref_predict_full(const ref_graph* g, uint32_t depth, uint32_t in_dim, uint32
   });
 }
 
+// predict (src/gnn.cpp:280-291) over parts [first, first+count): default_pool()
+// runs one part per item (the nested SpMM then runs inline, src/worker_pool.cpp:55-60),
+// each part = forward(materialize(g, part)) with the restated dense product,
+// scored on core rows. pred (global, n entries) receives the core labels.
+int ref_predict_parts(const ref_graph* g, const ref_parts* h, uint32_t first, uint32_t count,
+                      uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                      const double* prm, uint8_t* pred) {
+  return guarded([&] {
+    if (first + count > h->parts.size()) throw std::invalid_argument("ref_predict_parts: range");
+    default_pool().for_each(count, [&](std::size_t i) {
+      const AugmentedPartition& part = h->parts[first + i];
+      const EdaGraph e = materialize(g->g, part);
+      const uint32_t n = e.n;
+      spmm::CsrMatrix<double> a;
+      a.rows = a.cols = n;
+      a.row_ptr = e.row_ptr;
+      a.col_idx = e.col_idx;
+      a.values.resize(e.col_idx.size());
+      for (uint32_t v = 0; v < n; ++v) {
+        const double inv = e.degree[v] > 0 ? 1.0 / e.degree[v] : 0.0;
+        for (uint64_t q = e.row_ptr[v]; q < e.row_ptr[v + 1]; ++q) a.values[q] = inv;
+      }
+      const spmm::SpmmPlan plan = spmm::build_plan(a, 0);
+      std::vector<double> x(static_cast<size_t>(n) * in_dim);
+      for (size_t k = 0; k < x.size(); ++k) x[k] = e.features[k];
+      uint32_t in = in_dim;
+      const double* q = prm;
+      for (uint32_t l = 0; l < depth; ++l) {
+        const double* ws = q;
+        const double* wn = q + in * hidden;
+        const double* b = q + 2 * in * hidden;
+        q += 2 * in * hidden + hidden;
+        std::vector<double> m(static_cast<size_t>(n) * in);
+        spmm::execute(plan, a, x.data(), in, m.data(), &default_pool());  // nested: runs inline
+        std::vector<double> hn(static_cast<size_t>(n) * hidden);
+        for (uint32_t r = 0; r < n; ++r)
+          for (uint32_t j = 0; j < hidden; ++j) {
+            double s1 = 0.0, s2 = 0.0;
+            for (uint32_t k = 0; k < in; ++k) s1 += x[static_cast<size_t>(r) * in + k] * ws[k * hidden + j];
+            for (uint32_t k = 0; k < in; ++k) s2 += m[static_cast<size_t>(r) * in + k] * wn[k * hidden + j];
+            const double z = (s1 + s2) + b[j];
+            hn[static_cast<size_t>(r) * hidden + j] = z > 0.0 ? z : 0.0;
+          }
+        x.swap(hn);
+        in = hidden;
+      }
+      const double* wo = q;
+      const double* bo = q + in * classes;
+      for (uint32_t r = 0; r < part.num_core(); ++r) {
+        uint32_t arg = 0;
+        double best = 0.0;
+        for (uint32_t c = 0; c < classes; ++c) {
+          double s = 0.0;
+          for (uint32_t k = 0; k < in; ++k) s += x[static_cast<size_t>(r) * in + k] * wo[k * classes + c];
+          s += bo[c];
+          if (c == 0 || s > best) { best = s; arg = c; }
+        }
+        if (pred) pred[part.core_nodes[r]] = static_cast<uint8_t>(arg);
+      }
+    });
+  });
+}
+
 }  // extern "C"

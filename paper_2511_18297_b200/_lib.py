@@ -37,6 +37,9 @@ _SIG = {
     "groot_device_synchronize": (i32, []),
     "groot_kernel_launches": (u64, []),
     "groot_reset_kernel_launches": (None, []),
+    "groot_profile_enable": (i32, [i32]),
+    "groot_profile_read": (i32, [u32, P, P, P, P]),
+    "groot_empty_cache": (i32, []),
     "groot_csa_sizes": (i32, [u32, P, P, P]),
     "groot_gen_csa": (i32, [u32, P, P, P]),
     "groot_aiger_sizes": (i32, [C.c_char_p, C.c_size_t, P, P, P]),

@@ -69,6 +69,20 @@ int guarded(F&& f) {
 }
 int num_sms();
 
+// Caching device allocator (like torch's): blocks are rounded to size
+// classes and recycled, so per-call temporaries (CUB scratch, CSR counters,
+// activations of a re-encoded graph) cost no cudaMalloc/cudaFree after warm-up.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+void dev_empty_cache();
+
+// Per-kernel CUDA-event timing on the library stream (groot_profile_*).
+struct ProfScope {
+  int slot = -1;
+  explicit ProfScope(const char* name);
+  ~ProfScope();
+};
+
 // Owning device buffer.
 template <class T>
 struct DevBuf {
@@ -87,10 +101,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) GROOT_CUDA(cudaMalloc(&p, count * sizeof(T) + 16));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T) + 16));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }

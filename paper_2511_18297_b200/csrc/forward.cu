@@ -632,18 +632,25 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
   HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
   const unsigned sms = static_cast<unsigned>(num_sms());
   // layer 0
-  if (g->num_hd)
+  if (g->num_hd) {
+    ProfScope ps("hd_mean_feat");
     GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                  g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
+  }
   Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), m->l0.p, hd, g->act[0].p};
-  GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, 32, sms * 8), 256, 0, l0);
+  {
+    ProfScope ps("sage_layer0");
+    GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, 32, sms * 8), 256, 0, l0);
+  }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   for (uint32_t l = 1; l < m->depth; ++l) {
     const float* hin = g->act[(l - 1) & 1].p;
     float* hout = g->act[l & 1].p;
-    if (g->num_hd)
+    if (g->num_hd) {
+      ProfScope ps("hd_mean32");
       GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
+    }
     LayerArgs a{};
     a.n = n;
     a.rp = g->rp.p;
@@ -660,8 +667,13 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     a.labels = g->labels.p;
     a.confusion = confusion;
     const unsigned grid = std::min<uint32_t>(ntiles, sms);
-    if (l + 1 == m->depth) GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a);
-    else GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a);
+    if (l + 1 == m->depth) {
+      ProfScope ps("sage_layer_tc_last");
+      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a);
+    } else {
+      ProfScope ps("sage_layer_tc");
+      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a);
+    }
   }
   if (m->depth == 1)
     GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, g->act[0].p, m->head.p, m->classes, cls, logits,
@@ -697,9 +709,12 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
     classify_rows(g, hd_threshold());
     HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
     const unsigned sms = static_cast<unsigned>(num_sms());
-    if (g->num_hd)
+    if (g->num_hd) {
+      ProfScope ps("spmm_hd_mean32");
       GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, dense, out, 1);
+    }
+    ProfScope ps("spmm_mean32");
     GROOT_LAUNCH(spmm_mean32_kernel, blocks_for(g->n, 64, sms * 8), 256, 0, g->n, g->rp.p, g->col.p, dense, hd, out);
   } else {
     GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
