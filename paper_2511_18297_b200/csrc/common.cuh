@@ -171,8 +171,10 @@ struct groot_model {
   uint32_t depth = 0, in_dim = 0, hidden = 0, classes = 0;
   std::vector<double> params;       // fp64, ASG1 order (host copy)
   groot::DevBuf<float> l0;          // layer 0: Ws[4x32], Wn[4x32], b[32]
+  float l0w[4 * 32 * 2 + 32];       // same, passed by value as kernel parameters
   groot::DevBuf<uint32_t> bimg;     // layers >= 1: 16 KB smem image each (B hi/lo, swizzled)
   groot::DevBuf<float> bias;        // layers >= 1: 32 each
   groot::DevBuf<float> naive_w;     // fp32 row-major weights for the naive debug path
   groot::DevBuf<float> head;        // W_out[32 x classes] then b_out[classes]
+  float headw[32 * 8 + 8];          // same, classes padded to 8, passed as kernel parameters
 };

@@ -23,19 +23,23 @@ namespace groot {
 
 constexpr int kF = 32;                       // hidden width (tensor-core layers)
 constexpr int kTileM = 128;                  // rows per MMA tile (UMMA M)
-constexpr int kEpiWarps = 4;                 // warps 0..3: TMEM lane quadrants
-constexpr int kProdWarps = 8;                // warps 4..11: gather producers
-constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 12: TMEM alloc + MMA issue
-constexpr int kThreads = (kMmaWarp + 1) * 32;     // 416
-constexpr int kStages = 2;
+constexpr int kEpiWarps = 4;                 // warps 0..3: TMEM lane quadrants; warp 0 lane 0 issues MMA
+constexpr int kProdWarps = 16;               // warps 4..19: gather producers (8 rows each)
+// 20 warps = 5 per SM sub-partition: 5 x 96 regs x 32 lanes fits one sub-partition's
+// 16K registers (a 21st warp would force the cap down to 80 registers).
+constexpr int kThreads = (kEpiWarps + kProdWarps) * 32;  // 640
+constexpr int kStages = 3;
 constexpr uint32_t kTileBytes = kTileM * 128;     // 128 rows x 32 fp32
 constexpr uint32_t kStageBytes = 4 * kTileBytes;  // h_hi, h_lo, m_hi, m_lo
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
 constexpr int kMaxClasses = 8;
 constexpr uint32_t kTmemCols = 64;                // two 32-column fp32 accumulators
+constexpr uint32_t kPrefetchWaves = 3;            // L2 prefetch distance (in waves of gridDim tiles)
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBBytes + kEpiBytes +
-                                (kF * kMaxClasses + kMaxClasses + kF) * 4 + 8 * 8 + 4 + 25 * 4 + 1024;
+                                (kF * kMaxClasses + kMaxClasses + kF) * 4 + 16 * 8 + 4 + 25 * 4 + 4 * kStages +
+                                1024;
+static_assert(kSmemBytes <= 232448, "fused layer exceeds the 227 KB shared-memory limit");
 
 uint32_t hd_threshold() {
   static uint32_t t = [] {
@@ -152,6 +156,13 @@ __device__ __forceinline__ void store_split(uint8_t* hi_base, uint32_t i, int j,
   *reinterpret_cast<float4*>(hi_base + kTileBytes + off) = l;
 }
 
+// Head weights by value: kernel parameters live in the constant bank, so the
+// 32 x classes FFMAs of the last epilogue read them as free operands.
+struct HeadW {
+  float w[32][8];  // W_out[k][c], classes padded to 8
+  float b[8];
+};
+
 struct LayerArgs {
   uint32_t n;
   const uint32_t* rp;
@@ -170,33 +181,33 @@ struct LayerArgs {
 };
 
 template <bool kLast>
-__global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+__global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the SWIZZLE_128B operand tiles, computed on the shared
+  // address so the pointer stays in the shared window (STS, not generic ST).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * kStageBytes;
   uint8_t* sE = sB + kBBytes;
   float* sHead = reinterpret_cast<float*>(sE + kEpiBytes);
   float* sBias = sHead + kF * kMaxClasses + kMaxClasses;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + kF);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  uint64_t* tfull = bars + 4;
-  uint64_t* tempty = bars + 6;
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* full = bars;                 // [kStages] producers -> MMA
+  uint64_t* empty = bars + kStages;      // [kStages] MMA done reading the stage
+  uint64_t* tfull = bars + 2 * kStages;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained by the epilogue
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* sConf = sTmem + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n = a.n;
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+  const uint32_t G = gridDim.x;
 
   for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
   if (threadIdx.x < kF) sBias[threadIdx.x] = a.bias[threadIdx.x];
-  if (kLast) {
-    for (uint32_t i = threadIdx.x; i < kF * a.classes + a.classes; i += kThreads) sHead[i] = a.head[i];
-    if (threadIdx.x < 25) sConf[threadIdx.x] = 0;
-  }
+  if (kLast && threadIdx.x < 25) sConf[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], kProdWarps * 32);
@@ -208,80 +219,176 @@ __global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerA
     }
     ptx::mbar_fence_init();
   }
-  if (warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
+  if (warp == 0) ptx::tmem_alloc<kTmemCols>(sTmem);
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *sTmem;
 
-  if (warp >= kEpiWarps && warp < kMmaWarp) {
+  // tcgen05.mma issue for tile `it` (one thread): 3xTF32 [h|m] x [Ws;Wn] into TMEM.
+  constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
+  const uint32_t a0 = ptx::smem_addr(sA), b0s = ptx::smem_addr(sB);
+  auto issue_mma = [&](uint32_t it) {
+    const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+    const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+    ptx::mbar_wait(&full[s], ph);
+    ptx::mbar_wait(&tempty[acc], aph ^ 1);
+    ptx::tc_fence_after();
+    const uint32_t d = tmem_base + acc * kF;
+#pragma unroll
+    for (uint32_t kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (uint32_t kk = 0; kk < 4; ++kk) {
+        const uint32_t ao = a0 + s * kStageBytes + kb * 2 * kTileBytes + kk * 32;
+        const uint32_t bo = b0s + kb * 8192 + kk * 32;
+        const uint64_t ahi = ptx::umma_desc_sw128(ao), alo = ptx::umma_desc_sw128(ao + kTileBytes);
+        const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
+        ptx::mma_tf32(d, ahi, bhi, idesc, (kb | kk) != 0);
+        ptx::mma_tf32(d, ahi, blo, idesc, 1);
+        ptx::mma_tf32(d, alo, bhi, idesc, 1);
+      }
+    ptx::mma_commit(&empty[s]);
+    ptx::mma_commit(&tfull[acc]);
+  };
+
+  if (warp >= kEpiWarps) {
     // ===== gather producers =====
+    // 16 warps x 8 rows = one 128-row tile per pass. Rolling index pipeline:
+    // while the feature gathers of tile t are in flight, col_idx of tile t+G
+    // and row_ptr of tile t+2G are loaded, so a tile costs one memory round
+    // trip instead of three (row_ptr -> col_idx -> features).
     const int pw = warp - kEpiWarps;
     const int g = lane >> 3, j = lane & 7, gbase = lane & 24;
+    const uint32_t thr = a.hd.threshold;
+    uint32_t li[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) li[q] = pw * 8 + q * 4 + g;
+    auto rp_load = [&](uint32_t tt, uint32_t (&b)[2], uint32_t (&e)[2]) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t r = tt * kTileM + li[q];
+        const bool ok = tt < ntiles && r < n;
+        b[q] = ok ? __ldg(a.rp + r) : 0u;
+        e[q] = ok ? __ldg(a.rp + r + 1) : 0u;
+      }
+    };
+    auto col_load = [&](const uint32_t (&b)[2], const uint32_t (&d)[2], uint32_t (&c)[2]) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        c[q] = (static_cast<uint32_t>(j) < d[q] && d[q] < thr) ? __ldg(a.col + b[q] + j) : 0u;
+    };
+    uint32_t b0[2], d0[2], c0[2], b1[2], e1[2];
+    {
+      uint32_t e0[2];
+      rp_load(blockIdx.x, b0, e0);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) d0[q] = e0[q] - b0[q];
+      col_load(b0, d0, c0);
+      rp_load(blockIdx.x + G, b1, e1);
+    }
+    constexpr int U = 4;  // neighbours per row in the first burst (CSA LD rows have degree <= 4)
     uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+      if (pw == 0 && lane == 0) {
+        // L2 prefetch of the feature rows PF waves ahead: the fanout rows this
+        // wave gathers are first touched there, so they then hit L2, not DRAM.
+        const uint32_t tp = t + kPrefetchWaves * G;
+        if (tp < ntiles) {
+          const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - tp * kTileM);
+          ptx::prefetch_l2(a.hin + static_cast<size_t>(tp) * kTileM * kF, rows * 128u);
+        }
+      }
+      uint32_t dl[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) dl[q] = d0[q] < thr ? d0[q] : 0u;
+      // burst: U neighbour chunks + the self chunk per row, all independent.
+      float4 v[2][U], hs[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t r = t * kTileM + li[q];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const uint32_t ci = __shfl_sync(0xffffffffu, c0[q], gbase + k);
+          if (static_cast<uint32_t>(k) < dl[q]) v[q][k] = ptx::ldg_f4(a.hin + static_cast<size_t>(ci) * kF + 4 * j);
+        }
+        hs[q] = r < n ? ptx::ldg_f4(a.hin + static_cast<size_t>(r) * kF + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // index prefetch for the next two tiles (in flight with the burst)
+      uint32_t d1[2], c1[2], b2[2], e2[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) d1[q] = e1[q] - b1[q];
+      col_load(b1, d1, c1);
+      rp_load(t + 2 * G, b2, e2);
+      // consume in nonzero order (predicated adds: no selects, no moves)
+      float4 m[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        m[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (static_cast<uint32_t>(k) < dl[q]) m[q] = f4add(m[q], v[q][k]);
+      }
+      const uint32_t dmax = __reduce_max_sync(0xffffffffu, max(dl[0], dl[1]));
+      if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
+        for (uint32_t k0 = 0; k0 < dmax; k0 += 8) {
+          uint32_t cc[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            cc[q] = k0 == 0 ? c0[q] : ((k0 + j < dl[q]) ? __ldg(a.col + b0[q] + k0 + j) : 0u);
+          for (uint32_t kk = (k0 == 0 ? U : 0); kk < 8; ++kk) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t ci = __shfl_sync(0xffffffffu, cc[q], gbase + kk);
+              if (k0 + kk < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(a.hin + static_cast<size_t>(ci) * kF + 4 * j));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (d0[q] >= thr) {
+          m[q] = ptx::ldg_f4(a.hd.mean + static_cast<size_t>(hd_slot(a.hd, t * kTileM + li[q])) * kF + 4 * j);
+        } else {
+          const float inv = d0[q] > 0 ? 1.0f / static_cast<float>(d0[q]) : 0.0f;
+          m[q] = f4scale(m[q], inv);
+        }
+      }
       ptx::mbar_wait(&empty[s], ph ^ 1);
       uint8_t* st = sA + s * kStageBytes;
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {
-        uint32_t li[2], row[2];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          li[q] = pw * 16 + pass * 8 + q * 4 + g;
-          row[q] = t * kTileM + li[q];
-        }
-        float4 m[2];
-        gather_mean32<2>(a.rp, a.col, a.hin, n, row, j, gbase, a.hd, m);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float4 h = row[q] < n ? ptx::ldg_f4(a.hin + static_cast<size_t>(row[q]) * kF + 4 * j)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-          store_split(st, li[q], j, h);                       // K block 0: self features
-          store_split(st + 2 * kTileBytes, li[q], j, m[q]);   // K block 1: neighbour mean
-        }
+      for (int q = 0; q < 2; ++q) {
+        store_split(st, li[q], j, hs[q]);                  // K block 0: self features
+        store_split(st + 2 * kTileBytes, li[q], j, m[q]);  // K block 1: neighbour mean
       }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
-    }
-  } else if (warp == kMmaWarp) {
-    // ===== MMA issuer (one thread) =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
-      const uint32_t a0 = ptx::smem_addr(sA), b0 = ptx::smem_addr(sB);
-      uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-        const uint32_t acc = it & 1, aph = (it >> 1) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        ptx::mbar_wait(&tempty[acc], aph ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d = tmem_base + acc * kF;
 #pragma unroll
-        for (uint32_t kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (uint32_t kk = 0; kk < 4; ++kk) {
-            const uint32_t ao = a0 + s * kStageBytes + kb * 2 * kTileBytes + kk * 32;
-            const uint32_t bo = b0 + kb * 8192 + kk * 32;
-            const uint64_t ahi = ptx::umma_desc_sw128(ao), alo = ptx::umma_desc_sw128(ao + kTileBytes);
-            const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
-            ptx::mma_tf32(d, ahi, bhi, idesc, (kb | kk) != 0);
-            ptx::mma_tf32(d, ahi, blo, idesc, 1);
-            ptx::mma_tf32(d, alo, bhi, idesc, 1);
-          }
-        ptx::mma_commit(&empty[s]);
-        ptx::mma_commit(&tfull[acc]);
+      for (int q = 0; q < 2; ++q) {
+        b0[q] = b1[q];
+        d0[q] = d1[q];
+        c0[q] = c1[q];
+        b1[q] = b2[q];
+        e1[q] = e2[q];
       }
     }
-    __syncwarp();
   } else {
-    // ===== epilogue: TMEM -> registers -> bias/ReLU -> store (or head + argmax) =====
-    const uint32_t q = warp;  // lanes 32q..32q+31 of TMEM
+    // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
+    const uint32_t q = warp;
     uint8_t* ew = sE + q * 4096;
-    uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const uint32_t acc = it & 1, ph = (it >> 1) & 1;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    // Warp 0 lane 0 issues the MMAs one tile ahead of its epilogue: iteration
+    // it issues MMA(it), then every epilogue warp drains tile it-1.
+    for (uint32_t it = 0; it <= my_tiles; ++it) {
+      if (warp == 0) {
+        if (lane == 0 && it < my_tiles) issue_mma(it);
+        __syncwarp();
+      }
+      if (it == 0) continue;
+      const uint32_t e = it - 1;
+      const uint32_t t = blockIdx.x + e * G;
+      const uint32_t acc = e & 1, ph = (e >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], ph);
       ptx::tc_fence_after();
       float r[32];
@@ -305,67 +412,65 @@ __global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerA
         }
         __syncwarp();
       } else {
+        // head 32 -> classes (weights in the constant bank), first-max argmax
         const uint32_t row = row0 + lane;
-        const uint32_t C = a.classes;
         float best = 0.f;
         uint32_t arg = 0;
-        for (uint32_t c = 0; c < C; ++c) {
-          float s = 0.f;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) s = fmaf(r[k], sHead[k * C + c], s);
-          s += sHead[kF * C + c];
-          if (c == 0 || s > best) { best = s; arg = c; }
-          if (a.logits && row < n) a.logits[static_cast<size_t>(row) * C + c] = s;
-        }
-        if (row < n) {
-          a.cls[row] = static_cast<uint8_t>(arg);
-          if (a.confusion && a.labels) {
-            const uint32_t tr = a.labels[row];
-            if (tr < 5 && arg < 5) atomicAdd(&sConf[tr * 5 + arg], 1u);
+        for (int c = 0; c < kMaxClasses; ++c) {
+          if (c < static_cast<int>(a.classes)) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) s = fmaf(r[k], hw.w[k][c], s);
+            s += hw.b[c];
+            if (c == 0 || s > best) { best = s; arg = c; }
+            if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + c] = s;
           }
         }
+        if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
       }
     }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (kLast && a.confusion && threadIdx.x < 25 && sConf[threadIdx.x])
-    atomicAdd(&a.confusion[threadIdx.x], static_cast<unsigned long long>(sConf[threadIdx.x]));
-  if (warp == kMmaWarp) {
+  if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
 // ---------------------------------------------------------------------------
-// Layer 0: 4 -> 32 from u8 features (one u32 word per node). 8 lanes per row,
-// lane j computes outputs 4j..4j+3. Neighbour feature words are summed as
-// packed byte counters (exact: LD degree < 256), so the mean is exact up to
-// the final 1/deg scaling.
+// Layer 0: 4 -> 32 from u8 features (one u32 word per node), thread per row:
+// each neighbour costs a 4-byte gather, so one thread owns a row and a warp
+// has 32 rows' gathers in flight. Neighbour feature words are summed as packed
+// byte counters (exact for LD degree < 256); weights are kernel parameters
+// (constant bank: free FFMA operands). The 32 outputs of a row are staged in
+// shared memory so each warp store writes four full 128-byte rows.
 // ---------------------------------------------------------------------------
+struct Layer0W {
+  float ws[4][kF], wn[4][kF], b[kF];
+};
+
 struct Layer0Args {
   uint32_t n;
   const uint32_t* rp;
   const uint32_t* col;
   const uint32_t* feat;
-  const float* w;  // Ws[4][32], Wn[4][32], b[32]
-  HdInfo hd;       // mean width 4
+  HdInfo hd;  // mean width 4
   float* hout;
 };
 
-__global__ void __launch_bounds__(256) sage_layer0_kernel(const Layer0Args a) {
-  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
-  float4 ws[4], wn[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    ws[k] = ptx::ldg_f4(a.w + k * 32 + 4 * j);
-    wn[k] = ptx::ldg_f4(a.w + 128 + k * 32 + 4 * j);
-  }
-  const float4 bias = ptx::ldg_f4(a.w + 256 + 4 * j);
+constexpr int kL0Threads = 256;
+constexpr int kL0Stride = 36;  // floats per staged row (144 B: conflict-free 16-B phases)
+
+__global__ void __launch_bounds__(kL0Threads) sage_layer0_kernel(const Layer0Args a, const Layer0W w) {
+  __shared__ __align__(16) float stage[kL0Threads / 32][32 * kL0Stride];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* sw = stage[wid];
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; base < a.n; base += warps * 4) {
-    const uint32_t row = base + g;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + wid) * 32; base < a.n; base += warps * 32) {
+    const uint32_t row = base + lane;
     uint32_t b = 0, d = 0;
     if (row < a.n) {
       b = __ldg(a.rp + row);
@@ -374,12 +479,17 @@ __global__ void __launch_bounds__(256) sage_layer0_kernel(const Layer0Args a) {
     const bool is_hd = d >= a.hd.threshold;
     const uint32_t dl = is_hd ? 0u : d;
     uint32_t packed = 0;
-    const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
-    for (uint32_t k = 0; k < dmax; k += 8)
-      if (k + j < dl) packed += __ldg(a.feat + __ldg(a.col + b + k + j));
-    packed += __shfl_xor_sync(0xffffffffu, packed, 1);
-    packed += __shfl_xor_sync(0xffffffffu, packed, 2);
-    packed += __shfl_xor_sync(0xffffffffu, packed, 4);
+    {
+      uint32_t c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = (static_cast<uint32_t>(k) < dl) ? __ldg(a.col + b + k) : 0u;
+      uint32_t f[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = (static_cast<uint32_t>(k) < dl) ? __ldg(a.feat + c[k]) : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) packed += f[k];
+      for (uint32_t k = 8; k < dl; ++k) packed += __ldg(a.feat + __ldg(a.col + b + k));
+    }
     float m[4];
     if (is_hd) {
       const float4 mm = ptx::ldg_f4(a.hd.mean + static_cast<size_t>(hd_slot(a.hd, row)) * 4);
@@ -389,23 +499,34 @@ __global__ void __launch_bounds__(256) sage_layer0_kernel(const Layer0Args a) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) m[k] = static_cast<float>((packed >> (8 * k)) & 0xFFu) * inv;
     }
-    if (row >= a.n) continue;
-    const uint32_t x = __ldg(a.feat + row);
-    float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1;
+    const uint32_t x = row < a.n ? __ldg(a.feat + row) : 0u;
+    float xk[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float xk = static_cast<float>((x >> (8 * k)) & 0xFFu);
-      s1.x = fmaf(xk, ws[k].x, s1.x); s1.y = fmaf(xk, ws[k].y, s1.y);
-      s1.z = fmaf(xk, ws[k].z, s1.z); s1.w = fmaf(xk, ws[k].w, s1.w);
-      s2.x = fmaf(m[k], wn[k].x, s2.x); s2.y = fmaf(m[k], wn[k].y, s2.y);
-      s2.z = fmaf(m[k], wn[k].z, s2.z); s2.w = fmaf(m[k], wn[k].w, s2.w);
+    for (int k = 0; k < 4; ++k) xk[k] = static_cast<float>((x >> (8 * k)) & 0xFFu);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      float z[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int o = 4 * c4 + i;
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          s1 = fmaf(xk[k], w.ws[k][o], s1);
+          s2 = fmaf(m[k], w.wn[k][o], s2);
+        }
+        z[i] = fmaxf((s1 + s2) + w.b[o], 0.f);
+      }
+      *reinterpret_cast<float4*>(sw + lane * kL0Stride + 4 * c4) = make_float4(z[0], z[1], z[2], z[3]);
     }
-    float4 z;
-    z.x = fmaxf((s1.x + s2.x) + bias.x, 0.f);
-    z.y = fmaxf((s1.y + s2.y) + bias.y, 0.f);
-    z.z = fmaxf((s1.z + s2.z) + bias.z, 0.f);
-    z.w = fmaxf((s1.w + s2.w) + bias.w, 0.f);
-    *reinterpret_cast<float4*>(a.hout + static_cast<size_t>(row) * kF + 4 * j) = z;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t ri = k * 4 + (lane >> 3), c = lane & 7;
+      const float4 v = *reinterpret_cast<const float4*>(sw + ri * kL0Stride + 4 * c);
+      if (base + ri < a.n) *reinterpret_cast<float4*>(a.hout + static_cast<size_t>(base + ri) * kF + 4 * c) = v;
+    }
+    __syncwarp();
   }
 }
 
@@ -576,6 +697,30 @@ __global__ void head_kernel(uint32_t n, const float* __restrict__ h, const float
   }
 }
 
+// confusion[truth][pred] (finish_prediction, src/gnn.cpp:268-276): block
+// histogram with warp-aggregated shared atomics, one global add per bin.
+__global__ void __launch_bounds__(256) confusion_kernel(uint32_t n, const uint8_t* __restrict__ cls,
+                                                        const uint8_t* __restrict__ labels,
+                                                        unsigned long long* __restrict__ conf) {
+  __shared__ uint32_t h[25];
+  if (threadIdx.x < 25) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint32_t i = base + lane;
+    uint32_t key = 0xFFFFFFFFu;
+    if (i < n) {
+      const uint32_t p = cls[i], t = labels[i];
+      if (p < 5 && t < 5) key = t * 5 + p;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (key != 0xFFFFFFFFu && (__ffs(peers) - 1) == lane) atomicAdd(&h[key], __popc(peers));
+  }
+  __syncthreads();
+  if (threadIdx.x < 25 && h[threadIdx.x]) atomicAdd(&conf[threadIdx.x], static_cast<unsigned long long>(h[threadIdx.x]));
+}
+
 // ---------------------------------------------------------------------------
 // Row classifier (K10): rows with degree >= threshold, ascending.
 // ---------------------------------------------------------------------------
@@ -637,10 +782,11 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                  g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
   }
-  Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), m->l0.p, hd, g->act[0].p};
+  Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), hd, g->act[0].p};
   {
     ProfScope ps("sage_layer0");
-    GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, 32, sms * 8), 256, 0, l0);
+    GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, kL0Threads, sms * 8), kL0Threads, 0, l0,
+                 *reinterpret_cast<const Layer0W*>(m->l0w));
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   for (uint32_t l = 1; l < m->depth; ++l) {
@@ -669,15 +815,21 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     const unsigned grid = std::min<uint32_t>(ntiles, sms);
     if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a);
+      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a,
+                   *reinterpret_cast<const HeadW*>(m->headw));
     } else {
       ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a);
+      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a,
+                   *reinterpret_cast<const HeadW*>(m->headw));
     }
   }
   if (m->depth == 1)
     GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, g->act[0].p, m->head.p, m->classes, cls, logits,
-                 g->labels.p, confusion);
+                 g->labels.p, nullptr);
+  if (confusion) {
+    ProfScope ps("confusion");
+    GROOT_LAUNCH(confusion_kernel, blocks_for(n, 256, sms * 8), 256, 0, n, cls, g->labels.p, confusion);
+  }
 }
 
 // Naive path (tests): same math, thread per row, plain loads.
@@ -745,6 +897,8 @@ void model_upload(groot_model* m) {
   const double* p = m->params.data();
   std::vector<float> l0(2 * I * H + H);
   for (size_t i = 0; i < l0.size(); ++i) l0[i] = static_cast<float>(p[i]);
+  static_assert(sizeof(Layer0W) == sizeof(m->l0w), "layer-0 parameter block");
+  std::memcpy(m->l0w, l0.data(), sizeof(m->l0w));
   m->l0.alloc(l0.size());
   m->l0.upload(l0.data(), l0.size());
   // naive path: all layers fp32 row-major, then head
@@ -778,6 +932,12 @@ void model_upload(groot_model* m) {
   }
   std::vector<float> head(H * C + C);
   for (uint32_t i = 0; i < H * C + C; ++i) head[i] = static_cast<float>(p[off + i]);
+  static_assert(sizeof(HeadW) == sizeof(m->headw), "head parameter block");
+  HeadW hw{};
+  for (uint32_t k = 0; k < H; ++k)
+    for (uint32_t c = 0; c < C; ++c) hw.w[k][c] = head[k * C + c];
+  for (uint32_t c = 0; c < C; ++c) hw.b[c] = head[H * C + c];
+  std::memcpy(m->headw, &hw, sizeof(hw));
   m->bimg.alloc(img.size());
   m->bimg.upload(img.data(), img.size());
   m->bias.alloc(bias.size());

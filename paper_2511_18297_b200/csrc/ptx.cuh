@@ -114,6 +114,11 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&r)[32
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// TMA bulk prefetch of a contiguous global range into L2 (no smem, no registers).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ---- conversions / loads --------------------------------------------------------
 // Round-to-nearest (ties away) fp32 -> tf32 (low 13 mantissa bits cleared).
 __device__ __forceinline__ float tf32_rna(float x) {
