@@ -35,11 +35,15 @@ constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo
 constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
 constexpr int kMaxClasses = 8;
 constexpr uint32_t kTmemCols = 64;                // two 32-column fp32 accumulators
-constexpr uint32_t kPrefetchWaves = 3;            // L2 prefetch distance (in waves of gridDim tiles)
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBBytes + kEpiBytes +
                                 (kF * kMaxClasses + kMaxClasses + kF) * 4 + 16 * 8 + 4 + 25 * 4 + 4 * kStages +
                                 1024;
 static_assert(kSmemBytes <= 232448, "fused layer exceeds the 227 KB shared-memory limit");
+
+static uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : dflt;
+}
 
 uint32_t hd_threshold() {
   static uint32_t t = [] {
@@ -174,6 +178,8 @@ struct LayerArgs {
   HdInfo hd;
   const float* head;     // W_out [32 x classes] row-major, then b_out
   uint32_t classes;
+  uint32_t pf_waves;     // L2 prefetch distance in waves (0 = off)
+  int evict_first_out;   // store hout with an L2 evict-first policy
   uint8_t* cls;          // last layer: n classes
   float* logits;         // last layer: n x classes (optional)
   const uint8_t* labels; // optional (confusion)
@@ -294,8 +300,8 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       if (pw == 0 && lane == 0) {
         // L2 prefetch of the feature rows PF waves ahead: the fanout rows this
         // wave gathers are first touched there, so they then hit L2, not DRAM.
-        const uint32_t tp = t + kPrefetchWaves * G;
-        if (tp < ntiles) {
+        const uint32_t tp = t + a.pf_waves * G;
+        if (a.pf_waves && tp < ntiles) {
           const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - tp * kTileM);
           ptx::prefetch_l2(a.hin + static_cast<size_t>(tp) * kTileM * kF, rows * 128u);
         }
@@ -377,6 +383,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
     // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
     const uint32_t q = warp;
     uint8_t* ew = sE + q * 4096;
+    const uint64_t pol = ptx::policy_evict_first();
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
     // Warp 0 lane 0 issues the MMAs one tile ahead of its epilogue: iteration
     // it issues MMA(it), then every epilogue warp drains tile it-1.
@@ -408,7 +415,11 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
         for (int k = 0; k < 8; ++k) {
           const uint32_t ri = k * 4 + (lane >> 3), c = lane & 7;
           const float4 v = *reinterpret_cast<const float4*>(ew + ri * 128 + ((c ^ (ri & 7)) << 4));
-          if (row0 + ri < n) *reinterpret_cast<float4*>(a.hout + static_cast<size_t>(row0 + ri) * kF + 4 * c) = v;
+          if (row0 + ri < n) {
+            float* dst = a.hout + static_cast<size_t>(row0 + ri) * kF + 4 * c;
+            if (a.evict_first_out) ptx::stg_f4_hint(dst, v, pol);
+            else *reinterpret_cast<float4*>(dst) = v;
+          }
         }
         __syncwarp();
       } else {
@@ -604,23 +615,109 @@ __global__ void __launch_bounds__(256) hd_mean_feat_kernel(const uint32_t* __res
 
 // Standalone LD aggregation (groot_spmm_mean, f = 32): the same gather as the
 // fused layer, writing the mean rows (HD rows are written by hd_mean32_kernel).
-__global__ void __launch_bounds__(256) spmm_mean32_kernel(uint32_t n, const uint32_t* __restrict__ rp,
-                                                          const uint32_t* __restrict__ col,
-                                                          const float* __restrict__ H, HdInfo hd,
-                                                          float* __restrict__ out) {
-  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
-  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; base < n; base += warps * 8) {
-    uint32_t row[2] = {base + g, base + 4 + g};
-    float4 m[2];
-    HdInfo none = hd;
-    gather_mean32<2>(rp, col, H, n, row, j, gbase, none, m);
+// Standalone LD aggregation (groot_spmm_mean, f = 32) — the LD-kernel of the
+// degree-polarised split: persistent warps, 8-lane groups (one 128-byte row
+// per group, LDG.128 per lane), 8 rows per warp per step with the same
+// rolling index pipeline as the fused layer (features of step i, col_idx of
+// step i+1 and row_ptr of step i+2 in flight together). HD rows are written
+// by hd_mean32_kernel.
+template <int NR>
+__device__ __forceinline__ uint32_t dmax_of(const uint32_t (&d)[NR]) {
+  uint32_t m = 0;
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (row[q] < n) {
-        const uint32_t d = __ldg(rp + row[q] + 1) - __ldg(rp + row[q]);
-        if (d < hd.threshold) *reinterpret_cast<float4*>(out + static_cast<size_t>(row[q]) * kF + 4 * j) = m[q];
+  for (int q = 0; q < NR; ++q) m = max(m, d[q]);
+  return m;
+}
+
+template <int NR, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) spmm_mean32_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+                                                                     const uint32_t* __restrict__ col,
+                                                                     const float* __restrict__ H, uint32_t thr,
+                                                                     float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
+  const uint32_t W = gridDim.x * (blockDim.x >> 5);               // warps in the grid
+  const uint32_t w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr uint32_t R = 4 * NR;  // rows per warp step
+  const uint32_t nchunks = (n + R - 1) / R;
+  auto rp_load = [&](uint32_t ch, uint32_t (&b)[NR], uint32_t (&e)[NR]) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const uint32_t r = ch * R + q * 4 + g;
+      const bool ok = ch < nchunks && r < n;
+      b[q] = ok ? __ldg(rp + r) : 0u;
+      e[q] = ok ? __ldg(rp + r + 1) : 0u;
+    }
+  };
+  auto col_load = [&](const uint32_t (&b)[NR], const uint32_t (&d)[NR], uint32_t (&c)[NR]) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) c[q] = (static_cast<uint32_t>(j) < d[q] && d[q] < thr) ? __ldg(col + b[q] + j) : 0u;
+  };
+  uint32_t b0[NR], d0[NR], c0[NR], b1[NR], e1[NR];
+  {
+    uint32_t e0[NR];
+    rp_load(w0, b0, e0);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) d0[q] = e0[q] - b0[q];
+    col_load(b0, d0, c0);
+    rp_load(w0 + W, b1, e1);
+  }
+  constexpr int U = 4;
+  for (uint32_t ch = w0; ch < nchunks; ch += W) {
+    uint32_t dl[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) dl[q] = d0[q] < thr ? d0[q] : 0u;
+    float4 v[NR][U];
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t ci = __shfl_sync(0xffffffffu, c0[q], gbase + k);
+        if (static_cast<uint32_t>(k) < dl[q]) v[q][k] = ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j);
       }
+    uint32_t d1[NR], c1[NR], b2[NR], e2[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) d1[q] = e1[q] - b1[q];
+    col_load(b1, d1, c1);
+    rp_load(ch + 2 * W, b2, e2);
+    float4 m[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      m[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (static_cast<uint32_t>(k) < dl[q]) m[q] = f4add(m[q], v[q][k]);
+    }
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, dmax_of<NR>(dl));
+    if (dmax > static_cast<uint32_t>(U)) {
+      for (uint32_t k0 = 0; k0 < dmax; k0 += 8) {
+        uint32_t cc[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) cc[q] = k0 == 0 ? c0[q] : ((k0 + j < dl[q]) ? __ldg(col + b0[q] + k0 + j) : 0u);
+        for (uint32_t kk = (k0 == 0 ? U : 0); kk < 8; ++kk) {
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            const uint32_t ci = __shfl_sync(0xffffffffu, cc[q], gbase + kk);
+            if (k0 + kk < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const uint32_t r = ch * R + q * 4 + g;
+      if (r < n && d0[q] < thr) {
+        const float inv = d0[q] > 0 ? 1.0f / static_cast<float>(d0[q]) : 0.0f;
+        *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * kF + 4 * j) = f4scale(m[q], inv);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      b0[q] = b1[q];
+      d0[q] = d1[q];
+      c0[q] = c1[q];
+      b1[q] = b2[q];
+      e1[q] = e2[q];
+    }
   }
 }
 
@@ -808,6 +905,8 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     a.hd = hd;
     a.head = m->head.p;
     a.classes = m->classes;
+    a.pf_waves = env_u32("GROOT_PF_WAVES", 3);
+    a.evict_first_out = static_cast<int>(env_u32("GROOT_EVICT_FIRST", 1));
     a.cls = cls;
     a.logits = logits;
     a.labels = g->labels.p;
@@ -867,7 +966,18 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
                    g->rp.p, g->col.p, dense, out, 1);
     }
     ProfScope ps("spmm_mean32");
-    GROOT_LAUNCH(spmm_mean32_kernel, blocks_for(g->n, 64, sms * 8), 256, 0, g->n, g->rp.p, g->col.p, dense, hd, out);
+    static const int occ = [] {
+      const char* e = std::getenv("GROOT_SPMM_BLOCKS");
+      return e ? std::atoi(e) : 2;
+    }();
+    const uint32_t thr = hd.threshold;
+    switch (occ) {
+      case 1: GROOT_LAUNCH((spmm_mean32_kernel<2, 2>), sms * 2, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
+      case 2: GROOT_LAUNCH((spmm_mean32_kernel<1, 4>), sms * 4, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
+      case 3: GROOT_LAUNCH((spmm_mean32_kernel<1, 6>), sms * 6, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
+      case 4: GROOT_LAUNCH((spmm_mean32_kernel<1, 8>), sms * 8, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
+      default: GROOT_LAUNCH((spmm_mean32_kernel<2, 3>), sms * 3, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
+    }
   } else {
     GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
                  nullptr, dense, f, out);
