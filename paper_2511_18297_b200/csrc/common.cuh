@@ -176,5 +176,6 @@ struct groot_model {
   groot::DevBuf<float> bias;        // layers >= 1: 32 each
   groot::DevBuf<float> naive_w;     // fp32 row-major weights for the naive debug path
   groot::DevBuf<float> head;        // W_out[32 x classes] then b_out[classes]
-  float headw[32 * 8 + 8];          // same, classes padded to 8, passed as kernel parameters
+  float headw[32 * 8 + 8 + 32];     // same, classes padded to 8, + layer bias; kernel parameters
+  std::vector<float> bias_h;        // layers >= 1 biases (host copy for the parameter block)
 };

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "common.cuh"
@@ -34,7 +35,8 @@ constexpr uint32_t kStageBytes = 4 * kTileBytes;  // h_hi, h_lo, m_hi, m_lo
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
 constexpr int kMaxClasses = 8;
-constexpr uint32_t kTmemCols = 64;                // two 32-column fp32 accumulators
+constexpr uint32_t kAccCols = 32;                 // one fp32 accumulator of 32 columns
+constexpr uint32_t kTmemCols = 2 * kAccCols;      // double-buffered
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBBytes + kEpiBytes +
                                 (kF * kMaxClasses + kMaxClasses + kF) * 4 + 16 * 8 + 4 + 25 * 4 + 4 * kStages +
                                 1024;
@@ -48,7 +50,9 @@ static uint32_t env_u32(const char* name, uint32_t dflt) {
 uint32_t hd_threshold() {
   static uint32_t t = [] {
     const char* e = std::getenv("GROOT_HD_THRESHOLD");
-    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 128u;
+    // LD rows (degree < threshold) index a 256-entry reciprocal table in the fused layer.
+    const uint32_t v = e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 128u;
+    return v < 1 ? 1u : (v > 256 ? 256u : v);
   }();
   return t;
 }
@@ -165,7 +169,25 @@ __device__ __forceinline__ void store_split(uint8_t* hi_base, uint32_t i, int j,
 struct HeadW {
   float w[32][8];  // W_out[k][c], classes padded to 8
   float b[8];
+  float bias[32];  // this layer's bias (constant-bank operand in the epilogue)
 };
+
+// TF32 split by truncation: hi = x with the low 13 mantissa bits cleared (an
+// exact TF32 value, so the tensor core reads it unchanged whatever its input
+// rounding), lo = x - hi (exact in fp32, Sterbenz). Two ops per element.
+__device__ __forceinline__ void store_split_trunc(uint8_t* hi_base, uint32_t i, uint32_t chunk, float4 x) {
+  float4 h, l;
+  h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+  h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+  h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+  h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+  const float2 l01 = ptx::fsub2(make_float2(x.x, x.y), make_float2(h.x, h.y));
+  const float2 l23 = ptx::fsub2(make_float2(x.z, x.w), make_float2(h.z, h.w));
+  l = make_float4(l01.x, l01.y, l23.x, l23.y);
+  const uint32_t off = i * 128u + ((chunk ^ (i & 7u)) << 4);
+  *reinterpret_cast<float4*>(hi_base + off) = h;
+  *reinterpret_cast<float4*>(hi_base + kTileBytes + off) = l;
+}
 
 struct LayerArgs {
   uint32_t n;
@@ -179,6 +201,7 @@ struct LayerArgs {
   const float* head;     // W_out [32 x classes] row-major, then b_out
   uint32_t classes;
   uint32_t pf_waves;     // L2 prefetch distance in waves (0 = off)
+  unsigned long long* trace;  // diagnostic timeline of CTA 0 (nullptr = off): [64 tiles][16 events]
   int evict_first_out;   // store hout with an L2 evict-first policy
   uint8_t* cls;          // last layer: n classes
   float* logits;         // last layer: n x classes (optional)
@@ -204,6 +227,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained by the epilogue
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* sConf = sTmem + 1;
+  float* sInv = sHead;  // 1/deg for deg < 256 (correctly rounded, == 1.0f/d)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n = a.n;
@@ -213,6 +237,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
   for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
   if (threadIdx.x < kF) sBias[threadIdx.x] = a.bias[threadIdx.x];
+  for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
   if (kLast && threadIdx.x < 25) sConf[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -238,10 +263,14 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
   auto issue_mma = [&](uint32_t it) {
     const uint32_t s = it % kStages, ph = (it / kStages) & 1;
     const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+    unsigned long long* trow = (a.trace && blockIdx.x == 0 && it < 64) ? a.trace + it * 16 + 10 : nullptr;
+    if (trow) trow[0] = clock64();
     ptx::mbar_wait(&full[s], ph);
+    if (trow) trow[1] = clock64();
     ptx::mbar_wait(&tempty[acc], aph ^ 1);
+    if (trow) trow[2] = clock64();
     ptx::tc_fence_after();
-    const uint32_t d = tmem_base + acc * kF;
+    const uint32_t d = tmem_base + acc * kAccCols;
 #pragma unroll
     for (uint32_t kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -250,134 +279,163 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
         const uint32_t bo = b0s + kb * 8192 + kk * 32;
         const uint64_t ahi = ptx::umma_desc_sw128(ao), alo = ptx::umma_desc_sw128(ao + kTileBytes);
         const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
-        ptx::mma_tf32(d, ahi, bhi, idesc, (kb | kk) != 0);
+        const uint32_t first = (kb | kk) != 0;
+        ptx::mma_tf32(d, ahi, bhi, idesc, first);
         ptx::mma_tf32(d, ahi, blo, idesc, 1);
         ptx::mma_tf32(d, alo, bhi, idesc, 1);
       }
     ptx::mma_commit(&empty[s]);
     ptx::mma_commit(&tfull[acc]);
+    if (trow) trow[3] = clock64();
   };
 
   if (warp >= kEpiWarps) {
     // ===== gather producers =====
-    // 16 warps x 8 rows = one 128-row tile per pass. Rolling index pipeline:
-    // while the feature gathers of tile t are in flight, col_idx of tile t+G
-    // and row_ptr of tile t+2G are loaded, so a tile costs one memory round
-    // trip instead of three (row_ptr -> col_idx -> features).
+    // 16 warps x 8 rows = one 128-row tile per pass; 4 lanes per row, lane j
+    // owns features 8j..8j+7 (two LDG.128 per neighbour), so the per-row index
+    // work (shuffles, predicates, 1/deg) is shared by 4 lanes, and the sums use
+    // packed f32x2 adds. Rolling index pipeline: while the feature gathers of
+    // tile t are in flight, col_idx of tile t+G and row_ptr of tile t+2G load.
     const int pw = warp - kEpiWarps;
-    const int g = lane >> 3, j = lane & 7, gbase = lane & 24;
+    const int j = lane & 3, gbase = lane & ~3;
+    const uint32_t li = pw * 8 + (lane >> 2);  // tile-local row of this lane group
     const uint32_t thr = a.hd.threshold;
-    uint32_t li[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) li[q] = pw * 8 + q * 4 + g;
-    auto rp_load = [&](uint32_t tt, uint32_t (&b)[2], uint32_t (&e)[2]) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t r = tt * kTileM + li[q];
-        const bool ok = tt < ntiles && r < n;
-        b[q] = ok ? __ldg(a.rp + r) : 0u;
-        e[q] = ok ? __ldg(a.rp + r + 1) : 0u;
-      }
+    const float* hin_j = a.hin + 8 * j;
+    auto rp_load = [&](uint32_t tt, uint32_t& b, uint32_t& e) {
+      const uint32_t r = tt * kTileM + li;
+      const bool ok = tt < ntiles && r < n;
+      b = ok ? __ldg(a.rp + r) : 0u;
+      e = ok ? __ldg(a.rp + r + 1) : 0u;
     };
-    auto col_load = [&](const uint32_t (&b)[2], const uint32_t (&d)[2], uint32_t (&c)[2]) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        c[q] = (static_cast<uint32_t>(j) < d[q] && d[q] < thr) ? __ldg(a.col + b[q] + j) : 0u;
+    auto col_load = [&](uint32_t b, uint32_t d) {
+      return (static_cast<uint32_t>(j) < d && d < thr) ? __ldg(a.col + b + j) : 0u;
     };
-    uint32_t b0[2], d0[2], c0[2], b1[2], e1[2];
+    // Index pipeline state: tile t (b0,d0,c0), t+G (b1,d1,c1), t+2G (b2,d2),
+    // raw row_ptr of t+3G (b3,e3) and t+4G (loaded this iteration). col_idx is
+    // loaded 2 tiles ahead and row_ptr 4 tiles ahead of use, so neither load
+    // sits on the per-tile critical path even at loaded DRAM latency.
+    uint32_t b0, d0, c0, b1, d1, c1, b2, d2, b3, e3;
     {
-      uint32_t e0[2];
-      rp_load(blockIdx.x, b0, e0);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) d0[q] = e0[q] - b0[q];
-      col_load(b0, d0, c0);
-      rp_load(blockIdx.x + G, b1, e1);
+      uint32_t e;
+      rp_load(blockIdx.x, b0, e);
+      d0 = e - b0;
+      rp_load(blockIdx.x + G, b1, e);
+      d1 = e - b1;
+      rp_load(blockIdx.x + 2 * G, b2, e);
+      d2 = e - b2;
+      rp_load(blockIdx.x + 3 * G, b3, e3);
+      c0 = col_load(b0, d0);
+      c1 = col_load(b1, d1);
     }
-    constexpr int U = 4;  // neighbours per row in the first burst (CSA LD rows have degree <= 4)
+    constexpr int U = 4;  // neighbours per row in the first burst (= lanes per row)
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      if (pw == 0 && lane == 0) {
-        // L2 prefetch of the feature rows PF waves ahead: the fanout rows this
-        // wave gathers are first touched there, so they then hit L2, not DRAM.
+      if (pw == 0 && lane == 0 && a.pf_waves) {
+        // L2 prefetch of the feature rows pf_waves waves ahead (first touches of fanout rows).
         const uint32_t tp = t + a.pf_waves * G;
-        if (a.pf_waves && tp < ntiles) {
+        if (tp < ntiles) {
           const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - tp * kTileM);
           ptx::prefetch_l2(a.hin + static_cast<size_t>(tp) * kTileM * kF, rows * 128u);
         }
       }
-      uint32_t dl[2];
+      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && pw == 0 && it < 64;
+      unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
+      if (tr) trow[0] = clock64();
+      const uint32_t dl = d0 < thr ? d0 : 0u;
+      if (tr) {  // control dependency: stamp only once the index values have landed
+        if (c0 == 0xFFFFFFF0u && d0 == 0xFFFFFFF0u) asm volatile("trap;");
+        trow[1] = clock64();
+      }
+      const uint32_t r = t * kTileM + li;
+      // burst: 2 x 16 B of each of up to U neighbours + of the self row
+      float4 v[U][2], hs[2];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) dl[q] = d0[q] < thr ? d0[q] : 0u;
-      // burst: U neighbour chunks + the self chunk per row, all independent.
-      float4 v[2][U], hs[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t r = t * kTileM + li[q];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const uint32_t ci = __shfl_sync(0xffffffffu, c0[q], gbase + k);
-          if (static_cast<uint32_t>(k) < dl[q]) v[q][k] = ptx::ldg_f4(a.hin + static_cast<size_t>(ci) * kF + 4 * j);
+      for (int k = 0; k < U; ++k) {
+        const uint32_t ci = __shfl_sync(0xffffffffu, c0, gbase + k);
+        if (static_cast<uint32_t>(k) < dl) {
+          ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, v[k][0], v[k][1]);
         }
-        hs[q] = r < n ? ptx::ldg_f4(a.hin + static_cast<size_t>(r) * kF + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      // index prefetch for the next two tiles (in flight with the burst)
-      uint32_t d1[2], c1[2], b2[2], e2[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) d1[q] = e1[q] - b1[q];
-      col_load(b1, d1, c1);
-      rp_load(t + 2 * G, b2, e2);
-      // consume in nonzero order (predicated adds: no selects, no moves)
-      float4 m[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        m[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-          if (static_cast<uint32_t>(k) < dl[q]) m[q] = f4add(m[q], v[q][k]);
+      if (r < n) {
+        ptx::ldg_f8(hin_j + static_cast<size_t>(r) * kF, hs[0], hs[1]);
+      } else {
+        hs[0] = hs[1] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      const uint32_t dmax = __reduce_max_sync(0xffffffffu, max(dl[0], dl[1]));
+      // index loads for later tiles (in flight with the burst)
+      const uint32_t c2 = col_load(b2, d2);
+      uint32_t b4, e4;
+      rp_load(t + 4 * G, b4, e4);
+      // consume in nonzero order with packed f32x2 adds
+      if (tr) trow[2] = clock64();
+      float2 m0 = make_float2(0.f, 0.f), m1 = m0, m2 = m0, m3 = m0;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (static_cast<uint32_t>(k) < dl) {
+          m0 = ptx::fadd2(m0, make_float2(v[k][0].x, v[k][0].y));
+          m1 = ptx::fadd2(m1, make_float2(v[k][0].z, v[k][0].w));
+          m2 = ptx::fadd2(m2, make_float2(v[k][1].x, v[k][1].y));
+          m3 = ptx::fadd2(m3, make_float2(v[k][1].z, v[k][1].w));
+        }
+      if (tr) {
+        if (m0.x == -1234.5f && m3.y == -1234.5f && hs[1].w == -1234.5f) asm volatile("trap;");
+        trow[3] = clock64();
+      }
+      const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
       if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
-        for (uint32_t k0 = 0; k0 < dmax; k0 += 8) {
-          uint32_t cc[2];
+        for (uint32_t k0 = U; k0 < dmax; k0 += U) {
+          const uint32_t cc = (k0 + j < dl) ? __ldg(a.col + b0 + k0 + j) : 0u;
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
-            cc[q] = k0 == 0 ? c0[q] : ((k0 + j < dl[q]) ? __ldg(a.col + b0[q] + k0 + j) : 0u);
-          for (uint32_t kk = (k0 == 0 ? U : 0); kk < 8; ++kk) {
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const uint32_t ci = __shfl_sync(0xffffffffu, cc[q], gbase + kk);
-              if (k0 + kk < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(a.hin + static_cast<size_t>(ci) * kF + 4 * j));
+          for (int kk = 0; kk < U; ++kk) {
+            const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + kk);
+            if (k0 + kk < dl) {
+              float4 x0, x1;
+              ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, x0, x1);
+              m0 = ptx::fadd2(m0, make_float2(x0.x, x0.y));
+              m1 = ptx::fadd2(m1, make_float2(x0.z, x0.w));
+              m2 = ptx::fadd2(m2, make_float2(x1.x, x1.y));
+              m3 = ptx::fadd2(m3, make_float2(x1.z, x1.w));
             }
           }
         }
       }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (d0[q] >= thr) {
-          m[q] = ptx::ldg_f4(a.hd.mean + static_cast<size_t>(hd_slot(a.hd, t * kTileM + li[q])) * kF + 4 * j);
-        } else {
-          const float inv = d0[q] > 0 ? 1.0f / static_cast<float>(d0[q]) : 0.0f;
-          m[q] = f4scale(m[q], inv);
-        }
+      float4 mm[2];
+      if (d0 >= thr) {
+        const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
+        mm[0] = ptx::ldg_f4(src);
+        mm[1] = ptx::ldg_f4(src + 4);
+      } else {
+        const float inv = sInv[d0];
+        const float2 iv = make_float2(inv, inv);
+        m0 = ptx::fmul2(m0, iv);
+        m1 = ptx::fmul2(m1, iv);
+        m2 = ptx::fmul2(m2, iv);
+        m3 = ptx::fmul2(m3, iv);
+        mm[0] = make_float4(m0.x, m0.y, m1.x, m1.y);
+        mm[1] = make_float4(m2.x, m2.y, m3.x, m3.y);
       }
+      if (tr) trow[4] = clock64();
       ptx::mbar_wait(&empty[s], ph ^ 1);
+      if (tr) trow[5] = clock64();
       uint8_t* st = sA + s * kStageBytes;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        store_split(st, li[q], j, hs[q]);                  // K block 0: self features
-        store_split(st + 2 * kTileBytes, li[q], j, m[q]);  // K block 1: neighbour mean
+      for (int c = 0; c < 2; ++c) {
+        store_split_trunc(st, li, 2 * j + c, hs[c]);                  // K block 0: self features
+        store_split_trunc(st + 2 * kTileBytes, li, 2 * j + c, mm[c]);  // K block 1: neighbour mean
       }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        b0[q] = b1[q];
-        d0[q] = d1[q];
-        c0[q] = c1[q];
-        b1[q] = b2[q];
-        e1[q] = e2[q];
-      }
+      if (tr) trow[6] = clock64();
+      b0 = b1;
+      d0 = d1;
+      c0 = c1;
+      b1 = b2;
+      d1 = d2;
+      c1 = c2;
+      b2 = b3;
+      d2 = e3 - b3;
+      b3 = b4;
+      e3 = e4;
     }
   } else {
     // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
@@ -397,13 +455,16 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       const uint32_t t = blockIdx.x + e * G;
       const uint32_t acc = e & 1, ph = (e >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], ph);
+      if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 14] = clock64();
       ptx::tc_fence_after();
       float r[32];
-      ptx::tmem_ld_32x32b_x32(tmem_base + acc * kF + ((q * 32u) << 16), r);
+      const uint32_t tq = tmem_base + acc * kAccCols + ((q * 32u) << 16);
+      ptx::tmem_ld_32x32b_x32(tq, r);
+
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + sBias[i], 0.0f);
+      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + hw.bias[i], 0.0f);
       const uint32_t row0 = t * kTileM + q * 32;
       if (!kLast) {
 #pragma unroll
@@ -440,6 +501,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
         }
         if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
       }
+      if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 15] = clock64();
     }
   }
 
@@ -905,21 +967,40 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     a.hd = hd;
     a.head = m->head.p;
     a.classes = m->classes;
-    a.pf_waves = env_u32("GROOT_PF_WAVES", 3);
+    a.pf_waves = env_u32("GROOT_PF_WAVES", 0);
     a.evict_first_out = static_cast<int>(env_u32("GROOT_EVICT_FIRST", 1));
     a.cls = cls;
     a.logits = logits;
     a.labels = g->labels.p;
     a.confusion = confusion;
+    static const char* trace_path = std::getenv("GROOT_TRACE");
+    DevBuf<unsigned long long> trace;
+    if (trace_path && l == 1) {
+      trace.alloc(64 * 16);
+      trace.zero();
+      a.trace = trace.p;
+    }
     const unsigned grid = std::min<uint32_t>(ntiles, sms);
+    HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
+    std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
     if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a,
-                   *reinterpret_cast<const HeadW*>(m->headw));
+      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw);
     } else {
       ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a,
-                   *reinterpret_cast<const HeadW*>(m->headw));
+      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw);
+    }
+    if (a.trace) {
+      std::vector<unsigned long long> h(64 * 16);
+      trace.download(h.data(), h.size());
+      stream_sync();
+      if (FILE* fp = std::fopen(trace_path, "w")) {
+        for (int i = 0; i < 64; ++i) {
+          for (int k = 0; k < 16; ++k) std::fprintf(fp, "%llu ", h[i * 16 + k]);
+          std::fprintf(fp, "\n");
+        }
+        std::fclose(fp);
+      }
     }
   }
   if (m->depth == 1)
@@ -1043,6 +1124,7 @@ void model_upload(groot_model* m) {
   std::vector<float> head(H * C + C);
   for (uint32_t i = 0; i < H * C + C; ++i) head[i] = static_cast<float>(p[off + i]);
   static_assert(sizeof(HeadW) == sizeof(m->headw), "head parameter block");
+  m->bias_h = bias;
   HeadW hw{};
   for (uint32_t k = 0; k < H; ++k)
     for (uint32_t c = 0; c < C; ++c) hw.w[k][c] = head[k * C + c];

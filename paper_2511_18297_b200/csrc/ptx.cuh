@@ -137,6 +137,34 @@ __device__ __forceinline__ void stg_f4_hint(float* p, float4 v, uint64_t pol) {
                : "memory");
 }
 
+// Prefetch one line into L2 (per-thread).
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// ---- packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2) -----------------------------
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) {
+  return (static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
+}
+__device__ __forceinline__ float2 bits_f2(unsigned long long u) {
+  return make_float2(__uint_as_float(static_cast<uint32_t>(u)), __uint_as_float(static_cast<uint32_t>(u >> 32)));
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(r);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(r);
+}
+
 // ---- conversions / loads --------------------------------------------------------
 // Round-to-nearest (ties away) fp32 -> tf32 (low 13 mantissa bits cleared).
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -147,6 +175,12 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
+}
+// 256-bit read-only load (sm_100: LDG.E.ENL2.256) into two float4.
+__device__ __forceinline__ void ldg_f8(const float* p, float4& a, float4& b) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(p));
 }
 // Streaming (read-once) 128-bit load: do not allocate in L1.
 __device__ __forceinline__ float4 ldg_f4_stream(const float* p) {
