@@ -93,6 +93,10 @@ int groot_batch(const groot_graph* g, uint32_t copies, groot_graph** out);
 int groot_graph_from_host(uint32_t n, const uint64_t* row_ptr, const uint32_t* col_idx,
                           const uint8_t* features, const uint8_t* labels, uint64_t num_edges,
                           const uint32_t* fwd_edges, groot_graph** out);
+/* build_symmetric_csr (src/encode.cpp:14-31) on the device from a forward edge
+ * list: rows ascending, duplicates kept. features/labels may be NULL. */
+int groot_graph_from_edges(uint32_t n, const uint8_t* features, const uint8_t* labels, uint64_t num_edges,
+                           const uint32_t* fwd_edges, groot_graph** out);
 int groot_graph_sizes(const groot_graph* g, uint32_t* n, uint64_t* nnz, uint64_t* num_edges);
 /* Copy any subset of the EdaGraph arrays back to host (NULL = skip). */
 int groot_graph_copy_out(const groot_graph* g, uint64_t* row_ptr, uint32_t* col_idx,
@@ -169,6 +173,12 @@ int groot_predict_full(const groot_model* m, const groot_graph* g, uint8_t* labe
  * each node scored from the part that owns it as a core node. */
 int groot_predict(const groot_model* m, const groot_graph* g, const groot_parts* p,
                   uint8_t* labels_host, uint64_t* confusion, double* accuracy);
+
+/* predict restricted to the parts in part_ids (multi-GPU: each rank forwards
+ * its own parts): labels_host (n entries, in/out) receives the classes of the
+ * core nodes of those parts; all other entries are left unchanged. */
+int groot_predict_parts(const groot_model* m, const groot_graph* g, const groot_parts* p,
+                        const uint32_t* part_ids, uint32_t count, uint8_t* labels_host);
 
 /* Device-resident session entry points (no host copies; work enqueued on the
  * library stream). labels_dev u8[n], logits_dev f32[n*classes] (NULL = skip),

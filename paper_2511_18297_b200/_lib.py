@@ -47,6 +47,7 @@ _SIG = {
     "groot_encode": (i32, [u32, u32, P, u32, P, P, P]),
     "groot_batch": (i32, [P, u32, P]),
     "groot_graph_from_host": (i32, [u32, P, P, P, P, u64, P, P]),
+    "groot_graph_from_edges": (i32, [u32, P, P, u64, P, P]),
     "groot_graph_sizes": (i32, [P, P, P, P]),
     "groot_graph_copy_out": (i32, [P, P, P, P, P, P, P]),
     "groot_graph_device_ptrs": (i32, [P, P, P, P, P, P]),
@@ -79,6 +80,7 @@ _SIG = {
     "groot_predict_full": (i32, [P, P, P, P, P]),
     "groot_predict": (i32, [P, P, P, P, P, P]),
     "groot_predict_full_dev": (i32, [P, P, P, P, P]),
+    "groot_predict_parts": (i32, [P, P, P, P, u32, P]),
     "groot_classify_aig": (i32, [P, u32, u32, P, u32, P, P, u32, P, P, P]),
     "groot_build_plan": (i32, [P, u32, u32, u32, P, P, P, P, P, P]),
     "groot_spmm_mean": (i32, [P, P, u32, P]),

@@ -500,6 +500,15 @@ def predict(model: Model, g: EdaGraph, parts: AugmentedPartitions) -> Prediction
     return Prediction(labels, conf, acc.value)
 
 
+def predict_parts(model: Model, g: EdaGraph, parts: AugmentedPartitions, part_ids, labels=None) -> np.ndarray:
+    """predict restricted to `part_ids`: returns the global label vector with the core
+    nodes of those parts filled in (others from `labels`, default zeros)."""
+    ids = np.ascontiguousarray(part_ids, np.uint32)
+    out = np.zeros(g.n, np.uint8) if labels is None else np.ascontiguousarray(labels, np.uint8).copy()
+    check(lib().groot_predict_parts(model.handle, g.handle, parts.handle, ptr(ids), ids.shape[0], ptr(out)))
+    return out
+
+
 def classify_aig(model: Model, aig: Aig, labels, copies: int = 1) -> Prediction:
     """End to end: host AIG -> encode -> batch -> predict_full -> host classes."""
     ands = np.ascontiguousarray(aig.and_lits, np.uint32)

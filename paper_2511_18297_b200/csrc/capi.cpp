@@ -40,6 +40,7 @@ int num_sms() {
 // graph_build.cu / forward.cu
 groot_graph* encode(uint32_t, uint32_t, const uint32_t*, uint32_t, const uint32_t*, const uint8_t*);
 groot_graph* batch(const groot_graph*, uint32_t);
+groot_graph* graph_from_edges(uint32_t, const uint8_t*, const uint8_t*, uint64_t, const uint32_t*);
 groot_graph* graph_from_host(uint32_t, const uint64_t*, const uint32_t*, const uint8_t*, const uint8_t*, uint64_t,
                              const uint32_t*);
 void graph_copy_out(const groot_graph*, uint64_t*, uint32_t*, uint8_t*, uint8_t*, uint32_t*, uint32_t*);
@@ -49,7 +50,8 @@ groot_assignment* load_assignment(const char*, uint32_t);
 uint64_t edge_cut(const groot_graph*, const groot_assignment*);
 groot_parts* regrow(const groot_graph*, const groot_assignment*, int);
 groot_graph* materialize(const groot_graph*, const groot_parts*, uint32_t);
-groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<uint64_t>&);
+groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<uint64_t>&,
+                            const std::vector<uint32_t>*);
 void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
 void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void forward_naive_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
@@ -351,6 +353,15 @@ int groot_graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col, c
   });
 }
 
+int groot_graph_from_edges(uint32_t n, const uint8_t* feat, const uint8_t* lab, uint64_t ne, const uint32_t* edges,
+                           groot_graph** out) {
+  return guarded([&] {
+    need(out, "groot_graph_from_edges");
+    if (ne) need(edges, "groot_graph_from_edges");
+    *out = graph_from_edges(n, feat, lab, ne, edges);
+  });
+}
+
 int groot_graph_sizes(const groot_graph* g, uint32_t* n, uint64_t* nnz, uint64_t* ne) {
   return guarded([&] {
     need(g, "groot_graph_sizes");
@@ -648,7 +659,7 @@ int groot_predict(const groot_model* m, const groot_graph* g, const groot_parts*
     need(g, "groot_predict");
     need(p, "groot_predict");
     std::vector<uint64_t> node_off;
-    groot_graph* u = union_of_parts(g, p, node_off);
+    groot_graph* u = union_of_parts(g, p, node_off, nullptr);
     try {
       DevBuf<uint8_t> cls(u->n), out(g->n);
       out.zero();
@@ -663,6 +674,31 @@ int groot_predict(const groot_model* m, const groot_graph* g, const groot_parts*
         if (truth[v] < 5 && pred[v] < 5) ++conf[truth[v] * 5 + pred[v]];
       if (labels_host) std::copy(pred.begin(), pred.end(), labels_host);
       finish_confusion(conf, g->n, confusion, accuracy);
+    } catch (...) {
+      delete u;
+      throw;
+    }
+    delete u;
+  });
+}
+
+int groot_predict_parts(const groot_model* m, const groot_graph* g, const groot_parts* p, const uint32_t* part_ids,
+                        uint32_t count, uint8_t* labels_host) {
+  return guarded([&] {
+    need(m, "groot_predict_parts");
+    need(g, "groot_predict_parts");
+    need(p, "groot_predict_parts");
+    need(labels_host, "groot_predict_parts");
+    std::vector<uint32_t> ids(part_ids, part_ids + count);
+    std::vector<uint64_t> node_off;
+    groot_graph* u = union_of_parts(g, p, node_off, &ids);
+    try {
+      DevBuf<uint8_t> cls(u->n), out(g->n);
+      out.upload(labels_host, g->n);
+      if (u->n) forward_device(m, u, cls.p, nullptr, nullptr);
+      scatter_core_labels(p, node_off, cls.p, out.p);
+      out.download(labels_host, g->n);
+      stream_sync();
     } catch (...) {
       delete u;
       throw;

@@ -205,6 +205,13 @@ void build_csr(uint32_t n, uint64_t ne, const uint32_t* d_edges, uint32_t* d_rp,
   stream_sync();
 }
 
+__global__ void check_edges_kernel(uint64_t ne, const uint2* __restrict__ e, uint32_t n, uint32_t* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 uv = e[i];
+    if (uv.x >= n || uv.y >= n) atomicMin(bad, static_cast<uint32_t>(i));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3: batch (src/encode.cpp:70-101)
 // ---------------------------------------------------------------------------
@@ -541,6 +548,27 @@ groot_graph* graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col
   return g;
 }
 
+groot_graph* graph_from_edges(uint32_t n, const uint8_t* feat, const uint8_t* lab, uint64_t ne,
+                              const uint32_t* edges) {
+  groot_graph* g = graph_alloc(n, ne);
+  try {
+    if (feat) g->feat.upload(feat, 4ull * n); else g->feat.zero();
+    if (lab) g->labels.upload(lab, n); else g->labels.zero();
+    g->edges.upload(edges, 2 * ne);
+    DevBuf<uint32_t> bad(1);
+    const uint32_t none = 0xFFFFFFFFu;
+    bad.upload(&none, 1);
+    if (ne) GROOT_LAUNCH(check_edges_kernel, blocks_for(ne, 256), 256, 0, ne, reinterpret_cast<const uint2*>(g->edges.p), n, bad.p);
+    if (read_scalar(bad.p) != none) fail(GROOT_EINVAL, "graph: edge endpoint out of range");
+    build_csr(n, ne, g->edges.p, g->rp.p, g->col.p);
+    stream_sync();
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  return g;
+}
+
 void graph_copy_out(const groot_graph* g, uint64_t* rp, uint32_t* col, uint8_t* feat, uint8_t* lab,
                     uint32_t* deg, uint32_t* edges) {
   if (rp) {
@@ -762,28 +790,38 @@ groot_graph* materialize(const groot_graph* g, const groot_parts* P, uint32_t p)
 }
 
 // Block-diagonal union of all materialized parts (predict runs one forward over it).
-groot_graph* union_of_parts(const groot_graph* g, const groot_parts* P, std::vector<uint64_t>& node_off) {
+groot_graph* union_of_parts(const groot_graph* g, const groot_parts* P, std::vector<uint64_t>& node_off,
+                            const std::vector<uint32_t>* subset) {
   const uint32_t k = P->k;
+  std::vector<uint8_t> use(k, subset ? 0 : 1);
+  if (subset)
+    for (uint32_t p : *subset) {
+      if (p >= k) fail(GROOT_EINVAL, "predict: part index out of range");
+      use[p] = 1;
+    }
   node_off.assign(k + 1ull, 0);
   for (uint32_t p = 0; p < k; ++p)
-    node_off[p + 1] = node_off[p] + (P->core_off[p + 1] - P->core_off[p]) + (P->bnd_off[p + 1] - P->bnd_off[p]);
+    node_off[p + 1] = node_off[p] + (use[p] ? (P->core_off[p + 1] - P->core_off[p]) + (P->bnd_off[p + 1] - P->bnd_off[p]) : 0);
   require(node_off[k] < 0xFFFFFFFFull, "predict: augmented node count exceeds 2^32-1");
   const uint32_t n = static_cast<uint32_t>(node_off[k]);
-  const uint64_t ne = P->edge_off[k];
+  std::vector<uint64_t> eoff(k + 1ull, 0);
+  for (uint32_t p = 0; p < k; ++p) eoff[p + 1] = eoff[p] + (use[p] ? P->edge_off[p + 1] - P->edge_off[p] : 0);
+  const uint64_t ne = eoff[k];
   groot_graph* o = graph_alloc(n, ne);
   try {
     DevBuf<uint32_t> l2g(n);
-    for (uint32_t p = 0; p < k; ++p) part_l2g(P, p, l2g.p + node_off[p]);
+    for (uint32_t p = 0; p < k; ++p)
+      if (use[p]) part_l2g(P, p, l2g.p + node_off[p]);
     if (n)
       GROOT_LAUNCH(gather_nodes_kernel, blocks_for(n, 256), 256, 0, n, l2g.p,
                    reinterpret_cast<const uint32_t*>(g->feat.p), g->labels.p,
                    reinterpret_cast<uint32_t*>(o->feat.p), o->labels.p);
     for (uint32_t p = 0; p < k; ++p) {
-      const uint64_t cnt = P->edge_off[p + 1] - P->edge_off[p];
+      const uint64_t cnt = use[p] ? P->edge_off[p + 1] - P->edge_off[p] : 0;
       if (cnt)
         GROOT_LAUNCH(add_offset_pairs_kernel, blocks_for(cnt, 256), 256, 0, cnt,
                      reinterpret_cast<const uint2*>(P->edges.p) + P->edge_off[p],
-                     static_cast<uint32_t>(node_off[p]), reinterpret_cast<uint2*>(o->edges.p) + P->edge_off[p]);
+                     static_cast<uint32_t>(node_off[p]), reinterpret_cast<uint2*>(o->edges.p) + eoff[p]);
     }
     build_csr(n, ne, o->edges.p, o->rp.p, o->col.p);
     stream_sync();
@@ -798,6 +836,7 @@ groot_graph* union_of_parts(const groot_graph* g, const groot_parts* P, std::vec
 void scatter_core_labels(const groot_parts* P, const std::vector<uint64_t>& node_off, const uint8_t* d_cls,
                          uint8_t* d_out) {
   for (uint32_t p = 0; p < P->k; ++p) {
+    if (node_off[p + 1] == node_off[p]) continue;  // part not in the forwarded subset
     const uint32_t nc = static_cast<uint32_t>(P->core_off[p + 1] - P->core_off[p]);
     if (nc)
       GROOT_LAUNCH(scatter_core_labels_kernel, blocks_for(nc, 256), 256, 0, nc, P->core.p + P->core_off[p],

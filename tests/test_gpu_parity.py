@@ -377,3 +377,37 @@ def test_large_batch_copy_consistency(api, golden_dir):
     assert gb.n == 16 * g1.n
     pb = api.predict_full(model, gb).labels.reshape(16, -1)
     assert (pb == p1[None, :]).all()
+
+
+def test_shard_device_compute(api, golden_dir):
+    """Per-rank device compute of the sharding layer: rank shares computed one
+    after another on one GPU and merged equal the single-process reference."""
+    from paper_2511_18297_b200 import shard
+    prm = trained_params(golden_dir)
+    model = api.Model.from_params(prm)
+    circ = api.gen_csa_multiplier(16)
+    h1 = ora_graph(16)
+    compute = shard.device_copy_compute(model, circ)
+    world, copies = 3, 5
+    blocks, conf = [], np.zeros((5, 5), np.uint64)
+    for r in range(world):
+        lab, c = compute(shard.copy_shard(r, world, copies, h1.n))
+        blocks.append(lab)
+        conf += c
+    hb = O.batch(h1, copies)
+    opred, oconf, _, _ = O.predict_full(hb, prm)
+    np.testing.assert_array_equal(np.concatenate(blocks), opred)
+    np.testing.assert_array_equal(conf, oconf)
+    # partitions: each "rank" forwards only its parts (groot_predict_parts)
+    g = dev_graph(api, 16, 2)
+    hg = ora_graph(16, 2)
+    k = 6
+    parts = api.regrow(g, api.partition_topo_chunks(g, k))
+    pcompute = shard.device_parts_compute(model, g, parts)
+    pred = np.zeros(g.n, np.uint8)
+    for r in range(world):
+        ids, lab = pcompute(shard.owned_parts(k, r, world))
+        pred[ids] = lab
+    oparts = O.regrow(hg, O.topo_chunks(hg.n, k), k)
+    opred2, _, _ = O.predict(hg, oparts, prm)
+    np.testing.assert_array_equal(pred, opred2)
