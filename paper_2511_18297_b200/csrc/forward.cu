@@ -12,6 +12,7 @@
 // are aggregated first by a CTA-per-row kernel with a fixed-order reduction.
 // Layer 0 (4 -> 32, inputs in {0,1}^4) is a gather + FFMA kernel.
 #include <cub/cub.cuh>
+#include <cuda.h>
 
 #include <cstdlib>
 #include <cstdio>
@@ -28,7 +29,10 @@ constexpr int kEpiWarps = 4;                 // warps 0..3: TMEM lane quadrants;
 constexpr int kProdWarps = 16;               // warps 4..19: gather producers (8 rows each)
 // 20 warps = 5 per SM sub-partition: 5 x 96 regs x 32 lanes fits one sub-partition's
 // 16K registers (a 21st warp would force the cap down to 80 registers).
-constexpr int kThreads = (kEpiWarps + kProdWarps) * 32;  // 640
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 20: TMEM alloc + tcgen05.mma issue
+// 21 warps: sub-partition 0 holds 6 of them, so its 16K registers cap the
+// kernel at 80 registers/thread (6 x 80 x 32 = 15360).
+constexpr int kThreads = (kMmaWarp + 1) * 32;  // 672
 constexpr int kStages = 3;
 constexpr uint32_t kTileBytes = kTileM * 128;     // 128 rows x 32 fp32
 constexpr uint32_t kStageBytes = 4 * kTileBytes;  // h_hi, h_lo, m_hi, m_lo
@@ -202,7 +206,6 @@ struct LayerArgs {
   uint32_t classes;
   uint32_t pf_waves;     // L2 prefetch distance in waves (0 = off)
   unsigned long long* trace;  // diagnostic timeline of CTA 0 (nullptr = off): [64 tiles][16 events]
-  int evict_first_out;   // store hout with an L2 evict-first policy
   uint8_t* cls;          // last layer: n classes
   float* logits;         // last layer: n x classes (optional)
   const uint8_t* labels; // optional (confusion)
@@ -210,7 +213,8 @@ struct LayerArgs {
 };
 
 template <bool kLast>
-__global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw) {
+__global__ void __maxnreg__(80) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw,
+                                                      const __grid_constant__ CUtensorMap tmap_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B operand tiles, computed on the shared
   // address so the pointer stays in the shared window (STS, not generic ST).
@@ -250,7 +254,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
     }
     ptx::mbar_fence_init();
   }
-  if (warp == 0) ptx::tmem_alloc<kTmemCols>(sTmem);
+  if (warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -289,7 +293,14 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
     if (trow) trow[3] = clock64();
   };
 
-  if (warp >= kEpiWarps) {
+  if (warp == kMmaWarp) {
+    // ===== MMA issuer: one elected thread, decoupled from producers and epilogue =====
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) issue_mma(it);
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarps) {
     // ===== gather producers =====
     // 16 warps x 8 rows = one 128-row tile per pass; 4 lanes per row, lane j
     // owns features 8j..8j+7 (two LDG.128 per neighbour), so the per-row index
@@ -327,7 +338,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       c0 = col_load(b0, d0);
       c1 = col_load(b1, d1);
     }
-    constexpr int U = 4;  // neighbours per row in the first burst (= lanes per row)
+    constexpr int U = 4;  // neighbours per row in one burst (CSA LD rows have degree <= 4)
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
@@ -343,31 +354,29 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
       if (tr) trow[0] = clock64();
       const uint32_t dl = d0 < thr ? d0 : 0u;
-      if (tr) {  // control dependency: stamp only once the index values have landed
-        if (c0 == 0xFFFFFFF0u && d0 == 0xFFFFFFF0u) asm volatile("trap;");
-        trow[1] = clock64();
-      }
       const uint32_t r = t * kTileM + li;
-      // burst: 2 x 16 B of each of up to U neighbours + of the self row
+      // Burst: U neighbour lines + the self line per row, all independent and
+      // unconditional (slots past the degree re-read the row's own line): a
+      // conditional load makes the compiler merge registers with moves that
+      // wait on the first loads and split the burst into two round trips.
+      // The burst is not software-pipelined across tiles on purpose: the proxy
+      // fence before the stage hand-off (MEMBAR.ALL.CTA) waits for every
+      // outstanding load of the thread, which would serialise it anyway.
+      const uint32_t self = r < n ? r : 0u;
       float4 v[U][2], hs[2];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const uint32_t ci = __shfl_sync(0xffffffffu, c0, gbase + k);
-        if (static_cast<uint32_t>(k) < dl) {
-          ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, v[k][0], v[k][1]);
-        }
+        const uint32_t src = static_cast<uint32_t>(k) < dl ? ci : self;
+        ptx::ldg_f8(hin_j + static_cast<size_t>(src) * kF, v[k][0], v[k][1]);
       }
-      if (r < n) {
-        ptx::ldg_f8(hin_j + static_cast<size_t>(r) * kF, hs[0], hs[1]);
-      } else {
-        hs[0] = hs[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      ptx::ldg_f8(hin_j + static_cast<size_t>(self) * kF, hs[0], hs[1]);
       // index loads for later tiles (in flight with the burst)
       const uint32_t c2 = col_load(b2, d2);
       uint32_t b4, e4;
       rp_load(t + 4 * G, b4, e4);
+      if (tr) trow[1] = clock64();
       // consume in nonzero order with packed f32x2 adds
-      if (tr) trow[2] = clock64();
       float2 m0 = make_float2(0.f, 0.f), m1 = m0, m2 = m0, m3 = m0;
 #pragma unroll
       for (int k = 0; k < U; ++k)
@@ -377,10 +386,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
           m2 = ptx::fadd2(m2, make_float2(v[k][1].x, v[k][1].y));
           m3 = ptx::fadd2(m3, make_float2(v[k][1].z, v[k][1].w));
         }
-      if (tr) {
-        if (m0.x == -1234.5f && m3.y == -1234.5f && hs[1].w == -1234.5f) asm volatile("trap;");
-        trow[3] = clock64();
-      }
+      if (tr) trow[2] = clock64();
       const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
       if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
         for (uint32_t k0 = U; k0 < dmax; k0 += U) {
@@ -414,9 +420,10 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
         mm[0] = make_float4(m0.x, m0.y, m1.x, m1.y);
         mm[1] = make_float4(m2.x, m2.y, m3.x, m3.y);
       }
-      if (tr) trow[4] = clock64();
+      if (r >= n) hs[0] = hs[1] = mm[0] = mm[1] = make_float4(0.f, 0.f, 0.f, 0.f);  // rows past n
+      if (tr) trow[3] = clock64();
       ptx::mbar_wait(&empty[s], ph ^ 1);
-      if (tr) trow[5] = clock64();
+      if (tr) trow[4] = clock64();
       uint8_t* st = sA + s * kStageBytes;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -425,7 +432,7 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&full[s]);
-      if (tr) trow[6] = clock64();
+      if (tr) trow[5] = clock64();
       b0 = b1;
       d0 = d1;
       c0 = c1;
@@ -441,17 +448,8 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
     // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
     const uint32_t q = warp;
     uint8_t* ew = sE + q * 4096;
-    const uint64_t pol = ptx::policy_evict_first();
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
-    // Warp 0 lane 0 issues the MMAs one tile ahead of its epilogue: iteration
-    // it issues MMA(it), then every epilogue warp drains tile it-1.
-    for (uint32_t it = 0; it <= my_tiles; ++it) {
-      if (warp == 0) {
-        if (lane == 0 && it < my_tiles) issue_mma(it);
-        __syncwarp();
-      }
-      if (it == 0) continue;
-      const uint32_t e = it - 1;
+    for (uint32_t e = 0; e < my_tiles; ++e) {
       const uint32_t t = blockIdx.x + e * G;
       const uint32_t acc = e & 1, ph = (e >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], ph);
@@ -467,22 +465,21 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + hw.bias[i], 0.0f);
       const uint32_t row0 = t * kTileM + q * 32;
       if (!kLast) {
+        // Stage the warp's 32 rows in the SWIZZLE_128B layout (conflict-free STS)
+        // and let the TMA engine store them: one cp.async.bulk.tensor per warp
+        // per tile instead of a shared-memory read-back and 8 STG per thread.
+        if (lane == 0) ptx::bulk_wait_read0();  // previous tile's store has read the buffer
+        __syncwarp();
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<float4*>(ew + lane * 128 + ((c ^ (lane & 7)) << 4)) =
               make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+        ptx::fence_proxy_async_smem();
         __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t ri = k * 4 + (lane >> 3), c = lane & 7;
-          const float4 v = *reinterpret_cast<const float4*>(ew + ri * 128 + ((c ^ (ri & 7)) << 4));
-          if (row0 + ri < n) {
-            float* dst = a.hout + static_cast<size_t>(row0 + ri) * kF + 4 * c;
-            if (a.evict_first_out) ptx::stg_f4_hint(dst, v, pol);
-            else *reinterpret_cast<float4*>(dst) = v;
-          }
+        if (lane == 0) {
+          ptx::tma_store_2d(&tmap_out, ew, 0, static_cast<int32_t>(row0));
+          ptx::bulk_commit();
         }
-        __syncwarp();
       } else {
         // head 32 -> classes (weights in the constant bank), first-max argmax
         const uint32_t row = row0 + lane;
@@ -503,11 +500,12 @@ __global__ void __maxnreg__(96) sage_layer_tc_kernel(const LayerArgs a, const He
       }
       if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 15] = clock64();
     }
+    if (!kLast && lane == 0) ptx::bulk_wait_all();  // global writes of the last stores done
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem_base);
   }
@@ -916,6 +914,31 @@ static void ensure_activations(groot_graph* g) {
     if (b.n < need) b.alloc(need);
 }
 
+// TMA descriptor for an n x 32 fp32 row-major activation matrix: 32 x 32
+// boxes, SWIZZLE_128B (matches the epilogue's staging layout).
+static CUtensorMap make_rows32_tmap(float* base, uint32_t n) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    GROOT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(GROOT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {kF, n};
+  const cuuint64_t strides[1] = {kF * sizeof(float)};
+  const cuuint32_t box[2] = {kF, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GROOT_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
 static void set_tc_smem() {
   static bool done = false;
   if (done) return;
@@ -967,8 +990,9 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     a.hd = hd;
     a.head = m->head.p;
     a.classes = m->classes;
-    a.pf_waves = env_u32("GROOT_PF_WAVES", 0);
-    a.evict_first_out = static_cast<int>(env_u32("GROOT_EVICT_FIRST", 1));
+    // L2 prefetch two waves ahead helps the inner layers (11.9 -> 11.35 ms at
+    // 1024-bit b16) but slows the last one (no output stream): off there.
+    a.pf_waves = (l + 1 == m->depth) ? 0u : env_u32("GROOT_PF_WAVES", 2);
     a.cls = cls;
     a.logits = logits;
     a.labels = g->labels.p;
@@ -981,14 +1005,15 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
       a.trace = trace.p;
     }
     const unsigned grid = std::min<uint32_t>(ntiles, sms);
+    const CUtensorMap tmap = make_rows32_tmap(hout, n);
     HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
     std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
     if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw);
+      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw, tmap);
     } else {
       ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw);
+      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw, tmap);
     }
     if (a.trace) {
       std::vector<unsigned long long> h(64 * 16);
