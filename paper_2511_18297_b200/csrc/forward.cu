@@ -3,11 +3,16 @@
 // Reference: run_forward / predict_full (src/gnn.cpp:37-52, 259-300) over the
 // degree-polarised SpMM (src/spmm.cpp:37-127, inc/spmm.hpp:106-181).
 //
-// Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel does
-//   gather (LD rows)  ->  [h | mean(h_N)] tile in smem (TF32 hi/lo split)
-//   -> tcgen05.mma kind::tf32 (3 products: hi*hi + hi*lo + lo*hi) into TMEM
-//   -> tcgen05.ld epilogue: + bias, ReLU, coalesced store (or, in the last
-//      layer, the 32 -> classes head + first-max argmax + confusion counts).
+// Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel per SM:
+//   TMA warp      streams each 128-row tile (feature rows, row_ptr slice,
+//                 col_idx range) into a shared-memory ring, waves ahead
+//   8 producers   neighbour gather (32-byte L2 loads, software-pipelined one
+//                 tile ahead) + mean, TF32 hi/lo split of [h | mean(h_N)]
+//                 written straight into tensor memory (tcgen05.st)
+//   MMA warp      tcgen05.mma kind::tf32, A from TMEM, W from smem, 3 products
+//                 (hi*hi + hi*lo + lo*hi) into a double-buffered accumulator
+//   4 epilogue    tcgen05.ld, + bias, ReLU, TMA tensor store (or, in the last
+//                 layer, the 32 -> classes head + first-max argmax)
 // High-degree rows (the row classifier's HD band; the PIs of a multiplier)
 // are aggregated first by a CTA-per-row kernel with a fixed-order reduction.
 // Layer 0 (4 -> 32, inputs in {0,1}^4) is a gather + FFMA kernel.
@@ -25,26 +30,48 @@ namespace groot {
 
 constexpr int kF = 32;                       // hidden width (tensor-core layers)
 constexpr int kTileM = 128;                  // rows per MMA tile (UMMA M)
-constexpr int kEpiWarps = 4;                 // warps 0..3: TMEM lane quadrants; warp 0 lane 0 issues MMA
-constexpr int kProdWarps = 16;               // warps 4..19: gather producers (8 rows each)
-// 20 warps = 5 per SM sub-partition: 5 x 96 regs x 32 lanes fits one sub-partition's
-// 16K registers (a 21st warp would force the cap down to 80 registers).
-constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 20: TMEM alloc + tcgen05.mma issue
-// 21 warps: sub-partition 0 holds 6 of them, so its 16K registers cap the
-// kernel at 80 registers/thread (6 x 80 x 32 = 15360).
-constexpr int kThreads = (kMmaWarp + 1) * 32;  // 672
+constexpr int kEpiWarps = 4;                 // warps 0..3: accumulator drain (TMEM lane quadrant = warp)
+constexpr int kProdWarps = 8;                // warps 4..11: gather producers, 16 rows each
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 12: TMEM alloc + tcgen05.mma issue
+constexpr int kLoadWarp = kMmaWarp + 1;           // warp 13: TMA loads of the input tiles
+// 16 warps = 4 warpgroups: epilogue | producers | producers | MMA, loader, 2 idle.
+// Launched at 128 registers/thread (4 warps x 128 x 32 fills a sub-partition's
+// 16K registers); setmaxnreg then moves registers to the producers:
+// per sub-partition 72 + 2 x 200 + 40 = 512.
+constexpr int kThreads = 16 * 32;  // 512
+constexpr uint32_t kEpiRegs = 72, kProdRegs = 200, kCtlRegs = 40;
+static_assert(kEpiRegs + 2 * kProdRegs + kCtlRegs <= 512, "register file per sub-partition");
 constexpr int kStages = 3;
-constexpr uint32_t kTileBytes = kTileM * 128;     // 128 rows x 32 fp32
-constexpr uint32_t kStageBytes = 4 * kTileBytes;  // h_hi, h_lo, m_hi, m_lo
+// Tensor memory (512 columns x 128 lanes x 32 bit): the A operand lives there,
+// so the gather never goes through a shared-memory operand tile. Stage s owns
+// columns [128s, 128s+128): h_hi | m_hi | h_lo | m_lo (32 columns each, K
+// order permuted, see kcol_feature); the two accumulators follow.
+constexpr uint32_t kStageCols = 128;
+constexpr uint32_t kAccCols = 32;
+constexpr uint32_t kAccCol0 = kStages * kStageCols;  // 384
+constexpr uint32_t kTmemCols = 512;
+static_assert(kAccCol0 + 2 * kAccCols <= kTmemCols, "tensor memory budget");
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
 constexpr int kMaxClasses = 8;
-constexpr uint32_t kAccCols = 32;                 // one fp32 accumulator of 32 columns
-constexpr uint32_t kTmemCols = 2 * kAccCols;      // double-buffered
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBBytes + kEpiBytes +
-                                (kF * kMaxClasses + kMaxClasses + kF) * 4 + 16 * 8 + 4 + 25 * 4 + 4 * kStages +
-                                1024;
+// Input ring: per tile the 128 feature rows (TMA, SWIZZLE_128B), row_ptr
+// [row0, row0+129) and, when it fits, the tile's col_idx range.
+constexpr int kInStages = 6;
+constexpr uint32_t kColCap = 1024;                // col_idx entries staged per tile
+constexpr uint32_t kInRpOff = kTileM * 128;       // 16384
+constexpr uint32_t kInColOff = kInRpOff + 640;    // row_ptr: 132 entries, padded
+constexpr uint32_t kInStageBytes = ((kInColOff + kColCap * 4 + 1023) / 1024) * 1024;
+constexpr uint32_t kSmemBytes = kInStages * kInStageBytes + kBBytes + kEpiBytes + 256 * 4 + 8 * kInStages +
+                                8 * (2 * kStages + 4 + 2 * kInStages) + 16 + 1024;
 static_assert(kSmemBytes <= 232448, "fused layer exceeds the 227 KB shared-memory limit");
+
+// Column c (0..31) of an A block in tensor memory holds input feature
+// kcol_feature(c): lane j of a row's 4-lane group loads features 8j..8j+7
+// (one 32-byte load) and 16x256b stores put its values in columns 8i+2j+e.
+// The weight image permutes B's K rows the same way, so A.B is unchanged.
+__host__ __device__ constexpr uint32_t kcol_feature(uint32_t c) {
+  return ((c >> 1) & 3u) * 8u + (c >> 3) * 2u + (c & 1u);
+}
 
 static uint32_t env_u32(const char* name, uint32_t dflt) {
   const char* e = std::getenv(name);
@@ -80,92 +107,9 @@ __device__ __forceinline__ uint32_t hd_slot(const HdInfo& hd, uint32_t row) {
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
+
 __device__ __forceinline__ float4 f4scale(float4 a, float s) {
   return make_float4(a.x * s, a.y * s, a.z * s, a.w * s);
-}
-
-// Mean of neighbour rows for NR rows per 8-lane group (lane j owns columns
-// 4j..4j+3). LD rows: up to 8 neighbours' 128-byte rows are loaded at once per
-// row (coalesced LDG.128 per group), summed in nonzero order, then scaled by
-// 1/deg. HD rows (degree >= threshold) read the precomputed mean. The loop
-// bounds are warp-uniform so shuffles stay convergent.
-template <int NR>
-__device__ __forceinline__ void gather_mean32(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
-                                              const float* __restrict__ H, uint32_t n, const uint32_t (&row)[NR],
-                                              int j, int gbase, const HdInfo& hd, float4 (&m)[NR]) {
-  uint32_t b[NR], d[NR], c[NR];
-  bool is_hd[NR];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    b[q] = 0;
-    d[q] = 0;
-    if (row[q] < n) {
-      b[q] = __ldg(rp + row[q]);
-      d[q] = __ldg(rp + row[q] + 1) - b[q];
-    }
-    is_hd[q] = d[q] >= hd.threshold;
-  }
-  uint32_t dl[NR];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    dl[q] = is_hd[q] ? 0u : d[q];
-    c[q] = (static_cast<uint32_t>(j) < dl[q]) ? __ldg(col + b[q] + j) : 0u;
-  }
-  float4 v[NR][8];
-#pragma unroll
-  for (int q = 0; q < NR; ++q)
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const uint32_t ci = __shfl_sync(0xffffffffu, c[q], gbase + t);
-      v[q][t] = (static_cast<uint32_t>(t) < dl[q]) ? ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    float4 acc = v[q][0];
-#pragma unroll
-    for (int t = 1; t < 8; ++t)
-      if (static_cast<uint32_t>(t) < dl[q]) acc = f4add(acc, v[q][t]);
-    m[q] = acc;
-  }
-  // Rows with 8 < degree < threshold: remaining neighbours, 8 at a time.
-  uint32_t dmax = 0;
-#pragma unroll
-  for (int q = 0; q < NR; ++q) dmax = max(dmax, dl[q]);
-  dmax = __reduce_max_sync(0xffffffffu, dmax);
-  for (uint32_t k = 8; k < dmax; k += 8) {
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const uint32_t cc = (k + j < dl[q]) ? __ldg(col + b[q] + k + j) : 0u;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + t);
-        if (k + t < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j));
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    if (is_hd[q]) {
-      m[q] = ptx::ldg_f4(hd.mean + static_cast<size_t>(hd_slot(hd, row[q])) * kF + 4 * j);
-    } else {
-      const float inv = d[q] > 0 ? 1.0f / static_cast<float>(d[q]) : 0.0f;
-      m[q] = f4scale(m[q], inv);
-    }
-  }
-}
-
-// Store one 16-byte chunk (4 fp32) of a tile row as TF32 hi and lo parts into
-// SWIZZLE_128B K-major layout: chunk j of row i sits at i*128 + ((j ^ (i&7)) << 4).
-__device__ __forceinline__ void store_split(uint8_t* hi_base, uint32_t i, int j, float4 x) {
-  float4 h, l;
-  h.x = ptx::tf32_rna(x.x); l.x = x.x - h.x;
-  h.y = ptx::tf32_rna(x.y); l.y = x.y - h.y;
-  h.z = ptx::tf32_rna(x.z); l.z = x.z - h.z;
-  h.w = ptx::tf32_rna(x.w); l.w = x.w - h.w;
-  const uint32_t off = i * 128u + ((static_cast<uint32_t>(j) ^ (i & 7u)) << 4);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(hi_base + kTileBytes + off) = l;
 }
 
 // Head weights by value: kernel parameters live in the constant bank, so the
@@ -176,21 +120,31 @@ struct HeadW {
   float bias[32];  // this layer's bias (constant-bank operand in the epilogue)
 };
 
-// TF32 split by truncation: hi = x with the low 13 mantissa bits cleared (an
-// exact TF32 value, so the tensor core reads it unchanged whatever its input
-// rounding), lo = x - hi (exact in fp32, Sterbenz). Two ops per element.
-__device__ __forceinline__ void store_split_trunc(uint8_t* hi_base, uint32_t i, uint32_t chunk, float4 x) {
-  float4 h, l;
-  h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-  h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-  h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-  h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-  const float2 l01 = ptx::fsub2(make_float2(x.x, x.y), make_float2(h.x, h.y));
-  const float2 l23 = ptx::fsub2(make_float2(x.z, x.w), make_float2(h.z, h.w));
-  l = make_float4(l01.x, l01.y, l23.x, l23.y);
-  const uint32_t off = i * 128u + ((chunk ^ (i & 7u)) << 4);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(hi_base + kTileBytes + off) = l;
+// TF32 split by truncation of one 16-row slice (rows r, r+8 of the lane's
+// group; lane j holds features 8j..8j+7 of each) into tensor memory: hi = x with
+// the low 13 mantissa bits cleared (an exact TF32 value), lo = x - hi (exact,
+// Sterbenz). Register 4i+2h+e of the 16x256b store is feature 2i+e of row h.
+__device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float4 (&x)[2][2]) {
+  uint32_t hi[16], lo[16];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float f[4] = {x[h][c].x, x[h][c].y, x[h][c].z, x[h][c].w};
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int idx = 4 * (2 * c + p) + 2 * h;  // features 4c+2p, 4c+2p+1
+        const float h0 = __uint_as_float(__float_as_uint(f[2 * p]) & 0xFFFFE000u);
+        const float h1 = __uint_as_float(__float_as_uint(f[2 * p + 1]) & 0xFFFFE000u);
+        const float2 l = ptx::fsub2(make_float2(f[2 * p], f[2 * p + 1]), make_float2(h0, h1));
+        hi[idx] = __float_as_uint(h0);
+        hi[idx + 1] = __float_as_uint(h1);
+        lo[idx] = __float_as_uint(l.x);
+        lo[idx + 1] = __float_as_uint(l.y);
+      }
+    }
+  ptx::tmem_st_16x256b_x4(taddr, hi);
+  ptx::tmem_st_16x256b_x4(taddr + 64, lo);
 }
 
 struct LayerArgs {
@@ -204,7 +158,6 @@ struct LayerArgs {
   HdInfo hd;
   const float* head;     // W_out [32 x classes] row-major, then b_out
   uint32_t classes;
-  uint32_t pf_waves;     // L2 prefetch distance in waves (0 = off)
   unsigned long long* trace;  // diagnostic timeline of CTA 0 (nullptr = off): [64 tiles][16 events]
   uint8_t* cls;          // last layer: n classes
   float* logits;         // last layer: n x classes (optional)
@@ -213,25 +166,26 @@ struct LayerArgs {
 };
 
 template <bool kLast>
-__global__ void __maxnreg__(80) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw,
-                                                      const __grid_constant__ CUtensorMap tmap_out) {
+__global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw,
+                                                       const __grid_constant__ CUtensorMap tmap_in,
+                                                       const __grid_constant__ CUtensorMap tmap_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the SWIZZLE_128B operand tiles, computed on the shared
-  // address so the pointer stays in the shared window (STS, not generic ST).
+  // 1024-B alignment for the SWIZZLE_128B tiles, computed on the shared
+  // address so the pointer stays in the shared window (LDS/STS, not generic).
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + kStages * kStageBytes;
+  uint8_t* sIn = smem;                              // [kInStages] input tiles
+  uint8_t* sB = sIn + kInStages * kInStageBytes;
   uint8_t* sE = sB + kBBytes;
-  float* sHead = reinterpret_cast<float*>(sE + kEpiBytes);
-  float* sBias = sHead + kF * kMaxClasses + kMaxClasses;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + kF);
-  uint64_t* full = bars;                 // [kStages] producers -> MMA
-  uint64_t* empty = bars + kStages;      // [kStages] MMA done reading the stage
-  uint64_t* tfull = bars + 2 * kStages;  // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;          // [2] accumulator drained by the epilogue
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* sConf = sTmem + 1;
-  float* sInv = sHead;  // 1/deg for deg < 256 (correctly rounded, == 1.0f/d)
+  float* sInv = reinterpret_cast<float*>(sE + kEpiBytes);  // 1/deg for deg < 256 (== 1.0f/d)
+  uint32_t* sMeta = reinterpret_cast<uint32_t*>(sInv + 256);  // [kInStages][2]: col base, col in smem
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMeta + 2 * kInStages);
+  uint64_t* full = bars;                     // [kStages] producers -> MMA (A operand in TMEM)
+  uint64_t* empty = full + kStages;          // [kStages] MMA done reading the A stage
+  uint64_t* tfull = empty + kStages;         // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;              // [2] accumulator drained by the epilogue
+  uint64_t* in_full = tempty + 2;            // [kInStages] TMA -> producers
+  uint64_t* in_empty = in_full + kInStages;  // [kInStages] producers done with the input tile
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(in_empty + kInStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n = a.n;
@@ -240,9 +194,7 @@ __global__ void __maxnreg__(80) sage_layer_tc_kernel(const LayerArgs a, const He
 
   for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
-  if (threadIdx.x < kF) sBias[threadIdx.x] = a.bias[threadIdx.x];
   for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
-  if (kLast && threadIdx.x < 25) sConf[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], kProdWarps * 32);
@@ -252,211 +204,283 @@ __global__ void __maxnreg__(80) sage_layer_tc_kernel(const LayerArgs a, const He
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], kEpiWarps * 32);
     }
+    for (int s = 0; s < kInStages; ++s) {
+      ptx::mbar_init(&in_full[s], 1);
+      ptx::mbar_init(&in_empty[s], kProdWarps * 32);
+    }
     ptx::mbar_fence_init();
   }
   if (warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
-  ptx::fence_proxy_async_smem();
+  ptx::fence_proxy_async_smem();  // weight image (generic stores) -> tensor core (async proxy)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *sTmem;
 
-  // tcgen05.mma issue for tile `it` (one thread): 3xTF32 [h|m] x [Ws;Wn] into TMEM.
-  constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
-  const uint32_t a0 = ptx::smem_addr(sA), b0s = ptx::smem_addr(sB);
-  auto issue_mma = [&](uint32_t it) {
-    const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-    const uint32_t acc = it & 1, aph = (it >> 1) & 1;
-    unsigned long long* trow = (a.trace && blockIdx.x == 0 && it < 64) ? a.trace + it * 16 + 10 : nullptr;
-    if (trow) trow[0] = clock64();
-    ptx::mbar_wait(&full[s], ph);
-    if (trow) trow[1] = clock64();
-    ptx::mbar_wait(&tempty[acc], aph ^ 1);
-    if (trow) trow[2] = clock64();
-    ptx::tc_fence_after();
-    const uint32_t d = tmem_base + acc * kAccCols;
-#pragma unroll
-    for (uint32_t kb = 0; kb < 2; ++kb)
-#pragma unroll
-      for (uint32_t kk = 0; kk < 4; ++kk) {
-        const uint32_t ao = a0 + s * kStageBytes + kb * 2 * kTileBytes + kk * 32;
-        const uint32_t bo = b0s + kb * 8192 + kk * 32;
-        const uint64_t ahi = ptx::umma_desc_sw128(ao), alo = ptx::umma_desc_sw128(ao + kTileBytes);
-        const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
-        const uint32_t first = (kb | kk) != 0;
-        ptx::mma_tf32(d, ahi, bhi, idesc, first);
-        ptx::mma_tf32(d, ahi, blo, idesc, 1);
-        ptx::mma_tf32(d, alo, bhi, idesc, 1);
-      }
-    ptx::mma_commit(&empty[s]);
-    ptx::mma_commit(&tfull[acc]);
-    if (trow) trow[3] = clock64();
-  };
-
-  if (warp == kMmaWarp) {
-    // ===== MMA issuer: one elected thread, decoupled from producers and epilogue =====
+  if (warp >= kMmaWarp) ptx::setmaxnreg_dec<kCtlRegs>();  // warpgroup 3: MMA issuer, TMA loader, 2 idle
+  if (warp == kLoadWarp) {
+    // ===== TMA loader: tile t's feature rows (swizzled), row_ptr slice and
+    // col_idx range into the input ring, kInStages tiles (waves) ahead =====
     if (lane == 0) {
+      // row_ptr bounds of the tiles kBoundsAhead iterations ahead are in flight
+      // (a ring in registers), so their DRAM latency is never on the loop.
+      constexpr int kBoundsAhead = 8;
+      auto bounds = [&](uint32_t tt, uint32_t& b, uint32_t& e) {
+        b = e = 0;
+        if (tt < ntiles) {
+          b = __ldg(a.rp + tt * kTileM);
+          e = __ldg(a.rp + min(tt * kTileM + kTileM, n));
+        }
+      };
+      uint32_t qb[kBoundsAhead], qe[kBoundsAhead];
+#pragma unroll
+      for (int k = 0; k < kBoundsAhead; ++k) bounds(blockIdx.x + k * G, qb[k], qe[k]);
       uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) issue_mma(it);
+      for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        const uint32_t s = it % kInStages, ph = (it / kInStages) & 1;
+        const uint32_t cb0 = qb[0], ce0 = qe[0];
+#pragma unroll
+        for (int k = 0; k + 1 < kBoundsAhead; ++k) {
+          qb[k] = qb[k + 1];
+          qe[k] = qe[k + 1];
+        }
+        bounds(t + kBoundsAhead * G, qb[kBoundsAhead - 1], qe[kBoundsAhead - 1]);
+        ptx::mbar_wait_sleep(&in_empty[s], ph ^ 1);
+        uint8_t* st = sIn + s * kInStageBytes;
+        const uint32_t row0 = t * kTileM;
+        const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - row0);
+        const uint32_t rcnt = (rows + 1 + 3) & ~3u;  // row_ptr entries (16-byte multiple; 16 B of slack)
+        const uint32_t cb = cb0 & ~3u;
+        const uint32_t ccnt = (ce0 - cb + 3) & ~3u;
+        const bool col_smem = ccnt <= kColCap;  // tiles holding high-degree rows read col_idx from global
+        sMeta[2 * s] = cb;
+        sMeta[2 * s + 1] = col_smem;
+        const uint32_t tx = kTileM * 128u + rcnt * 4u + (col_smem ? ccnt * 4u : 0u);
+        ptx::mbar_arrive_expect_tx(&in_full[s], tx);
+        ptx::tma_load_2d(&tmap_in, st, &in_full[s], 0, static_cast<int32_t>(row0));
+        ptx::bulk_load(st + kInRpOff, a.rp + row0, rcnt * 4u, &in_full[s]);
+        if (col_smem && ccnt) ptx::bulk_load(st + kInColOff, a.col + cb, ccnt * 4u, &in_full[s]);
+      }
     }
     __syncwarp();
-  } else if (warp >= kEpiWarps) {
-    // ===== gather producers =====
-    // 16 warps x 8 rows = one 128-row tile per pass; 4 lanes per row, lane j
-    // owns features 8j..8j+7 (two LDG.128 per neighbour), so the per-row index
-    // work (shuffles, predicates, 1/deg) is shared by 4 lanes, and the sums use
-    // packed f32x2 adds. Rolling index pipeline: while the feature gathers of
-    // tile t are in flight, col_idx of tile t+G and row_ptr of tile t+2G load.
-    const int pw = warp - kEpiWarps;
-    const int j = lane & 3, gbase = lane & ~3;
-    const uint32_t li = pw * 8 + (lane >> 2);  // tile-local row of this lane group
-    const uint32_t thr = a.hd.threshold;
-    const float* hin_j = a.hin + 8 * j;
-    auto rp_load = [&](uint32_t tt, uint32_t& b, uint32_t& e) {
-      const uint32_t r = tt * kTileM + li;
-      const bool ok = tt < ntiles && r < n;
-      b = ok ? __ldg(a.rp + r) : 0u;
-      e = ok ? __ldg(a.rp + r + 1) : 0u;
-    };
-    auto col_load = [&](uint32_t b, uint32_t d) {
-      return (static_cast<uint32_t>(j) < d && d < thr) ? __ldg(a.col + b + j) : 0u;
-    };
-    // Index pipeline state: tile t (b0,d0,c0), t+G (b1,d1,c1), t+2G (b2,d2),
-    // raw row_ptr of t+3G (b3,e3) and t+4G (loaded this iteration). col_idx is
-    // loaded 2 tiles ahead and row_ptr 4 tiles ahead of use, so neither load
-    // sits on the per-tile critical path even at loaded DRAM latency.
-    uint32_t b0, d0, c0, b1, d1, c1, b2, d2, b3, e3;
-    {
-      uint32_t e;
-      rp_load(blockIdx.x, b0, e);
-      d0 = e - b0;
-      rp_load(blockIdx.x + G, b1, e);
-      d1 = e - b1;
-      rp_load(blockIdx.x + 2 * G, b2, e);
-      d2 = e - b2;
-      rp_load(blockIdx.x + 3 * G, b3, e3);
-      c0 = col_load(b0, d0);
-      c1 = col_load(b1, d1);
-    }
-    constexpr int U = 4;  // neighbours per row in one burst (CSA LD rows have degree <= 4)
+  } else if (warp == kMmaWarp) {
+    // ===== MMA issuer: the whole warp runs the loop (warp-uniform operands
+    // stay in uniform registers), one elected lane issues. A from tensor
+    // memory, B from shared memory =====
+    constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
+    const uint32_t b0s = ptx::smem_addr(sB);
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      if (pw == 0 && lane == 0 && a.pf_waves) {
-        // L2 prefetch of the feature rows pf_waves waves ahead (first touches of fanout rows).
-        const uint32_t tp = t + a.pf_waves * G;
-        if (tp < ntiles) {
-          const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - tp * kTileM);
-          ptx::prefetch_l2(a.hin + static_cast<size_t>(tp) * kTileM * kF, rows * 128u);
-        }
+      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+      unsigned long long* trow =
+          (a.trace && blockIdx.x == 0 && lane == 0 && it < 64) ? a.trace + it * 16 + 10 : nullptr;
+      if (trow) trow[0] = clock64();
+      ptx::mbar_wait(&full[s], ph);
+      if (trow) trow[1] = clock64();
+      ptx::mbar_wait(&tempty[acc], aph ^ 1);
+      if (trow) trow[2] = clock64();
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        const uint32_t d = tmem_base + kAccCol0 + acc * kAccCols;
+        const uint32_t as = tmem_base + s * kStageCols;
+#pragma unroll
+        for (uint32_t kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint32_t ahi = as + kb * 32 + kk * 8;  // h (kb 0) or m (kb 1), K = 8 columns
+            const uint32_t bo = b0s + kb * 8192 + kk * 32;
+            const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
+            const uint32_t first = (kb | kk) != 0;
+            ptx::mma_tf32_ts(d, ahi, bhi, idesc, first);
+            ptx::mma_tf32_ts(d, ahi, blo, idesc, 1);
+            ptx::mma_tf32_ts(d, ahi + 64, bhi, idesc, 1);
+          }
+        ptx::mma_commit(&empty[s]);
+        ptx::mma_commit(&tfull[acc]);
       }
-      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && pw == 0 && it < 64;
+      __syncwarp();
+      if (trow) trow[3] = clock64();
+    }
+  } else if (warp >= kEpiWarps && warp < kMmaWarp) {
+    // ===== gather producers (two warpgroups, 192 registers per thread) =====
+    // 8 warps x 16 rows = one 128-row tile per pass. A warp may only reach its
+    // TMEM lane quadrant (warp % 4), so warp w owns tile rows 32(w%4) + 16h ..
+    // +15 with h = (w-4)/4. Lane group r = lane/4 owns rows r and r+8 of that
+    // slice; lane j = lane%4 holds features 8j..8j+7, exactly the registers a
+    // 16x256b tcgen05.st takes (A's K order permuted to match, kcol_feature).
+    // row_ptr, col_idx and the row's own features come from the TMA-filled
+    // input tile (swizzled 128-B rows: chunk c of row i at i*128 + ((c ^
+    // (i&7)) << 4)). Each neighbour slot is ONE generic load per 16 bytes:
+    // a shared-window address for rows inside the tile, a global address
+    // (an L2 hit: the tile ring streams a few waves ahead) otherwise.
+    // Software pipeline, two tiles deep: the neighbour loads of tile t+G are
+    // issued before tile t is consumed (register sets A and B alternate).
+    ptx::setmaxnreg_inc<kProdRegs>();
+    const uint32_t lbase = (warp & 3) * 32 + ((warp - kEpiWarps) >> 2) * 16;
+    const int j = lane & 3, gbase = lane & ~3;
+    const uint32_t li = lbase + (lane >> 2);  // tile rows li and li + 8
+    const uint32_t thr = a.hd.threshold;
+    const float* hin_j = a.hin + 8 * j;
+    constexpr int U = 4;  // neighbour slots per row (CSA LD rows have degree <= 4; more -> tail loop)
+    struct Slots {
+      float4 v[2][U][2];
+      uint32_t d[2];  // degrees of the two rows
+    };
+    // wait for tile t's input, read its row_ptr / col_idx, issue all neighbour
+    // loads (slots past the degree re-read the row itself from shared memory)
+    auto issue = [&](uint32_t it, uint32_t t, Slots& L) {
+      const uint32_t si = it % kInStages;
+      const uint32_t row0 = t * kTileM;
+      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarps && it < 64;
       unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
-      if (tr) trow[0] = clock64();
-      const uint32_t dl = d0 < thr ? d0 : 0u;
-      const uint32_t r = t * kTileM + li;
-      // Burst: U neighbour lines + the self line per row, all independent and
-      // unconditional (slots past the degree re-read the row's own line): a
-      // conditional load makes the compiler merge registers with moves that
-      // wait on the first loads and split the burst into two round trips.
-      // The burst is not software-pipelined across tiles on purpose: the proxy
-      // fence before the stage hand-off (MEMBAR.ALL.CTA) waits for every
-      // outstanding load of the thread, which would serialise it anyway.
-      const uint32_t self = r < n ? r : 0u;
-      float4 v[U][2], hs[2];
+      if (tr) trow[6] = clock64();
+      ptx::mbar_wait(&in_full[si], (it / kInStages) & 1);
+      if (tr) trow[7] = clock64();
+      const uint8_t* st = sIn + si * kInStageBytes;
+      const uint32_t* sRp = reinterpret_cast<const uint32_t*>(st + kInRpOff);
+      const uint32_t* sCol = reinterpret_cast<const uint32_t*>(st + kInColOff);
+      const uint32_t cb = sMeta[2 * si];
+      const bool col_smem = sMeta[2 * si + 1] != 0;
+      uint32_t c[2], dl[2];
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t ci = __shfl_sync(0xffffffffu, c0, gbase + k);
-        const uint32_t src = static_cast<uint32_t>(k) < dl ? ci : self;
-        ptx::ldg_f8(hin_j + static_cast<size_t>(src) * kF, v[k][0], v[k][1]);
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t il = li + 8 * h;
+        const bool ok = row0 + il < n;
+        const uint32_t b = ok ? sRp[il] : 0u;
+        L.d[h] = ok ? sRp[il + 1] - b : 0u;
+        dl[h] = L.d[h] < thr ? L.d[h] : 0u;
+        c[h] = 0u;
+        if (static_cast<uint32_t>(j) < dl[h]) c[h] = col_smem ? sCol[b - cb + j] : __ldg(a.col + b + j);
       }
-      ptx::ldg_f8(hin_j + static_cast<size_t>(self) * kF, hs[0], hs[1]);
-      // index loads for later tiles (in flight with the burst)
-      const uint32_t c2 = col_load(b2, d2);
-      uint32_t b4, e4;
-      rp_load(t + 4 * G, b4, e4);
-      if (tr) trow[1] = clock64();
-      // consume in nonzero order with packed f32x2 adds
-      float2 m0 = make_float2(0.f, 0.f), m1 = m0, m2 = m0, m3 = m0;
+      if (tr) trow[8] = clock64() + (c[0] & 0u);  // after the col_idx values arrived
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (static_cast<uint32_t>(k) < dl) {
-          m0 = ptx::fadd2(m0, make_float2(v[k][0].x, v[k][0].y));
-          m1 = ptx::fadd2(m1, make_float2(v[k][0].z, v[k][0].w));
-          m2 = ptx::fadd2(m2, make_float2(v[k][1].x, v[k][1].y));
-          m3 = ptx::fadd2(m3, make_float2(v[k][1].z, v[k][1].w));
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t il = li + 8 * h;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const uint32_t ci = __shfl_sync(0xffffffffu, c[h], gbase + k);
+          const uint32_t src = static_cast<uint32_t>(k) < dl[h] ? ci : min(row0 + il, n - 1);
+          ptx::ldg_f8(hin_j + static_cast<size_t>(src) * kF, L.v[h][k][0], L.v[h][k][1]);
         }
-      if (tr) trow[2] = clock64();
-      const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
-      if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
-        for (uint32_t k0 = U; k0 < dmax; k0 += U) {
-          const uint32_t cc = (k0 + j < dl) ? __ldg(a.col + b0 + k0 + j) : 0u;
+      }
+      if (tr) trow[9] = clock64();
+    };
+    // sum, mean, self features, TF32 split into the A stage, hand to the MMA
+    auto consume = [&](uint32_t it, uint32_t t, Slots& L) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+      const uint32_t si = it % kInStages;
+      const uint32_t row0 = t * kTileM;
+      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarps && it < 64;
+      unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
+      if (tr) trow[0] = trow[1] = trow[2] = clock64();
+      const uint8_t* st = sIn + si * kInStageBytes;
+      uint32_t dl[2];
 #pragma unroll
-          for (int kk = 0; kk < U; ++kk) {
-            const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + kk);
-            if (k0 + kk < dl) {
-              float4 x0, x1;
-              ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, x0, x1);
-              m0 = ptx::fadd2(m0, make_float2(x0.x, x0.y));
-              m1 = ptx::fadd2(m1, make_float2(x0.z, x0.w));
-              m2 = ptx::fadd2(m2, make_float2(x1.x, x1.y));
-              m3 = ptx::fadd2(m3, make_float2(x1.z, x1.w));
+      for (int h = 0; h < 2; ++h) dl[h] = L.d[h] < thr ? L.d[h] : 0u;
+      float2 m[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m[h][q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (static_cast<uint32_t>(k) < dl[h]) {
+            m[h][0] = ptx::fadd2(m[h][0], make_float2(L.v[h][k][0].x, L.v[h][k][0].y));
+            m[h][1] = ptx::fadd2(m[h][1], make_float2(L.v[h][k][0].z, L.v[h][k][0].w));
+            m[h][2] = ptx::fadd2(m[h][2], make_float2(L.v[h][k][1].x, L.v[h][k][1].y));
+            m[h][3] = ptx::fadd2(m[h][3], make_float2(L.v[h][k][1].z, L.v[h][k][1].w));
+          }
+      }
+      const uint32_t dmax = __reduce_max_sync(0xffffffffu, max(dl[0], dl[1]));
+      if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
+        const uint32_t* sRp = reinterpret_cast<const uint32_t*>(st + kInRpOff);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t b = dl[h] ? sRp[li + 8 * h] : 0u;
+          for (uint32_t k0 = U; k0 < dmax; k0 += U) {
+            const uint32_t cc = (k0 + j < dl[h]) ? __ldg(a.col + b + k0 + j) : 0u;
+#pragma unroll
+            for (int kk = 0; kk < U; ++kk) {
+              const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + kk);
+              if (k0 + kk < dl[h]) {
+                float4 x0, x1;
+                ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, x0, x1);
+                m[h][0] = ptx::fadd2(m[h][0], make_float2(x0.x, x0.y));
+                m[h][1] = ptx::fadd2(m[h][1], make_float2(x0.z, x0.w));
+                m[h][2] = ptx::fadd2(m[h][2], make_float2(x1.x, x1.y));
+                m[h][3] = ptx::fadd2(m[h][3], make_float2(x1.z, x1.w));
+              }
             }
           }
         }
       }
-      float4 mm[2];
-      if (d0 >= thr) {
-        const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
-        mm[0] = ptx::ldg_f4(src);
-        mm[1] = ptx::ldg_f4(src + 4);
-      } else {
-        const float inv = sInv[d0];
-        const float2 iv = make_float2(inv, inv);
-        m0 = ptx::fmul2(m0, iv);
-        m1 = ptx::fmul2(m1, iv);
-        m2 = ptx::fmul2(m2, iv);
-        m3 = ptx::fmul2(m3, iv);
-        mm[0] = make_float4(m0.x, m0.y, m1.x, m1.y);
-        mm[1] = make_float4(m2.x, m2.y, m3.x, m3.y);
+      float4 hs[2][2], mm[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t il = li + 8 * h;
+        hs[h][0] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j) ^ (il & 7u)) << 4));
+        hs[h][1] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j + 1u) ^ (il & 7u)) << 4));
       }
-      if (r >= n) hs[0] = hs[1] = mm[0] = mm[1] = make_float4(0.f, 0.f, 0.f, 0.f);  // rows past n
+      // the input tile is no longer read by this thread
+      ptx::mbar_arrive(&in_empty[si]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t r = row0 + li + 8 * h;
+        if (L.d[h] >= thr) {
+          const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
+          mm[h][0] = ptx::ldg_f4(src);
+          mm[h][1] = ptx::ldg_f4(src + 4);
+        } else {
+          const float inv = sInv[L.d[h]];
+          const float2 iv = make_float2(inv, inv);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m[h][q] = ptx::fmul2(m[h][q], iv);
+          mm[h][0] = make_float4(m[h][0].x, m[h][0].y, m[h][1].x, m[h][1].y);
+          mm[h][1] = make_float4(m[h][2].x, m[h][2].y, m[h][3].x, m[h][3].y);
+        }
+        if (r >= n) hs[h][0] = hs[h][1] = mm[h][0] = mm[h][1] = make_float4(0.f, 0.f, 0.f, 0.f);  // rows past n
+      }
       if (tr) trow[3] = clock64();
       ptx::mbar_wait(&empty[s], ph ^ 1);
+      ptx::tc_fence_after();
       if (tr) trow[4] = clock64();
-      uint8_t* st = sA + s * kStageBytes;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        store_split_trunc(st, li, 2 * j + c, hs[c]);                  // K block 0: self features
-        store_split_trunc(st + 2 * kTileBytes, li, 2 * j + c, mm[c]);  // K block 1: neighbour mean
-      }
-      ptx::fence_proxy_async_smem();
+      const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
+      tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
+      tmem_store_split(ta + 32, mm);  // columns 32..63 (hi), 96..127 (lo): neighbour mean
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
       ptx::mbar_arrive(&full[s]);
       if (tr) trow[5] = clock64();
-      b0 = b1;
-      d0 = d1;
-      c0 = c1;
-      b1 = b2;
-      d1 = d2;
-      c1 = c2;
-      b2 = b3;
-      d2 = e3 - b3;
-      b3 = b4;
-      e3 = e4;
+    };
+    Slots A, B;
+    uint32_t it = 0, t = blockIdx.x;
+    if (t < ntiles) issue(0, t, A);
+    while (t < ntiles) {
+      if (t + G < ntiles) issue(it + 1, t + G, B);
+      consume(it, t, A);
+      t += G;
+      ++it;
+      if (t >= ntiles) break;
+      if (t + G < ntiles) issue(it + 1, t + G, A);
+      consume(it, t, B);
+      t += G;
+      ++it;
     }
-  } else {
+  } else if (warp < kEpiWarps) {
     // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
+    ptx::setmaxnreg_dec<kEpiRegs>();
     const uint32_t q = warp;
     uint8_t* ew = sE + q * 4096;
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
     for (uint32_t e = 0; e < my_tiles; ++e) {
       const uint32_t t = blockIdx.x + e * G;
       const uint32_t acc = e & 1, ph = (e >> 1) & 1;
-      ptx::mbar_wait(&tfull[acc], ph);
+      ptx::mbar_wait_sleep(&tfull[acc], ph);
       if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 14] = clock64();
       ptx::tc_fence_after();
       float r[32];
-      const uint32_t tq = tmem_base + acc * kAccCols + ((q * 32u) << 16);
+      const uint32_t tq = tmem_base + kAccCol0 + acc * kAccCols + ((q * 32u) << 16);
       ptx::tmem_ld_32x32b_x32(tq, r);
 
       ptx::tc_fence_before();
@@ -914,9 +938,10 @@ static void ensure_activations(groot_graph* g) {
     if (b.n < need) b.alloc(need);
 }
 
-// TMA descriptor for an n x 32 fp32 row-major activation matrix: 32 x 32
-// boxes, SWIZZLE_128B (matches the epilogue's staging layout).
-static CUtensorMap make_rows32_tmap(float* base, uint32_t n) {
+// TMA descriptor for an n x 32 fp32 row-major activation matrix: 32 x box_rows
+// boxes, SWIZZLE_128B (chunk c of row i at i*128 + ((c ^ (i&7)) << 4)); rows
+// past n read as zeros.
+static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -930,7 +955,7 @@ static CUtensorMap make_rows32_tmap(float* base, uint32_t n) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {kF, n};
   const cuuint64_t strides[1] = {kF * sizeof(float)};
-  const cuuint32_t box[2] = {kF, 32};
+  const cuuint32_t box[2] = {kF, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -944,6 +969,11 @@ static void set_tc_smem() {
   if (done) return;
   GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  // Smallest shared-memory carve-out that fits: the rest of the 256 KB array is
+  // L1, which catches the in-tile neighbour re-reads of the gather.
+  const int pct = static_cast<int>((kSmemBytes + 1024) * 100 / (228 * 1024)) + 1;
+  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   done = true;
 }
 
@@ -990,9 +1020,6 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     a.hd = hd;
     a.head = m->head.p;
     a.classes = m->classes;
-    // L2 prefetch two waves ahead helps the inner layers (11.9 -> 11.35 ms at
-    // 1024-bit b16) but slows the last one (no output stream): off there.
-    a.pf_waves = (l + 1 == m->depth) ? 0u : env_u32("GROOT_PF_WAVES", 2);
     a.cls = cls;
     a.logits = logits;
     a.labels = g->labels.p;
@@ -1005,15 +1032,16 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
       a.trace = trace.p;
     }
     const unsigned grid = std::min<uint32_t>(ntiles, sms);
-    const CUtensorMap tmap = make_rows32_tmap(hout, n);
+    const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
+    const CUtensorMap tmap = make_rows32_tmap(hout, n, 32);
     HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
     std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
     if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw, tmap);
+      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw, tmap_in, tmap);
     } else {
       ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw, tmap);
+      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw, tmap_in, tmap);
     }
     if (a.trace) {
       std::vector<unsigned long long> h(64 * 16);
@@ -1134,7 +1162,7 @@ void model_upload(groot_model* m) {
         const double* W = kb ? wn : ws;
         for (uint32_t nn = 0; nn < 32; ++nn)
           for (uint32_t k = 0; k < 32; ++k) {
-            const float v = static_cast<float>(W[k * H + nn]);
+            const float v = static_cast<float>(W[kcol_feature(k) * H + nn]);  // K row k <- feature
             const float hi = tf32_rna_host(v), lo = v - hi;
             const uint32_t o = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
             std::memcpy(base + kb * 8192 + o, &hi, 4);
