@@ -290,7 +290,8 @@ def run_ours(args):
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-                traffic = json.load(f).get("sage_layer_tc", {}).get("dram_bytes_per_launch")
+                summ = json.load(f)
+                traffic = summ.get("kernels", {}).get("sage_layer_tc", {}).get("dram_bytes_per_launch")
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -1,0 +1,78 @@
+"""Build profiles/ncu_summary.json from `ncu --set full` reports.
+
+usage: python scripts/make_profile_summary.py ROUND OUT.json REPORT [REPORT ...]
+
+Per kernel (first capture of each name): duration, DRAM bytes read/written
+(the `traffic` figure bench.py reports), throughput percentages, launch
+shape, and for the fused layer the top SASS lines by warp-stall samples.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import ncu_summary as N  # noqa: E402
+
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def short_name(k):
+    if "sage_layer_tc_kernel" in k:
+        return "sage_layer_tc_last" if ("(bool)1" in k or "<true>" in k or "<1>" in k) else "sage_layer_tc"
+    for key in ("sage_layer0", "hd_mean_feat", "hd_mean32", "confusion", "spmm_mean32", "spmm_generic", "naive_layer"):
+        if key in k:
+            return key
+    return k.split("(")[0].split()[-1]
+
+
+def val(m, key, scale=False):
+    e = m.get(key)
+    if not isinstance(e, dict):
+        return None
+    try:
+        v = float(str(e["value"]).replace(",", ""))
+    except ValueError:
+        return None
+    return v * UNIT.get(e.get("unit", ""), 1.0) if scale else v
+
+
+def main(rnd, out, reports):
+    kernels = {}
+    for rep in reports:
+        stalls = {short_name(s["kernel"]): s["top"] for s in N.top_sass(rep, 8)}
+        for m in N.raw(rep):
+            kname = m["kernel"]
+            name = short_name(kname)
+            if name in kernels:
+                continue
+            rd, wr = val(m, "dram__bytes_read.sum", True), val(m, "dram__bytes_write.sum", True)
+            e = {
+                "duration_ms": val(m, "gpu__time_duration.sum"),
+                "dram_read_bytes": rd,
+                "dram_write_bytes": wr,
+                "dram_bytes_per_launch": (rd or 0) + (wr or 0),
+                "dram_throughput_pct": val(m, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                "lts_throughput_pct": val(m, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "l1tex_throughput_pct": val(m, "l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "tensor_pipe_active_pct": val(m, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "warps_active_pct": val(m, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "registers": val(m, "launch__registers_per_thread"),
+                "grid": val(m, "launch__grid_size"),
+                "block": val(m, "launch__block_size"),
+                "source": os.path.basename(rep),
+            }
+            if name.startswith("sage_layer_tc") and name in stalls:
+                e["top_stalls"] = stalls[name]
+            kernels[name] = e
+    res = {"round": rnd, "source": "ncu --set full --clock-control none (" + ", ".join(os.path.basename(r) for r in reports)
+           + "); 1024-bit CSA b16 graph", "kernels": kernels}
+    # bench.py reads <kernel>.dram_bytes_per_launch at the top level
+    for k in ("sage_layer_tc", "sage_layer_tc_last"):
+        if k in kernels:
+            res[k] = {"dram_bytes_per_launch": kernels[k]["dram_bytes_per_launch"]}
+    with open(out, "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]), sys.argv[2], sys.argv[3:])
