@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libgroot_b200.so")
-SOURCES = ["graph_build.cu", "forward.cu", "plan.cu", "capi.cpp", "runtime.cpp"]
-HEADERS = ["common.cuh", "ptx.cuh"]
+SOURCES = ["graph_build.cu", "forward.cu", "tile_plan.cu", "plan.cu", "capi.cpp", "runtime.cpp"]
+HEADERS = ["common.cuh", "ptx.cuh", "tile_plan.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",

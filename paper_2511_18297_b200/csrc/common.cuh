@@ -151,6 +151,12 @@ struct groot_graph {
   groot::DevBuf<uint32_t> hd_rows;  // rows with degree >= hd_threshold, ascending
   groot::DevBuf<float> hd_mean;     // num_hd x 32 neighbour means (scratch per layer)
   groot::DevBuf<float> act[2];      // n x 32 ping-pong activations
+  // Per-tile gather plan of the fused layer / SpMM (tile_plan.cuh), built lazily.
+  uint32_t tp_threshold = 0, tp_halo_cap = 0, tp_slow = 0;
+  groot::DevBuf<uint32_t> tp_meta;  // TileMeta per tile (4 x u32)
+  groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
+  groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots
+  groot::DevBuf<uint32_t> tp_halo;  // halo rows per tile
 };
 
 struct groot_assignment {

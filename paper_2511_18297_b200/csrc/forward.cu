@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "tile_plan.cuh"
 
 namespace groot {
 
@@ -163,6 +164,13 @@ struct LayerArgs {
   float* logits;         // last layer: n x classes (optional)
   const uint8_t* labels; // optional (confusion)
   unsigned long long* confusion;  // optional, 25 counters
+  // tile plan (sage_tile_kernel)
+  const TileMeta* tmeta;
+  const uint16_t* lrp;
+  const uint16_t* lcol;
+  const uint32_t* halo;
+  float* spmm_out;       // SpMM mode: n x 32 neighbour means (LD rows)
+  uint32_t exp;          // experiment knob (GROOT_TK_EXP), 0 = normal
 };
 
 template <bool kLast>
@@ -532,6 +540,401 @@ __global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerA
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile-planned fused layer / SpMM (tile_plan.cuh). Same warp roles as above,
+// but every neighbour row is read from shared memory:
+//   loader warp   per tile: row offsets, local neighbour slots and the halo
+//                 list (bulk copies, barrier in_meta), the 128 tile rows (one
+//                 TMA box, barrier in_full); kHaloLag tiles later, once that
+//                 tile's halo list has landed, its 32 lanes copy the halo rows
+//                 into the stage behind the tile rows (cp.async 16 B, same
+//                 128-B swizzle as the TMA box) and arrive on in_full
+//   8 producers   per row: lrp -> local slots -> 2 x LDS.128 per neighbour,
+//                 sum in nonzero order, x 1/deg, TF32 split into TMEM (layer
+//                 modes) or a 256-bit store of the mean row (SpMM mode)
+//   MMA warp, 4 epilogue warps: as in sage_layer_tc_kernel.
+// Tiles flagged slow in the plan gather straight from the global CSR.
+// ---------------------------------------------------------------------------
+enum TileMode { kModeLayer = 0, kModeLast = 1, kModeSpmm = 2 };
+// Two rings: the per-tile plan records (row offsets, local slots, halo list;
+// ~3 KB) run kTkMetaLead tiles ahead of the row stages (tile + halo rows,
+// 36 KB), so a tile's halo list has landed by the time its rows are issued.
+constexpr int kTkRowStages = 4;
+constexpr int kTkMetaStages = 8;
+constexpr int kTkMetaLead = kTkMetaStages - kTkRowStages;
+constexpr uint32_t kCopiersMma = 2;   // warps 14, 15
+constexpr uint32_t kCopiersSpmm = 7;  // warps 0-3, 12, 14, 15
+constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;  // rows: tile 0..127, halo 128..
+constexpr uint32_t kTkLrpOff = 0;
+constexpr uint32_t kTkLcolOff = kTpLrp * 2u + 16u;
+constexpr uint32_t kTkHaloOff = kTkLcolOff + kTpColCap * 2u;
+constexpr uint32_t kTkMetaBytes = ((kTkHaloOff + kTpHaloCap * 4u + 127u) / 128u) * 128u;
+constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kBBytes + kEpiBytes +
+                                  256 * 4 + 16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
+                                  16 + 1024;
+static_assert(kTkRowBytes % 1024 == 0, "row stages must keep the 1024-B swizzle alignment");
+static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0, "bulk-copy destinations must be 16-B aligned");
+static_assert(kTkSmemBytes <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
+
+__device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const float4& x1) {
+  m[0] = ptx::fadd2(m[0], make_float2(x0.x, x0.y));
+  m[1] = ptx::fadd2(m[1], make_float2(x0.z, x0.w));
+  m[2] = ptx::fadd2(m[2], make_float2(x1.x, x1.y));
+  m[3] = ptx::fadd2(m[3], make_float2(x1.z, x1.w));
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
+                                                                const __grid_constant__ CUtensorMap tmap_in,
+                                                                const __grid_constant__ CUtensorMap tmap_out) {
+  constexpr bool kMma = kMode != kModeSpmm;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows
+  uint8_t* sPlan = sRows + kTkRowStages * kTkRowBytes;   // [kTkMetaStages] lrp | lcol | halo list
+  uint8_t* sB = sPlan + kTkMetaStages * kTkMetaBytes;
+  uint8_t* sE = sB + kBBytes;
+  float* sInv = reinterpret_cast<float*>(sE + kEpiBytes);
+  uint4* sMeta = reinterpret_cast<uint4*>(sInv + 256);  // [kTkMetaStages] TileMeta of the staged plan
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMeta + kTkMetaStages);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* m_full = tempty + 2;
+  uint64_t* m_empty = m_full + kTkMetaStages;
+  uint64_t* r_full = m_empty + kTkMetaStages;
+  uint64_t* r_empty = r_full + kTkRowStages;
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(r_empty + kTkRowStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = a.n;
+  const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+  const uint32_t G = gridDim.x;
+
+  if (kMma)
+    for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
+      reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
+  for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], kProdWarps * 32);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], kEpiWarps * 32);
+    }
+    for (int s = 0; s < kTkMetaStages; ++s) {
+      ptx::mbar_init(&m_full[s], 1);
+      ptx::mbar_init(&m_empty[s], kProdWarps * 32);
+    }
+    for (int s = 0; s < kTkRowStages; ++s) {
+      ptx::mbar_init(&r_full[s], 1 + 32 * (kMma ? kCopiersMma : kCopiersSpmm));  // TMA box + copier lanes
+      ptx::mbar_init(&r_empty[s], kProdWarps * 32);
+    }
+    ptx::mbar_fence_init();
+  }
+  if (kMma && warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = kMma ? *sTmem : 0u;
+
+  // halo copier warps: the two spare warps (and, in SpMM mode, the idle
+  // epilogue and MMA warps)
+  const int copier = kMma ? (warp >= kLoadWarp + 1 ? warp - (kLoadWarp + 1) : -1)
+                          : (warp < kEpiWarps ? warp : warp == kMmaWarp ? kEpiWarps : warp > kLoadWarp ? warp - 9 : -1);
+  if (warp == kLoadWarp) {
+    // ===== loader: plan records and tile rows =====
+    if (lane == 0) {
+      constexpr int kQ = 4;  // TileMeta records prefetched into registers beyond the plan ring
+      auto meta_of = [&](uint32_t tt) -> uint4 {
+        return tt < ntiles ? __ldg(reinterpret_cast<const uint4*>(a.tmeta) + tt) : make_uint4(0, 0, 0, 0);
+      };
+      auto issue_plan = [&](uint32_t i, uint32_t t, const uint4& m) {
+        const uint32_t ms = i % kTkMetaStages;
+        ptx::mbar_wait(&m_empty[ms], ((i / kTkMetaStages) & 1) ^ 1);
+        uint8_t* sp = sPlan + ms * kTkMetaBytes;
+        sMeta[ms] = m;
+        const bool slow = (m.w & kTpSlow) != 0;
+        const uint32_t hpad = slow ? 0u : (m.w + 3u) & ~3u;
+        ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u);
+        ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(t) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
+        if (m.z) ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
+        if (hpad) ptx::bulk_load(sp + kTkHaloOff, a.halo + m.y, hpad * 4u, &m_full[ms]);
+      };
+      uint4 q[kQ];
+#pragma unroll
+      for (int k = 0; k < kQ; ++k) q[k] = meta_of(blockIdx.x + (kTkMetaLead + k) * G);
+      for (int i = 0; i < kTkMetaLead; ++i) {
+        const uint32_t t = blockIdx.x + i * G;
+        if (t < ntiles) issue_plan(i, t, meta_of(t));
+      }
+      uint32_t it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        const uint4 mq = q[0];
+#pragma unroll
+        for (int k = 0; k + 1 < kQ; ++k) q[k] = q[k + 1];
+        q[kQ - 1] = meta_of(t + (kTkMetaLead + kQ) * G);
+        const uint32_t tl = t + kTkMetaLead * G;
+        if (tl < ntiles) issue_plan(it + kTkMetaLead, tl, mq);
+        const uint32_t rs = it % kTkRowStages;
+        ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&r_full[rs], kTpRows * 128u);
+        ptx::tma_load_2d(&tmap_in, sRows + rs * kTkRowBytes, &r_full[rs], 0, static_cast<int32_t>(t * kTileM));
+      }
+    }
+    __syncwarp();
+  } else if (copier >= 0) {
+    // ===== halo copiers: 16-B cp.async per lane, 8 lanes per row =====
+    const uint32_t sRows_s = ptx::smem_addr(sRows);
+    const uint32_t gl = static_cast<uint32_t>(copier) * 32u + lane;
+    const uint32_t c = gl & 7, s0 = gl >> 3;
+    constexpr uint32_t kStride = (kMma ? kCopiersMma : kCopiersSpmm) * 4u;  // rows per pass of all copier lanes
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+      const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
+      ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
+      ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
+      const uint32_t hc = sMeta[ms].w;
+      if (!(hc & kTpSlow) && a.exp != 1) {
+        const uint32_t* hl = reinterpret_cast<const uint32_t*>(sPlan + ms * kTkMetaBytes + kTkHaloOff);
+        const uint32_t sbase = sRows_s + rs * kTkRowBytes + kTpRows * 128u;
+        // 4 halo ids per batch read before the copies are issued (the asm
+        // memory clobber would otherwise serialise each LDS behind a copy)
+        for (uint32_t b0 = s0; b0 < hc; b0 += 4 * kStride) {
+          uint32_t row[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) row[u] = b0 + u * kStride < hc ? hl[b0 + u * kStride] : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t slot = b0 + u * kStride;
+            if (slot < hc)
+              ptx::cp_async16(sbase + slot * 128u + ((c ^ (slot & 7u)) << 4),
+                              a.hin + static_cast<size_t>(row[u]) * kF + 4 * c);
+          }
+        }
+      }
+      ptx::cp_async_mbar_arrive(ptx::smem_addr(&r_full[rs]));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (kMma && warp == kMmaWarp) {
+    // ===== MMA issuer (as in sage_layer_tc_kernel) =====
+    constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
+    const uint32_t b0s = ptx::smem_addr(sB);
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+      ptx::mbar_wait(&full[s], ph);
+      ptx::mbar_wait(&tempty[acc], aph ^ 1);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        const uint32_t d = tmem_base + kAccCol0 + acc * kAccCols;
+        const uint32_t as = tmem_base + s * kStageCols;
+#pragma unroll
+        for (uint32_t kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint32_t ahi = as + kb * 32 + kk * 8;
+            const uint32_t bo = b0s + kb * 8192 + kk * 32;
+            const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
+            const uint32_t first = (kb | kk) != 0;
+            ptx::mma_tf32_ts(d, ahi, bhi, idesc, first);
+            ptx::mma_tf32_ts(d, ahi, blo, idesc, 1);
+            ptx::mma_tf32_ts(d, ahi + 64, bhi, idesc, 1);
+          }
+        ptx::mma_commit(&empty[s]);
+        ptx::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= kEpiWarps && warp < kMmaWarp) {
+    // ===== producers =====
+    const uint32_t lbase = (warp & 3) * 32 + ((warp - kEpiWarps) >> 2) * 16;
+    const uint32_t j = lane & 3;
+    const uint32_t li = lbase + (lane >> 2);  // tile rows li and li + 8
+    const uint32_t thr = a.hd.threshold;
+    const float* hin_j = a.hin + 8 * j;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+      const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
+      const uint32_t row0 = t * kTileM;
+      ptx::mbar_wait(&r_full[rs], (it / kTkRowStages) & 1);
+      ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
+      const uint8_t* st = sRows + rs * kTkRowBytes;
+      const uint8_t* sp = sPlan + ms * kTkMetaBytes;
+      const bool slow = (sMeta[ms].w & kTpSlow) != 0;
+      float2 m[2][4];
+      uint32_t d[2];
+      bool hd[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m[h][q] = make_float2(0.f, 0.f);
+      if (!slow) {
+        const uint16_t* lr = reinterpret_cast<const uint16_t*>(sp + kTkLrpOff);
+        const uint16_t* lc = reinterpret_cast<const uint16_t*>(sp + kTkLcolOff);
+        uint32_t lo[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t w0 = lr[li + 8 * h], w1 = lr[li + 8 * h + 1];
+          lo[h] = w0 & 0x7FFFu;
+          d[h] = (w1 & 0x7FFFu) - lo[h];
+          hd[h] = (w0 & kTpHdBit) != 0;
+        }
+        const uint32_t dm = max(d[0], d[1]);
+        for (uint32_t k0 = 0; k0 < dm; k0 += 4) {
+          uint32_t loc[2][4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) loc[h][u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
+          float4 x[2][4][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k0 + u < d[h]) {
+                const uint8_t* rowp = st + loc[h][u] * 128u;
+                const uint32_t c0 = (2u * j) ^ (loc[h][u] & 7u);
+                x[h][u][0] = *reinterpret_cast<const float4*>(rowp + (c0 << 4));
+                x[h][u][1] = *reinterpret_cast<const float4*>(rowp + ((c0 ^ 1u) << 4));
+              }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k0 + u < d[h]) acc_row(m[h], x[h][u][0], x[h][u][1]);
+        }
+      } else {
+        uint32_t b[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t r = row0 + li + 8 * h;
+          b[h] = r < n ? __ldg(a.rp + r) : 0u;
+          const uint32_t dd = r < n ? __ldg(a.rp + r + 1) - b[h] : 0u;
+          hd[h] = dd >= thr;
+          d[h] = hd[h] ? 0u : dd;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          for (uint32_t k = 0; k < d[h]; ++k) {
+            float4 x0, x1;
+            ptx::ldg_f8(hin_j + static_cast<size_t>(__ldg(a.col + b[h] + k)) * kF, x0, x1);
+            acc_row(m[h], x0, x1);
+          }
+      }
+      float4 hs[2][2], mm[2][2];
+      if (kMma) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t il = li + 8 * h;
+          hs[h][0] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j) ^ (il & 7u)) << 4));
+          hs[h][1] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j + 1u) ^ (il & 7u)) << 4));
+        }
+      }
+      ptx::mbar_arrive(&r_empty[rs]);
+      ptx::mbar_arrive(&m_empty[ms]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t r = row0 + li + 8 * h;
+        if (hd[h]) {
+          if (kMma) {
+            const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
+            mm[h][0] = ptx::ldg_f4(src);
+            mm[h][1] = ptx::ldg_f4(src + 4);
+          }
+        } else {
+          const float inv = sInv[d[h]];
+          const float2 iv = make_float2(inv, inv);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m[h][q] = ptx::fmul2(m[h][q], iv);
+          mm[h][0] = make_float4(m[h][0].x, m[h][0].y, m[h][1].x, m[h][1].y);
+          mm[h][1] = make_float4(m[h][2].x, m[h][2].y, m[h][3].x, m[h][3].y);
+        }
+        if (kMode == kModeSpmm) {
+          if (r < n && !hd[h]) ptx::stg_f8(a.spmm_out + static_cast<size_t>(r) * kF + 8 * j, mm[h][0], mm[h][1]);
+        } else if (r >= n) {
+          hs[h][0] = hs[h][1] = mm[h][0] = mm[h][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (kMma) {
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
+        tmem_store_split(ta, hs);
+        tmem_store_split(ta + 32, mm);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&full[s]);
+      }
+    }
+  } else if (kMma && warp < kEpiWarps) {
+    // ===== epilogue (as in sage_layer_tc_kernel) =====
+    const uint32_t q = warp;
+    uint8_t* ew = sE + q * 4096;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    for (uint32_t e = 0; e < my_tiles; ++e) {
+      const uint32_t t = blockIdx.x + e * G;
+      const uint32_t acc = e & 1, ph = (e >> 1) & 1;
+      ptx::mbar_wait_sleep(&tfull[acc], ph, 200);
+      ptx::tc_fence_after();
+      float r[32];
+      const uint32_t tq = tmem_base + kAccCol0 + acc * kAccCols + ((q * 32u) << 16);
+      ptx::tmem_ld_32x32b_x32(tq, r);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + hw.bias[i], 0.0f);
+      const uint32_t row0 = t * kTileM + q * 32;
+      if (kMode == kModeLayer) {
+        if (lane == 0) ptx::bulk_wait_read0();
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(ew + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+              make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&tmap_out, ew, 0, static_cast<int32_t>(row0));
+          ptx::bulk_commit();
+        }
+      } else {
+        const uint32_t row = row0 + lane;
+        float best = 0.f;
+        uint32_t arg = 0;
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) {
+          if (c < static_cast<int>(a.classes)) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) s = fmaf(r[k], hw.w[k][c], s);
+            s += hw.b[c];
+            if (c == 0 || s > best) { best = s; arg = c; }
+            if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + c] = s;
+          }
+        }
+        if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
+      }
+    }
+    if (kMode == kModeLayer && lane == 0) ptx::bulk_wait_all();
+  }
+
+  if (kMma) {
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    }
   }
 }
 
@@ -932,6 +1335,17 @@ void classify_rows(groot_graph* g, uint32_t thr) {
   stream_sync();
 }
 
+void build_tile_plan(groot_graph* g, uint32_t thr);
+
+// GROOT_LAYER=legacy selects the register-gather fused layer (A/B knob).
+static bool use_tile_plan() {
+  static const bool v = [] {
+    const char* e = std::getenv("GROOT_LAYER");
+    return !(e && std::strcmp(e, "legacy") == 0);
+  }();
+  return v;
+}
+
 static void ensure_activations(groot_graph* g) {
   const size_t need = static_cast<size_t>(g->n) * kF;
   for (auto& b : g->act)
@@ -967,6 +1381,9 @@ static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) 
 static void set_tc_smem() {
   static bool done = false;
   if (done) return;
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   // Smallest shared-memory carve-out that fits: the rest of the 256 KB array is
@@ -1036,7 +1453,20 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
     const CUtensorMap tmap = make_rows32_tmap(hout, n, 32);
     HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
     std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
-    if (l + 1 == m->depth) {
+    if (use_tile_plan()) {
+      build_tile_plan(g, g->hd_threshold);
+      a.tmeta = reinterpret_cast<const TileMeta*>(g->tp_meta.p);
+      a.lrp = g->tp_lrp.p;
+      a.lcol = g->tp_lcol.p;
+      a.halo = g->tp_halo.p;
+      if (l + 1 == m->depth) {
+        ProfScope ps("sage_layer_tc_last");
+        GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in, tmap);
+      } else {
+        ProfScope ps("sage_layer_tc");
+        GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in, tmap);
+      }
+    } else if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
       GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw, tmap_in, tmap);
     } else {
@@ -1098,6 +1528,29 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
       ProfScope ps("spmm_hd_mean32");
       GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, dense, out, 1);
+    }
+    if (use_tile_plan()) {
+      set_tc_smem();
+      build_tile_plan(g, hd.threshold);
+      ProfScope ps("spmm_mean32");
+      LayerArgs a{};
+      a.n = g->n;
+      a.rp = g->rp.p;
+      a.col = g->col.p;
+      a.hin = dense;
+      a.hd = hd;
+      a.tmeta = reinterpret_cast<const TileMeta*>(g->tp_meta.p);
+      a.lrp = g->tp_lrp.p;
+      a.lcol = g->tp_lcol.p;
+      a.halo = g->tp_halo.p;
+      a.spmm_out = out;
+      a.exp = env_u32("GROOT_TK_EXP", 0);
+      const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(dense), g->n, kTileM);
+      const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
+      HeadW hw{};
+      GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, kTkSmemBytes, a, hw,
+                   tmap_in, tmap_in);
+      return;
     }
     ProfScope ps("spmm_mean32");
     static const int occ = [] {
