@@ -3,19 +3,23 @@
 // Reference: run_forward / predict_full (src/gnn.cpp:37-52, 259-300) over the
 // degree-polarised SpMM (src/spmm.cpp:37-127, inc/spmm.hpp:106-181).
 //
-// Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel per SM:
-//   TMA warp      streams each 128-row tile (feature rows, row_ptr slice,
-//                 col_idx range) into a shared-memory ring, waves ahead
-//   8 producers   neighbour gather (32-byte L2 loads, software-pipelined one
-//                 tile ahead) + mean, TF32 hi/lo split of [h | mean(h_N)]
-//                 written straight into tensor memory (tcgen05.st)
+// Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel per SM
+// (sage_tile_kernel) walks 128-row tiles with the tile plan of tile_plan.cuh:
+//   loader warp   plan records (row offsets, u16 local neighbour slots, halo
+//                 list) by bulk copy, the tile's 128 feature rows by one TMA box
+//   copier warps  the tile's halo rows (out-of-tile neighbours) by cp.async,
+//                 into the stage right behind the tile rows
+//   8 producers   per row: neighbour rows from shared memory, sum in nonzero
+//                 order, x 1/deg, TF32 hi/lo split of [h | mean(h_N)] written
+//                 straight into tensor memory (tcgen05.st)
 //   MMA warp      tcgen05.mma kind::tf32, A from TMEM, W from smem, 3 products
 //                 (hi*hi + hi*lo + lo*hi) into a double-buffered accumulator
-//   4 epilogue    tcgen05.ld, + bias, ReLU, TMA tensor store (or, in the last
-//                 layer, the 32 -> classes head + first-max argmax)
-// High-degree rows (the row classifier's HD band; the PIs of a multiplier)
-// are aggregated first by a CTA-per-row kernel with a fixed-order reduction.
-// Layer 0 (4 -> 32, inputs in {0,1}^4) is a gather + FFMA kernel.
+//   4 epilogue    tcgen05.ld, + bias, ReLU, 256-bit stores of whole rows (or, in
+//                 the last layer, the 32 -> classes head + first-max argmax)
+// The same kernel without the MMA is the standalone LD SpMM. High-degree rows
+// (the row classifier's HD band; the PIs of a multiplier) are aggregated first
+// by a CTA-per-row kernel with a fixed-order reduction. Layer 0 (4 -> 32,
+// inputs in {0,1}^4) is a gather + FFMA kernel.
 #include <cub/cub.cuh>
 #include <cuda.h>
 
@@ -31,17 +35,12 @@ namespace groot {
 
 constexpr int kF = 32;                       // hidden width (tensor-core layers)
 constexpr int kTileM = 128;                  // rows per MMA tile (UMMA M)
+static_assert(kTileM == static_cast<int>(kTpRows), "plan tiles are MMA tiles");
 constexpr int kEpiWarps = 4;                 // warps 0..3: accumulator drain (TMEM lane quadrant = warp)
 constexpr int kProdWarps = 8;                // warps 4..11: gather producers, 16 rows each
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // warp 12: TMEM alloc + tcgen05.mma issue
-constexpr int kLoadWarp = kMmaWarp + 1;           // warp 13: TMA loads of the input tiles
-// 16 warps = 4 warpgroups: epilogue | producers | producers | MMA, loader, 2 idle.
-// Launched at 128 registers/thread (4 warps x 128 x 32 fills a sub-partition's
-// 16K registers); setmaxnreg then moves registers to the producers:
-// per sub-partition 72 + 2 x 200 + 40 = 512.
-constexpr int kThreads = 16 * 32;  // 512
-constexpr uint32_t kEpiRegs = 72, kProdRegs = 200, kCtlRegs = 40;
-static_assert(kEpiRegs + 2 * kProdRegs + kCtlRegs <= 512, "register file per sub-partition");
+constexpr int kLoadWarp = kMmaWarp + 1;           // warp 13: plan records + tile rows
+constexpr int kThreads = 16 * 32;  // 512; warps 14, 15 copy halo rows
 constexpr int kStages = 3;
 // Tensor memory (512 columns x 128 lanes x 32 bit): the A operand lives there,
 // so the gather never goes through a shared-memory operand tile. Stage s owns
@@ -53,19 +52,7 @@ constexpr uint32_t kAccCol0 = kStages * kStageCols;  // 384
 constexpr uint32_t kTmemCols = 512;
 static_assert(kAccCol0 + 2 * kAccCols <= kTmemCols, "tensor memory budget");
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
-constexpr uint32_t kEpiBytes = kEpiWarps * 32 * 128;
 constexpr int kMaxClasses = 8;
-// Input ring: per tile the 128 feature rows (TMA, SWIZZLE_128B), row_ptr
-// [row0, row0+129) and, when it fits, the tile's col_idx range.
-constexpr int kInStages = 6;
-constexpr uint32_t kColCap = 1024;                // col_idx entries staged per tile
-constexpr uint32_t kInRpOff = kTileM * 128;       // 16384
-constexpr uint32_t kInColOff = kInRpOff + 640;    // row_ptr: 132 entries, padded
-constexpr uint32_t kInStageBytes = ((kInColOff + kColCap * 4 + 1023) / 1024) * 1024;
-constexpr uint32_t kSmemBytes = kInStages * kInStageBytes + kBBytes + kEpiBytes + 256 * 4 + 8 * kInStages +
-                                8 * (2 * kStages + 4 + 2 * kInStages) + 16 + 1024;
-static_assert(kSmemBytes <= 232448, "fused layer exceeds the 227 KB shared-memory limit");
-
 // Column c (0..31) of an A block in tensor memory holds input feature
 // kcol_feature(c): lane j of a row's 4-lane group loads features 8j..8j+7
 // (one 32-byte load) and 16x256b stores put its values in columns 8i+2j+e.
@@ -73,6 +60,11 @@ static_assert(kSmemBytes <= 232448, "fused layer exceeds the 227 KB shared-memor
 __host__ __device__ constexpr uint32_t kcol_feature(uint32_t c) {
   return ((c >> 1) & 3u) * 8u + (c >> 3) * 2u + (c & 1u);
 }
+// Column holding feature f (inverse of kcol_feature): f = 8j + 2i + e -> 8i + 2j + e.
+__host__ __device__ constexpr uint32_t kcol_inverse(uint32_t f) {
+  return ((f >> 1) & 3u) * 8u + (f >> 3) * 2u + (f & 1u);
+}
+static_assert(kcol_inverse(kcol_feature(13)) == 13 && kcol_feature(kcol_inverse(22)) == 22, "permutation");
 
 static uint32_t env_u32(const char* name, uint32_t dflt) {
   const char* e = std::getenv(name);
@@ -153,429 +145,60 @@ struct LayerArgs {
   const uint32_t* rp;
   const uint32_t* col;
   const float* hin;      // n x 32
-  float* hout;           // n x 32 (unused in the last layer)
-  const uint32_t* bimg;  // 16 KB swizzled W image (hi/lo)
-  const float* bias;     // 32
+  float* hout;           // n x 32 (layer mode)
+  const uint32_t* bimg;  // 16 KB swizzled W image (hi/lo), K and N permuted by kcol_feature
   HdInfo hd;
-  const float* head;     // W_out [32 x classes] row-major, then b_out
   uint32_t classes;
-  unsigned long long* trace;  // diagnostic timeline of CTA 0 (nullptr = off): [64 tiles][16 events]
   uint8_t* cls;          // last layer: n classes
   float* logits;         // last layer: n x classes (optional)
-  const uint8_t* labels; // optional (confusion)
-  unsigned long long* confusion;  // optional, 25 counters
-  // tile plan (sage_tile_kernel)
+  // tile plan (tile_plan.cuh)
   const TileMeta* tmeta;
   const uint16_t* lrp;
   const uint16_t* lcol;
   const uint32_t* halo;
   float* spmm_out;       // SpMM mode: n x 32 neighbour means (LD rows)
-  uint32_t exp;          // experiment knob (GROOT_TK_EXP), 0 = normal
+  unsigned long long* trace;  // diagnostic timeline of CTA 0 (GROOT_TRACE): [64 tiles][16 clock64 stamps]
 };
 
-template <bool kLast>
-__global__ void __launch_bounds__(kThreads, 1) sage_layer_tc_kernel(const LayerArgs a, const HeadW hw,
-                                                       const __grid_constant__ CUtensorMap tmap_in,
-                                                       const __grid_constant__ CUtensorMap tmap_out) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the SWIZZLE_128B tiles, computed on the shared
-  // address so the pointer stays in the shared window (LDS/STS, not generic).
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sIn = smem;                              // [kInStages] input tiles
-  uint8_t* sB = sIn + kInStages * kInStageBytes;
-  uint8_t* sE = sB + kBBytes;
-  float* sInv = reinterpret_cast<float*>(sE + kEpiBytes);  // 1/deg for deg < 256 (== 1.0f/d)
-  uint32_t* sMeta = reinterpret_cast<uint32_t*>(sInv + 256);  // [kInStages][2]: col base, col in smem
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMeta + 2 * kInStages);
-  uint64_t* full = bars;                     // [kStages] producers -> MMA (A operand in TMEM)
-  uint64_t* empty = full + kStages;          // [kStages] MMA done reading the A stage
-  uint64_t* tfull = empty + kStages;         // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;              // [2] accumulator drained by the epilogue
-  uint64_t* in_full = tempty + 2;            // [kInStages] TMA -> producers
-  uint64_t* in_empty = in_full + kInStages;  // [kInStages] producers done with the input tile
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(in_empty + kInStages);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t n = a.n;
-  const uint32_t ntiles = (n + kTileM - 1) / kTileM;
-  const uint32_t G = gridDim.x;
-
-  for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
-    reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
-  for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], kProdWarps * 32);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], kEpiWarps * 32);
-    }
-    for (int s = 0; s < kInStages; ++s) {
-      ptx::mbar_init(&in_full[s], 1);
-      ptx::mbar_init(&in_empty[s], kProdWarps * 32);
-    }
-    ptx::mbar_fence_init();
-  }
-  if (warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
-  ptx::fence_proxy_async_smem();  // weight image (generic stores) -> tensor core (async proxy)
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *sTmem;
-
-  if (warp >= kMmaWarp) ptx::setmaxnreg_dec<kCtlRegs>();  // warpgroup 3: MMA issuer, TMA loader, 2 idle
-  if (warp == kLoadWarp) {
-    // ===== TMA loader: tile t's feature rows (swizzled), row_ptr slice and
-    // col_idx range into the input ring, kInStages tiles (waves) ahead =====
-    if (lane == 0) {
-      // row_ptr bounds of the tiles kBoundsAhead iterations ahead are in flight
-      // (a ring in registers), so their DRAM latency is never on the loop.
-      constexpr int kBoundsAhead = 8;
-      auto bounds = [&](uint32_t tt, uint32_t& b, uint32_t& e) {
-        b = e = 0;
-        if (tt < ntiles) {
-          b = __ldg(a.rp + tt * kTileM);
-          e = __ldg(a.rp + min(tt * kTileM + kTileM, n));
-        }
-      };
-      uint32_t qb[kBoundsAhead], qe[kBoundsAhead];
-#pragma unroll
-      for (int k = 0; k < kBoundsAhead; ++k) bounds(blockIdx.x + k * G, qb[k], qe[k]);
-      uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
-        const uint32_t s = it % kInStages, ph = (it / kInStages) & 1;
-        const uint32_t cb0 = qb[0], ce0 = qe[0];
-#pragma unroll
-        for (int k = 0; k + 1 < kBoundsAhead; ++k) {
-          qb[k] = qb[k + 1];
-          qe[k] = qe[k + 1];
-        }
-        bounds(t + kBoundsAhead * G, qb[kBoundsAhead - 1], qe[kBoundsAhead - 1]);
-        ptx::mbar_wait_sleep(&in_empty[s], ph ^ 1);
-        uint8_t* st = sIn + s * kInStageBytes;
-        const uint32_t row0 = t * kTileM;
-        const uint32_t rows = min(static_cast<uint32_t>(kTileM), n - row0);
-        const uint32_t rcnt = (rows + 1 + 3) & ~3u;  // row_ptr entries (16-byte multiple; 16 B of slack)
-        const uint32_t cb = cb0 & ~3u;
-        const uint32_t ccnt = (ce0 - cb + 3) & ~3u;
-        const bool col_smem = ccnt <= kColCap;  // tiles holding high-degree rows read col_idx from global
-        sMeta[2 * s] = cb;
-        sMeta[2 * s + 1] = col_smem;
-        const uint32_t tx = kTileM * 128u + rcnt * 4u + (col_smem ? ccnt * 4u : 0u);
-        ptx::mbar_arrive_expect_tx(&in_full[s], tx);
-        ptx::tma_load_2d(&tmap_in, st, &in_full[s], 0, static_cast<int32_t>(row0));
-        ptx::bulk_load(st + kInRpOff, a.rp + row0, rcnt * 4u, &in_full[s]);
-        if (col_smem && ccnt) ptx::bulk_load(st + kInColOff, a.col + cb, ccnt * 4u, &in_full[s]);
-      }
-    }
-    __syncwarp();
-  } else if (warp == kMmaWarp) {
-    // ===== MMA issuer: the whole warp runs the loop (warp-uniform operands
-    // stay in uniform registers), one elected lane issues. A from tensor
-    // memory, B from shared memory =====
-    constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
-    const uint32_t b0s = ptx::smem_addr(sB);
-    uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
-      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
-      unsigned long long* trow =
-          (a.trace && blockIdx.x == 0 && lane == 0 && it < 64) ? a.trace + it * 16 + 10 : nullptr;
-      if (trow) trow[0] = clock64();
-      ptx::mbar_wait(&full[s], ph);
-      if (trow) trow[1] = clock64();
-      ptx::mbar_wait(&tempty[acc], aph ^ 1);
-      if (trow) trow[2] = clock64();
-      ptx::tc_fence_after();
-      if (ptx::elect_one()) {
-        const uint32_t d = tmem_base + kAccCol0 + acc * kAccCols;
-        const uint32_t as = tmem_base + s * kStageCols;
-#pragma unroll
-        for (uint32_t kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (uint32_t kk = 0; kk < 4; ++kk) {
-            const uint32_t ahi = as + kb * 32 + kk * 8;  // h (kb 0) or m (kb 1), K = 8 columns
-            const uint32_t bo = b0s + kb * 8192 + kk * 32;
-            const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
-            const uint32_t first = (kb | kk) != 0;
-            ptx::mma_tf32_ts(d, ahi, bhi, idesc, first);
-            ptx::mma_tf32_ts(d, ahi, blo, idesc, 1);
-            ptx::mma_tf32_ts(d, ahi + 64, bhi, idesc, 1);
-          }
-        ptx::mma_commit(&empty[s]);
-        ptx::mma_commit(&tfull[acc]);
-      }
-      __syncwarp();
-      if (trow) trow[3] = clock64();
-    }
-  } else if (warp >= kEpiWarps && warp < kMmaWarp) {
-    // ===== gather producers (two warpgroups, 192 registers per thread) =====
-    // 8 warps x 16 rows = one 128-row tile per pass. A warp may only reach its
-    // TMEM lane quadrant (warp % 4), so warp w owns tile rows 32(w%4) + 16h ..
-    // +15 with h = (w-4)/4. Lane group r = lane/4 owns rows r and r+8 of that
-    // slice; lane j = lane%4 holds features 8j..8j+7, exactly the registers a
-    // 16x256b tcgen05.st takes (A's K order permuted to match, kcol_feature).
-    // row_ptr, col_idx and the row's own features come from the TMA-filled
-    // input tile (swizzled 128-B rows: chunk c of row i at i*128 + ((c ^
-    // (i&7)) << 4)). Each neighbour slot is ONE generic load per 16 bytes:
-    // a shared-window address for rows inside the tile, a global address
-    // (an L2 hit: the tile ring streams a few waves ahead) otherwise.
-    // Software pipeline, two tiles deep: the neighbour loads of tile t+G are
-    // issued before tile t is consumed (register sets A and B alternate).
-    ptx::setmaxnreg_inc<kProdRegs>();
-    const uint32_t lbase = (warp & 3) * 32 + ((warp - kEpiWarps) >> 2) * 16;
-    const int j = lane & 3, gbase = lane & ~3;
-    const uint32_t li = lbase + (lane >> 2);  // tile rows li and li + 8
-    const uint32_t thr = a.hd.threshold;
-    const float* hin_j = a.hin + 8 * j;
-    constexpr int U = 4;  // neighbour slots per row (CSA LD rows have degree <= 4; more -> tail loop)
-    struct Slots {
-      float4 v[2][U][2];
-      uint32_t d[2];  // degrees of the two rows
-    };
-    // wait for tile t's input, read its row_ptr / col_idx, issue all neighbour
-    // loads (slots past the degree re-read the row itself from shared memory)
-    auto issue = [&](uint32_t it, uint32_t t, Slots& L) {
-      const uint32_t si = it % kInStages;
-      const uint32_t row0 = t * kTileM;
-      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarps && it < 64;
-      unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
-      if (tr) trow[6] = clock64();
-      ptx::mbar_wait(&in_full[si], (it / kInStages) & 1);
-      if (tr) trow[7] = clock64();
-      const uint8_t* st = sIn + si * kInStageBytes;
-      const uint32_t* sRp = reinterpret_cast<const uint32_t*>(st + kInRpOff);
-      const uint32_t* sCol = reinterpret_cast<const uint32_t*>(st + kInColOff);
-      const uint32_t cb = sMeta[2 * si];
-      const bool col_smem = sMeta[2 * si + 1] != 0;
-      uint32_t c[2], dl[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t il = li + 8 * h;
-        const bool ok = row0 + il < n;
-        const uint32_t b = ok ? sRp[il] : 0u;
-        L.d[h] = ok ? sRp[il + 1] - b : 0u;
-        dl[h] = L.d[h] < thr ? L.d[h] : 0u;
-        c[h] = 0u;
-        if (static_cast<uint32_t>(j) < dl[h]) c[h] = col_smem ? sCol[b - cb + j] : __ldg(a.col + b + j);
-      }
-      if (tr) trow[8] = clock64() + (c[0] & 0u);  // after the col_idx values arrived
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t il = li + 8 * h;
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const uint32_t ci = __shfl_sync(0xffffffffu, c[h], gbase + k);
-          const uint32_t src = static_cast<uint32_t>(k) < dl[h] ? ci : min(row0 + il, n - 1);
-          ptx::ldg_f8(hin_j + static_cast<size_t>(src) * kF, L.v[h][k][0], L.v[h][k][1]);
-        }
-      }
-      if (tr) trow[9] = clock64();
-    };
-    // sum, mean, self features, TF32 split into the A stage, hand to the MMA
-    auto consume = [&](uint32_t it, uint32_t t, Slots& L) {
-      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      const uint32_t si = it % kInStages;
-      const uint32_t row0 = t * kTileM;
-      const bool tr = a.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarps && it < 64;
-      unsigned long long* trow = tr ? a.trace + it * 16 : nullptr;
-      if (tr) trow[0] = trow[1] = trow[2] = clock64();
-      const uint8_t* st = sIn + si * kInStageBytes;
-      uint32_t dl[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) dl[h] = L.d[h] < thr ? L.d[h] : 0u;
-      float2 m[2][4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) m[h][q] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-          if (static_cast<uint32_t>(k) < dl[h]) {
-            m[h][0] = ptx::fadd2(m[h][0], make_float2(L.v[h][k][0].x, L.v[h][k][0].y));
-            m[h][1] = ptx::fadd2(m[h][1], make_float2(L.v[h][k][0].z, L.v[h][k][0].w));
-            m[h][2] = ptx::fadd2(m[h][2], make_float2(L.v[h][k][1].x, L.v[h][k][1].y));
-            m[h][3] = ptx::fadd2(m[h][3], make_float2(L.v[h][k][1].z, L.v[h][k][1].w));
-          }
-      }
-      const uint32_t dmax = __reduce_max_sync(0xffffffffu, max(dl[0], dl[1]));
-      if (dmax > static_cast<uint32_t>(U)) {  // LD rows with more than U neighbours (rare in CSA)
-        const uint32_t* sRp = reinterpret_cast<const uint32_t*>(st + kInRpOff);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t b = dl[h] ? sRp[li + 8 * h] : 0u;
-          for (uint32_t k0 = U; k0 < dmax; k0 += U) {
-            const uint32_t cc = (k0 + j < dl[h]) ? __ldg(a.col + b + k0 + j) : 0u;
-#pragma unroll
-            for (int kk = 0; kk < U; ++kk) {
-              const uint32_t ci = __shfl_sync(0xffffffffu, cc, gbase + kk);
-              if (k0 + kk < dl[h]) {
-                float4 x0, x1;
-                ptx::ldg_f8(hin_j + static_cast<size_t>(ci) * kF, x0, x1);
-                m[h][0] = ptx::fadd2(m[h][0], make_float2(x0.x, x0.y));
-                m[h][1] = ptx::fadd2(m[h][1], make_float2(x0.z, x0.w));
-                m[h][2] = ptx::fadd2(m[h][2], make_float2(x1.x, x1.y));
-                m[h][3] = ptx::fadd2(m[h][3], make_float2(x1.z, x1.w));
-              }
-            }
-          }
-        }
-      }
-      float4 hs[2][2], mm[2][2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t il = li + 8 * h;
-        hs[h][0] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j) ^ (il & 7u)) << 4));
-        hs[h][1] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j + 1u) ^ (il & 7u)) << 4));
-      }
-      // the input tile is no longer read by this thread
-      ptx::mbar_arrive(&in_empty[si]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t r = row0 + li + 8 * h;
-        if (L.d[h] >= thr) {
-          const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
-          mm[h][0] = ptx::ldg_f4(src);
-          mm[h][1] = ptx::ldg_f4(src + 4);
-        } else {
-          const float inv = sInv[L.d[h]];
-          const float2 iv = make_float2(inv, inv);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) m[h][q] = ptx::fmul2(m[h][q], iv);
-          mm[h][0] = make_float4(m[h][0].x, m[h][0].y, m[h][1].x, m[h][1].y);
-          mm[h][1] = make_float4(m[h][2].x, m[h][2].y, m[h][3].x, m[h][3].y);
-        }
-        if (r >= n) hs[h][0] = hs[h][1] = mm[h][0] = mm[h][1] = make_float4(0.f, 0.f, 0.f, 0.f);  // rows past n
-      }
-      if (tr) trow[3] = clock64();
-      ptx::mbar_wait(&empty[s], ph ^ 1);
-      ptx::tc_fence_after();
-      if (tr) trow[4] = clock64();
-      const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
-      tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
-      tmem_store_split(ta + 32, mm);  // columns 32..63 (hi), 96..127 (lo): neighbour mean
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&full[s]);
-      if (tr) trow[5] = clock64();
-    };
-    Slots A, B;
-    uint32_t it = 0, t = blockIdx.x;
-    if (t < ntiles) issue(0, t, A);
-    while (t < ntiles) {
-      if (t + G < ntiles) issue(it + 1, t + G, B);
-      consume(it, t, A);
-      t += G;
-      ++it;
-      if (t >= ntiles) break;
-      if (t + G < ntiles) issue(it + 1, t + G, A);
-      consume(it, t, B);
-      t += G;
-      ++it;
-    }
-  } else if (warp < kEpiWarps) {
-    // ===== epilogue (4 warps, TMEM lane quadrant = warp) =====
-    ptx::setmaxnreg_dec<kEpiRegs>();
-    const uint32_t q = warp;
-    uint8_t* ew = sE + q * 4096;
-    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
-    for (uint32_t e = 0; e < my_tiles; ++e) {
-      const uint32_t t = blockIdx.x + e * G;
-      const uint32_t acc = e & 1, ph = (e >> 1) & 1;
-      ptx::mbar_wait_sleep(&tfull[acc], ph);
-      if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 14] = clock64();
-      ptx::tc_fence_after();
-      float r[32];
-      const uint32_t tq = tmem_base + kAccCol0 + acc * kAccCols + ((q * 32u) << 16);
-      ptx::tmem_ld_32x32b_x32(tq, r);
-
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + hw.bias[i], 0.0f);
-      const uint32_t row0 = t * kTileM + q * 32;
-      if (!kLast) {
-        // Stage the warp's 32 rows in the SWIZZLE_128B layout (conflict-free STS)
-        // and let the TMA engine store them: one cp.async.bulk.tensor per warp
-        // per tile instead of a shared-memory read-back and 8 STG per thread.
-        if (lane == 0) ptx::bulk_wait_read0();  // previous tile's store has read the buffer
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<float4*>(ew + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-              make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          ptx::tma_store_2d(&tmap_out, ew, 0, static_cast<int32_t>(row0));
-          ptx::bulk_commit();
-        }
-      } else {
-        // head 32 -> classes (weights in the constant bank), first-max argmax
-        const uint32_t row = row0 + lane;
-        float best = 0.f;
-        uint32_t arg = 0;
-#pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c) {
-          if (c < static_cast<int>(a.classes)) {
-            float s = 0.f;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) s = fmaf(r[k], hw.w[k][c], s);
-            s += hw.b[c];
-            if (c == 0 || s > best) { best = s; arg = c; }
-            if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + c] = s;
-          }
-        }
-        if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
-      }
-      if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && e < 64) a.trace[e * 16 + 15] = clock64();
-    }
-    if (!kLast && lane == 0) ptx::bulk_wait_all();  // global writes of the last stores done
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem_base);
-  }
+// Timeline stamp of CTA 0 for tile iteration it (< 64), event slot k (< 16).
+// Compiled in only with -DGROOT_TRACE_BUILD (the stamps cost registers).
+#ifdef GROOT_TRACE_BUILD
+constexpr bool kTraceOn = true;
+#else
+constexpr bool kTraceOn = false;
+#endif
+__device__ __forceinline__ void tstamp(unsigned long long* tr, uint32_t it, int k) {
+  if (kTraceOn && tr && blockIdx.x == 0 && it < 64) tr[it * 16 + k] = clock64();
 }
 
 // ---------------------------------------------------------------------------
-// Tile-planned fused layer / SpMM (tile_plan.cuh). Same warp roles as above,
-// but every neighbour row is read from shared memory:
-//   loader warp   per tile: row offsets, local neighbour slots and the halo
-//                 list (bulk copies, barrier in_meta), the 128 tile rows (one
-//                 TMA box, barrier in_full); kHaloLag tiles later, once that
-//                 tile's halo list has landed, its 32 lanes copy the halo rows
-//                 into the stage behind the tile rows (cp.async 16 B, same
-//                 128-B swizzle as the TMA box) and arrive on in_full
-//   8 producers   per row: lrp -> local slots -> 2 x LDS.128 per neighbour,
-//                 sum in nonzero order, x 1/deg, TF32 split into TMEM (layer
-//                 modes) or a 256-bit store of the mean row (SpMM mode)
-//   MMA warp, 4 epilogue warps: as in sage_layer_tc_kernel.
-// Tiles flagged slow in the plan gather straight from the global CSR.
+// Tile-planned fused layer / SpMM. Shared memory holds two rings:
+//   plan ring  (kTkMetaStages x ~3 KB): a tile's row offsets, local slots and
+//              halo list; issued kTkMetaLead tiles ahead of the rows, so the
+//              halo list is there when the tile's rows are fetched;
+//   row ring   (kTkRowStages x 36 KB): rows 0..127 = the tile (TMA box),
+//              rows 128.. = its halo (cp.async by the copier warps).
+// Rows are stored unswizzled. Lane j of a row's 4-lane group reads the 32 B
+// of features 8j..8j+7 as two 16-B loads; groups of odd parity issue the two
+// halves in the opposite order, so the two rows served in one 8-lane phase
+// always touch disjoint banks (even vs odd 16-B chunks) whatever the rows
+// are. Their accumulators are swapped back once per row.
 // ---------------------------------------------------------------------------
 enum TileMode { kModeLayer = 0, kModeLast = 1, kModeSpmm = 2 };
-// Two rings: the per-tile plan records (row offsets, local slots, halo list;
-// ~3 KB) run kTkMetaLead tiles ahead of the row stages (tile + halo rows,
-// 36 KB), so a tile's halo list has landed by the time its rows are issued.
 constexpr int kTkRowStages = 4;
 constexpr int kTkMetaStages = 8;
 constexpr int kTkMetaLead = kTkMetaStages - kTkRowStages;
 constexpr uint32_t kCopiersMma = 2;   // warps 14, 15
 constexpr uint32_t kCopiersSpmm = 7;  // warps 0-3, 12, 14, 15
-constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;  // rows: tile 0..127, halo 128..
+constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;
 constexpr uint32_t kTkLrpOff = 0;
 constexpr uint32_t kTkLcolOff = kTpLrp * 2u + 16u;
 constexpr uint32_t kTkHaloOff = kTkLcolOff + kTpColCap * 2u;
 constexpr uint32_t kTkMetaBytes = ((kTkHaloOff + kTpHaloCap * 4u + 127u) / 128u) * 128u;
-constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kBBytes + kEpiBytes +
-                                  256 * 4 + 16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
+constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kBBytes + (256 + 32) * 4 +
+                                  16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
                                   16 + 1024;
-static_assert(kTkRowBytes % 1024 == 0, "row stages must keep the 1024-B swizzle alignment");
+static_assert(kTkRowBytes % 1024 == 0, "row stages keep 1024-B alignment");
 static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 static_assert(kTkSmemBytes <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
 
@@ -585,28 +208,36 @@ __device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const 
   m[2] = ptx::fadd2(m[2], make_float2(x1.x, x1.y));
   m[3] = ptx::fadd2(m[3], make_float2(x1.z, x1.w));
 }
+__device__ __forceinline__ void swap_halves(float2 (&m)[4], bool sw) {
+  if (sw) {
+    const float2 t0 = m[0], t1 = m[1];
+    m[0] = m[2];
+    m[1] = m[3];
+    m[2] = t0;
+    m[3] = t1;
+  }
+}
 
 template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
-                                                                const __grid_constant__ CUtensorMap tmap_in,
-                                                                const __grid_constant__ CUtensorMap tmap_out) {
+                                                                const __grid_constant__ CUtensorMap tmap_in) {
   constexpr bool kMma = kMode != kModeSpmm;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows
   uint8_t* sPlan = sRows + kTkRowStages * kTkRowBytes;   // [kTkMetaStages] lrp | lcol | halo list
   uint8_t* sB = sPlan + kTkMetaStages * kTkMetaBytes;
-  uint8_t* sE = sB + kBBytes;
-  float* sInv = reinterpret_cast<float*>(sE + kEpiBytes);
-  uint4* sMeta = reinterpret_cast<uint4*>(sInv + 256);  // [kTkMetaStages] TileMeta of the staged plan
+  float* sInv = reinterpret_cast<float*>(sB + kBBytes);  // 1/d, d < 256
+  float* sBias = sInv + 256;                              // layer bias by output feature
+  uint4* sMeta = reinterpret_cast<uint4*>(sBias + 32);    // [kTkMetaStages] TileMeta of the staged plan
   uint64_t* bars = reinterpret_cast<uint64_t*>(sMeta + kTkMetaStages);
-  uint64_t* full = bars;
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* m_full = tempty + 2;
+  uint64_t* full = bars;                     // [kStages] producers -> MMA (A operand in TMEM)
+  uint64_t* empty = full + kStages;          // [kStages] MMA done reading the A stage
+  uint64_t* tfull = empty + kStages;         // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;              // [2] accumulator drained
+  uint64_t* m_full = tempty + 2;             // [kTkMetaStages] plan records landed
   uint64_t* m_empty = m_full + kTkMetaStages;
-  uint64_t* r_full = m_empty + kTkMetaStages;
+  uint64_t* r_full = m_empty + kTkMetaStages;  // [kTkRowStages] tile + halo rows landed
   uint64_t* r_empty = r_full + kTkRowStages;
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(r_empty + kTkRowStages);
 
@@ -614,11 +245,15 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   const uint32_t n = a.n;
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   const uint32_t G = gridDim.x;
+  constexpr uint32_t kCopiers = kMma ? kCopiersMma : kCopiersSpmm;
 
   if (kMma)
     for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
       reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
   for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
+  if (kMma) {
+    for (uint32_t i = threadIdx.x; i < 32; i += kThreads) sBias[i] = hw.bias[i];
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], kProdWarps * 32);
@@ -633,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_init(&m_empty[s], kProdWarps * 32);
     }
     for (int s = 0; s < kTkRowStages; ++s) {
-      ptx::mbar_init(&r_full[s], 1 + 32 * (kMma ? kCopiersMma : kCopiersSpmm));  // TMA box + copier lanes
+      ptx::mbar_init(&r_full[s], 1 + 32 * kCopiers);  // TMA box (expect_tx) + each copier lane's cp.async arrival
       ptx::mbar_init(&r_empty[s], kProdWarps * 32);
     }
     ptx::mbar_fence_init();
@@ -647,10 +282,10 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
 
   // halo copier warps: the two spare warps (and, in SpMM mode, the idle
   // epilogue and MMA warps)
-  const int copier = kMma ? (warp >= kLoadWarp + 1 ? warp - (kLoadWarp + 1) : -1)
+  const int copier = kMma ? (warp > kLoadWarp ? warp - (kLoadWarp + 1) : -1)
                           : (warp < kEpiWarps ? warp : warp == kMmaWarp ? kEpiWarps : warp > kLoadWarp ? warp - 9 : -1);
   if (warp == kLoadWarp) {
-    // ===== loader: plan records and tile rows =====
+    // ===== loader: plan records and tile rows (one lane) =====
     if (lane == 0) {
       constexpr int kQ = 4;  // TileMeta records prefetched into registers beyond the plan ring
       auto meta_of = [&](uint32_t tt) -> uint4 {
@@ -685,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if (tl < ntiles) issue_plan(it + kTkMetaLead, tl, mq);
         const uint32_t rs = it % kTkRowStages;
         ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
+        tstamp(a.trace, it, 0);
         ptx::mbar_arrive_expect_tx(&r_full[rs], kTpRows * 128u);
         ptx::tma_load_2d(&tmap_in, sRows + rs * kTkRowBytes, &r_full[rs], 0, static_cast<int32_t>(t * kTileM));
       }
@@ -695,16 +331,17 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     const uint32_t sRows_s = ptx::smem_addr(sRows);
     const uint32_t gl = static_cast<uint32_t>(copier) * 32u + lane;
     const uint32_t c = gl & 7, s0 = gl >> 3;
-    constexpr uint32_t kStride = (kMma ? kCopiersMma : kCopiersSpmm) * 4u;  // rows per pass of all copier lanes
+    constexpr uint32_t kStride = kCopiers * 4u;  // rows per pass of all copier lanes
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
-      ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
-      ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
+      ptx::mbar_wait_sleep(&m_full[ms], (it / kTkMetaStages) & 1, 100);
+      ptx::mbar_wait_sleep(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, 100);
       const uint32_t hc = sMeta[ms].w;
-      if (!(hc & kTpSlow) && a.exp != 1) {
+      if (gl == 0) tstamp(a.trace, it, 1);
+      if (!(hc & kTpSlow)) {
         const uint32_t* hl = reinterpret_cast<const uint32_t*>(sPlan + ms * kTkMetaBytes + kTkHaloOff);
-        const uint32_t sbase = sRows_s + rs * kTkRowBytes + kTpRows * 128u;
+        const uint32_t sbase = sRows_s + rs * kTkRowBytes + kTpRows * 128u + c * 16u;
         // 4 halo ids per batch read before the copies are issued (the asm
         // memory clobber would otherwise serialise each LDS behind a copy)
         for (uint32_t b0 = s0; b0 < hc; b0 += 4 * kStride) {
@@ -714,17 +351,17 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t slot = b0 + u * kStride;
-            if (slot < hc)
-              ptx::cp_async16(sbase + slot * 128u + ((c ^ (slot & 7u)) << 4),
-                              a.hin + static_cast<size_t>(row[u]) * kF + 4 * c);
+            if (slot < hc) ptx::cp_async16(sbase + slot * 128u, a.hin + static_cast<size_t>(row[u]) * kF + 4 * c);
           }
         }
       }
+      if (gl == 0) tstamp(a.trace, it, 2);
       ptx::cp_async_mbar_arrive(ptx::smem_addr(&r_full[rs]));
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (kMma && warp == kMmaWarp) {
-    // ===== MMA issuer (as in sage_layer_tc_kernel) =====
+    // ===== MMA issuer: the whole warp runs the loop (warp-uniform operands
+    // stay in uniform registers), one elected lane issues =====
     constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
     const uint32_t b0s = ptx::smem_addr(sB);
     uint32_t it = 0;
@@ -732,7 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
       const uint32_t acc = it & 1, aph = (it >> 1) & 1;
       ptx::mbar_wait(&full[s], ph);
+      if (lane == 0) tstamp(a.trace, it, 8);
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
+      if (lane == 0) tstamp(a.trace, it, 9);
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
         const uint32_t d = tmem_base + kAccCol0 + acc * kAccCols;
@@ -741,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         for (uint32_t kb = 0; kb < 2; ++kb)
 #pragma unroll
           for (uint32_t kk = 0; kk < 4; ++kk) {
-            const uint32_t ahi = as + kb * 32 + kk * 8;
+            const uint32_t ahi = as + kb * 32 + kk * 8;  // h (kb 0) or m (kb 1), K = 8 columns
             const uint32_t bo = b0s + kb * 8192 + kk * 32;
             const uint64_t bhi = ptx::umma_desc_sw128(bo), blo = ptx::umma_desc_sw128(bo + 4096);
             const uint32_t first = (kb | kk) != 0;
@@ -753,11 +392,18 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         ptx::mma_commit(&tfull[acc]);
       }
       __syncwarp();
+      if (lane == 0) tstamp(a.trace, it, 10);
     }
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
-    // ===== producers =====
+    // ===== producers: 8 warps x 16 rows. Warp w may only reach its TMEM
+    // lane quadrant (w % 4): it owns tile rows 32(w%4) + 16h' .. +15 with
+    // h' = (w-4)/4; lane group r = lane/4 owns rows r and r+8 of that slice,
+    // lane j = lane%4 features 8j..8j+7 — the registers a 16x256b tcgen05.st
+    // takes (A's K order permuted to match, kcol_feature) =====
     const uint32_t lbase = (warp & 3) * 32 + ((warp - kEpiWarps) >> 2) * 16;
     const uint32_t j = lane & 3;
+    const uint32_t gp = (lane >> 2) & 1;                   // lane group parity: which half is read first
+    const uint32_t off0 = (2u * j + gp) * 16u, off1 = (2u * j + 1u - gp) * 16u;
     const uint32_t li = lbase + (lane >> 2);  // tile rows li and li + 8
     const uint32_t thr = a.hd.threshold;
     const float* hin_j = a.hin + 8 * j;
@@ -765,8 +411,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++it) {
       const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
       const uint32_t row0 = t * kTileM;
+      unsigned long long* tr = (warp == kEpiWarps && lane == 0) ? a.trace : nullptr;
+      unsigned long long* tr7 = (warp == kEpiWarps + 3 && lane == 0) ? a.trace : nullptr;
+      tstamp(tr, it, 3);
+      tstamp(tr7, it, 13);
       ptx::mbar_wait(&r_full[rs], (it / kTkRowStages) & 1);
       ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
+      tstamp(tr, it, 4);
       const uint8_t* st = sRows + rs * kTkRowBytes;
       const uint8_t* sp = sPlan + ms * kTkMetaBytes;
       const bool slow = (sMeta[ms].w & kTpSlow) != 0;
@@ -788,30 +439,28 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           d[h] = (w1 & 0x7FFFu) - lo[h];
           hd[h] = (w0 & kTpHdBit) != 0;
         }
-        const uint32_t dm = max(d[0], d[1]);
-        for (uint32_t k0 = 0; k0 < dm; k0 += 4) {
-          uint32_t loc[2][4];
+        // rows one after the other (4 neighbour rows in flight per row keeps
+        // the producers inside 128 registers)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h)
+          for (uint32_t k0 = 0; k0 < d[h]; k0 += 4) {
+            uint32_t loc[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) loc[h][u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
-          float4 x[2][4][2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
+            for (int u = 0; u < 4; ++u) loc[u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
+            float4 x[4][2];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (k0 + u < d[h]) {
-                const uint8_t* rowp = st + loc[h][u] * 128u;
-                const uint32_t c0 = (2u * j) ^ (loc[h][u] & 7u);
-                x[h][u][0] = *reinterpret_cast<const float4*>(rowp + (c0 << 4));
-                x[h][u][1] = *reinterpret_cast<const float4*>(rowp + ((c0 ^ 1u) << 4));
+                const uint8_t* rowp = st + loc[u] * 128u;
+                x[u][0] = *reinterpret_cast<const float4*>(rowp + off0);
+                x[u][1] = *reinterpret_cast<const float4*>(rowp + off1);
               }
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (k0 + u < d[h]) acc_row(m[h], x[h][u][0], x[h][u][1]);
-        }
+              if (k0 + u < d[h]) acc_row(m[h], x[u][0], x[u][1]);
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) swap_halves(m[h], gp != 0);
       } else {
         uint32_t b[2];
 #pragma unroll
@@ -834,11 +483,15 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       if (kMma) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t il = li + 8 * h;
-          hs[h][0] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j) ^ (il & 7u)) << 4));
-          hs[h][1] = *reinterpret_cast<const float4*>(st + il * 128u + (((2u * j + 1u) ^ (il & 7u)) << 4));
+          const uint8_t* rowp = st + (li + 8 * h) * 128u;
+          const float4 f0 = *reinterpret_cast<const float4*>(rowp + off0);
+          const float4 f1 = *reinterpret_cast<const float4*>(rowp + off1);
+          hs[h][0] = gp ? f1 : f0;
+          hs[h][1] = gp ? f0 : f1;
         }
       }
+      tstamp(tr, it, 5);
+      tstamp(tr7, it, 14);
       ptx::mbar_arrive(&r_empty[rs]);
       ptx::mbar_arrive(&m_empty[ms]);
 #pragma unroll
@@ -867,65 +520,87 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       if (kMma) {
         const uint32_t s = it % kStages, ph = (it / kStages) & 1;
         ptx::mbar_wait(&empty[s], ph ^ 1);
+        tstamp(tr, it, 6);
         ptx::tc_fence_after();
         const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
-        tmem_store_split(ta, hs);
-        tmem_store_split(ta + 32, mm);
+        tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
+        tmem_store_split(ta + 32, mm);  // columns 32..63 (hi), 96..127 (lo): neighbour mean
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&full[s]);
+        tstamp(tr, it, 7);
+        tstamp(tr7, it, 15);
       }
     }
   } else if (kMma && warp < kEpiWarps) {
-    // ===== epilogue (as in sage_layer_tc_kernel) =====
+    // ===== epilogue (4 warps, TMEM lane quadrant = warp). The weight image
+    // permutes the output columns by kcol_feature, so a 16x256b load gives
+    // lane j of a 4-lane group features 8j..8j+7 of two rows: whole 128-B
+    // rows leave as 256-bit stores, no staging =====
     const uint32_t q = warp;
-    uint8_t* ew = sE + q * 4096;
+    const uint32_t j = lane & 3, r4 = lane >> 2;
+    float b8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b8[k] = sBias[8 * j + k];
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
     for (uint32_t e = 0; e < my_tiles; ++e) {
       const uint32_t t = blockIdx.x + e * G;
       const uint32_t acc = e & 1, ph = (e >> 1) & 1;
       ptx::mbar_wait_sleep(&tfull[acc], ph, 200);
+      if (warp == 0 && lane == 0) tstamp(a.trace, e, 11);
       ptx::tc_fence_after();
-      float r[32];
       const uint32_t tq = tmem_base + kAccCol0 + acc * kAccCols + ((q * 32u) << 16);
-      ptx::tmem_ld_32x32b_x32(tq, r);
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + hw.bias[i], 0.0f);
       const uint32_t row0 = t * kTileM + q * 32;
       if (kMode == kModeLayer) {
-        if (lane == 0) ptx::bulk_wait_read0();
-        __syncwarp();
+        float v[2][16];
+        ptx::tmem_ld_16x256b_x4(tq, v[0]);
+        ptx::tmem_ld_16x256b_x4(tq + (16u << 16), v[1]);
+        ptx::tmem_wait_ld();
+        ptx::tmem_regs_ready(v[0]);
+        ptx::tmem_regs_ready(v[1]);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<float4*>(ew + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-              make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          ptx::tma_store_2d(&tmap_out, ew, 0, static_cast<int32_t>(row0));
-          ptx::bulk_commit();
-        }
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // register 4i+2h+e = column 8i+2j+e = feature 8j+2i+e of row r4 + 8h
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) o[2 * i + e2] = fmaxf(v[hh][4 * i + 2 * h + e2] + b8[2 * i + e2], 0.0f);
+            const uint32_t row = row0 + 16 * hh + r4 + 8 * h;
+            if (row < n)
+              ptx::stg_f8(a.hout + static_cast<size_t>(row) * kF + 8 * j, make_float4(o[0], o[1], o[2], o[3]),
+                          make_float4(o[4], o[5], o[6], o[7]));
+          }
       } else {
+        float r[32];
+        ptx::tmem_ld_32x32b_x32(tq, r);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        // column c holds output feature kcol_feature(c)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = fmaxf(r[c] + hw.bias[kcol_feature(c)], 0.0f);
         const uint32_t row = row0 + lane;
         float best = 0.f;
         uint32_t arg = 0;
 #pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c) {
-          if (c < static_cast<int>(a.classes)) {
-            float s = 0.f;
+        for (int cl = 0; cl < kMaxClasses; ++cl) {
+          if (cl < static_cast<int>(a.classes)) {
+            float sc = 0.f;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) s = fmaf(r[k], hw.w[k][c], s);
-            s += hw.b[c];
-            if (c == 0 || s > best) { best = s; arg = c; }
-            if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + c] = s;
+            for (int k = 0; k < 32; ++k) sc = fmaf(r[kcol_inverse(k)], hw.w[k][cl], sc);
+            sc += hw.b[cl];
+            if (cl == 0 || sc > best) { best = sc; arg = cl; }
+            if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + cl] = sc;
           }
         }
         if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
       }
+      if (warp == 0 && lane == 0) tstamp(a.trace, e, 12);
     }
-    if (kMode == kModeLayer && lane == 0) ptx::bulk_wait_all();
   }
 
   if (kMma) {
@@ -1100,114 +775,6 @@ __global__ void __launch_bounds__(256) hd_mean_feat_kernel(const uint32_t* __res
   }
 }
 
-// Standalone LD aggregation (groot_spmm_mean, f = 32): the same gather as the
-// fused layer, writing the mean rows (HD rows are written by hd_mean32_kernel).
-// Standalone LD aggregation (groot_spmm_mean, f = 32) — the LD-kernel of the
-// degree-polarised split: persistent warps, 8-lane groups (one 128-byte row
-// per group, LDG.128 per lane), 8 rows per warp per step with the same
-// rolling index pipeline as the fused layer (features of step i, col_idx of
-// step i+1 and row_ptr of step i+2 in flight together). HD rows are written
-// by hd_mean32_kernel.
-template <int NR>
-__device__ __forceinline__ uint32_t dmax_of(const uint32_t (&d)[NR]) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int q = 0; q < NR; ++q) m = max(m, d[q]);
-  return m;
-}
-
-template <int NR, int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks) spmm_mean32_kernel(uint32_t n, const uint32_t* __restrict__ rp,
-                                                                     const uint32_t* __restrict__ col,
-                                                                     const float* __restrict__ H, uint32_t thr,
-                                                                     float* __restrict__ out) {
-  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7, gbase = lane & 24;
-  const uint32_t W = gridDim.x * (blockDim.x >> 5);               // warps in the grid
-  const uint32_t w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr uint32_t R = 4 * NR;  // rows per warp step
-  const uint32_t nchunks = (n + R - 1) / R;
-  auto rp_load = [&](uint32_t ch, uint32_t (&b)[NR], uint32_t (&e)[NR]) {
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const uint32_t r = ch * R + q * 4 + g;
-      const bool ok = ch < nchunks && r < n;
-      b[q] = ok ? __ldg(rp + r) : 0u;
-      e[q] = ok ? __ldg(rp + r + 1) : 0u;
-    }
-  };
-  auto col_load = [&](const uint32_t (&b)[NR], const uint32_t (&d)[NR], uint32_t (&c)[NR]) {
-#pragma unroll
-    for (int q = 0; q < NR; ++q) c[q] = (static_cast<uint32_t>(j) < d[q] && d[q] < thr) ? __ldg(col + b[q] + j) : 0u;
-  };
-  uint32_t b0[NR], d0[NR], c0[NR], b1[NR], e1[NR];
-  {
-    uint32_t e0[NR];
-    rp_load(w0, b0, e0);
-#pragma unroll
-    for (int q = 0; q < NR; ++q) d0[q] = e0[q] - b0[q];
-    col_load(b0, d0, c0);
-    rp_load(w0 + W, b1, e1);
-  }
-  constexpr int U = 4;
-  for (uint32_t ch = w0; ch < nchunks; ch += W) {
-    uint32_t dl[NR];
-#pragma unroll
-    for (int q = 0; q < NR; ++q) dl[q] = d0[q] < thr ? d0[q] : 0u;
-    float4 v[NR][U];
-#pragma unroll
-    for (int q = 0; q < NR; ++q)
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t ci = __shfl_sync(0xffffffffu, c0[q], gbase + k);
-        if (static_cast<uint32_t>(k) < dl[q]) v[q][k] = ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j);
-      }
-    uint32_t d1[NR], c1[NR], b2[NR], e2[NR];
-#pragma unroll
-    for (int q = 0; q < NR; ++q) d1[q] = e1[q] - b1[q];
-    col_load(b1, d1, c1);
-    rp_load(ch + 2 * W, b2, e2);
-    float4 m[NR];
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      m[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (static_cast<uint32_t>(k) < dl[q]) m[q] = f4add(m[q], v[q][k]);
-    }
-    const uint32_t dmax = __reduce_max_sync(0xffffffffu, dmax_of<NR>(dl));
-    if (dmax > static_cast<uint32_t>(U)) {
-      for (uint32_t k0 = 0; k0 < dmax; k0 += 8) {
-        uint32_t cc[NR];
-#pragma unroll
-        for (int q = 0; q < NR; ++q) cc[q] = k0 == 0 ? c0[q] : ((k0 + j < dl[q]) ? __ldg(col + b0[q] + k0 + j) : 0u);
-        for (uint32_t kk = (k0 == 0 ? U : 0); kk < 8; ++kk) {
-#pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            const uint32_t ci = __shfl_sync(0xffffffffu, cc[q], gbase + kk);
-            if (k0 + kk < dl[q]) m[q] = f4add(m[q], ptx::ldg_f4(H + static_cast<size_t>(ci) * kF + 4 * j));
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const uint32_t r = ch * R + q * 4 + g;
-      if (r < n && d0[q] < thr) {
-        const float inv = d0[q] > 0 ? 1.0f / static_cast<float>(d0[q]) : 0.0f;
-        *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * kF + 4 * j) = f4scale(m[q], inv);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      b0[q] = b1[q];
-      d0[q] = d1[q];
-      c0[q] = c1[q];
-      b1[q] = b2[q];
-      e1[q] = e2[q];
-    }
-  }
-}
-
 // General CSR SpMM (spmm::execute over CsrMatrix<float>): 8 lanes per row,
 // columns strided by 8, nonzeros accumulated in order. vals == nullptr -> 1/deg.
 __global__ void __launch_bounds__(256) spmm_generic_kernel(uint32_t rows, const uint32_t* __restrict__ rp,
@@ -1337,13 +904,20 @@ void classify_rows(groot_graph* g, uint32_t thr) {
 
 void build_tile_plan(groot_graph* g, uint32_t thr);
 
-// GROOT_LAYER=legacy selects the register-gather fused layer (A/B knob).
-static bool use_tile_plan() {
-  static const bool v = [] {
-    const char* e = std::getenv("GROOT_LAYER");
-    return !(e && std::strcmp(e, "legacy") == 0);
-  }();
-  return v;
+// Kernel arguments common to the fused layer and the SpMM: CSR (slow tiles),
+// input rows, HD band, tile plan.
+static LayerArgs plan_args(const groot_graph* g, const float* hin, const HdInfo& hd) {
+  LayerArgs a{};
+  a.n = g->n;
+  a.rp = g->rp.p;
+  a.col = g->col.p;
+  a.hin = hin;
+  a.hd = hd;
+  a.tmeta = reinterpret_cast<const TileMeta*>(g->tp_meta.p);
+  a.lrp = g->tp_lrp.p;
+  a.lcol = g->tp_lcol.p;
+  a.halo = g->tp_halo.p;
+  return a;
 }
 
 static void ensure_activations(groot_graph* g) {
@@ -1353,8 +927,7 @@ static void ensure_activations(groot_graph* g) {
 }
 
 // TMA descriptor for an n x 32 fp32 row-major activation matrix: 32 x box_rows
-// boxes, SWIZZLE_128B (chunk c of row i at i*128 + ((c ^ (i&7)) << 4)); rows
-// past n read as zeros.
+// boxes, unswizzled (row i of the box at i * 128 B); rows past n read as zeros.
 static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1372,7 +945,7 @@ static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) 
   const cuuint32_t box[2] = {kF, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(GROOT_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return m;
@@ -1384,13 +957,6 @@ static void set_tc_smem() {
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-  // Smallest shared-memory carve-out that fits: the rest of the 256 KB array is
-  // L1, which catches the in-tile neighbour re-reads of the gather.
-  const int pct = static_cast<int>((kSmemBytes + 1024) * 100 / (228 * 1024)) + 1;
-  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_layer_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   done = true;
 }
 
@@ -1418,6 +984,7 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
                  *reinterpret_cast<const Layer0W*>(m->l0w));
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+  if (m->depth > 1) build_tile_plan(g, g->hd_threshold);
   for (uint32_t l = 1; l < m->depth; ++l) {
     const float* hin = g->act[(l - 1) & 1].p;
     float* hout = g->act[l & 1].p;
@@ -1426,21 +993,16 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
       GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
     }
-    LayerArgs a{};
-    a.n = n;
-    a.rp = g->rp.p;
-    a.col = g->col.p;
-    a.hin = hin;
+    LayerArgs a = plan_args(g, hin, hd);
     a.hout = hout;
     a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
-    a.bias = m->bias.p + static_cast<size_t>(l - 1) * kF;
-    a.hd = hd;
-    a.head = m->head.p;
     a.classes = m->classes;
     a.cls = cls;
     a.logits = logits;
-    a.labels = g->labels.p;
-    a.confusion = confusion;
+    const unsigned grid = std::min<uint32_t>(ntiles, sms);
+    const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
+    HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
+    std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
     static const char* trace_path = std::getenv("GROOT_TRACE");
     DevBuf<unsigned long long> trace;
     if (trace_path && l == 1) {
@@ -1448,30 +1010,12 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
       trace.zero();
       a.trace = trace.p;
     }
-    const unsigned grid = std::min<uint32_t>(ntiles, sms);
-    const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
-    const CUtensorMap tmap = make_rows32_tmap(hout, n, 32);
-    HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
-    std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
-    if (use_tile_plan()) {
-      build_tile_plan(g, g->hd_threshold);
-      a.tmeta = reinterpret_cast<const TileMeta*>(g->tp_meta.p);
-      a.lrp = g->tp_lrp.p;
-      a.lcol = g->tp_lcol.p;
-      a.halo = g->tp_halo.p;
-      if (l + 1 == m->depth) {
-        ProfScope ps("sage_layer_tc_last");
-        GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in, tmap);
-      } else {
-        ProfScope ps("sage_layer_tc");
-        GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in, tmap);
-      }
-    } else if (l + 1 == m->depth) {
+    if (l + 1 == m->depth) {
       ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_layer_tc_kernel<true>, grid, kThreads, kSmemBytes, a, hw, tmap_in, tmap);
+      GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
     } else {
       ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_layer_tc_kernel<false>, grid, kThreads, kSmemBytes, a, hw, tmap_in, tmap);
+      GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
     }
     if (a.trace) {
       std::vector<unsigned long long> h(64 * 16);
@@ -1529,42 +1073,15 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
       GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, dense, out, 1);
     }
-    if (use_tile_plan()) {
-      set_tc_smem();
-      build_tile_plan(g, hd.threshold);
-      ProfScope ps("spmm_mean32");
-      LayerArgs a{};
-      a.n = g->n;
-      a.rp = g->rp.p;
-      a.col = g->col.p;
-      a.hin = dense;
-      a.hd = hd;
-      a.tmeta = reinterpret_cast<const TileMeta*>(g->tp_meta.p);
-      a.lrp = g->tp_lrp.p;
-      a.lcol = g->tp_lcol.p;
-      a.halo = g->tp_halo.p;
-      a.spmm_out = out;
-      a.exp = env_u32("GROOT_TK_EXP", 0);
-      const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(dense), g->n, kTileM);
-      const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
-      HeadW hw{};
-      GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, kTkSmemBytes, a, hw,
-                   tmap_in, tmap_in);
-      return;
-    }
+    set_tc_smem();
+    build_tile_plan(g, hd.threshold);
     ProfScope ps("spmm_mean32");
-    static const int occ = [] {
-      const char* e = std::getenv("GROOT_SPMM_BLOCKS");
-      return e ? std::atoi(e) : 2;
-    }();
-    const uint32_t thr = hd.threshold;
-    switch (occ) {
-      case 1: GROOT_LAUNCH((spmm_mean32_kernel<2, 2>), sms * 2, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
-      case 2: GROOT_LAUNCH((spmm_mean32_kernel<1, 4>), sms * 4, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
-      case 3: GROOT_LAUNCH((spmm_mean32_kernel<1, 6>), sms * 6, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
-      case 4: GROOT_LAUNCH((spmm_mean32_kernel<1, 8>), sms * 8, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
-      default: GROOT_LAUNCH((spmm_mean32_kernel<2, 3>), sms * 3, 256, 0, g->n, g->rp.p, g->col.p, dense, thr, out); break;
-    }
+    LayerArgs a = plan_args(g, dense, hd);
+    a.spmm_out = out;
+    const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(dense), g->n, kTileM);
+    const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
+    HeadW hw{};
+    GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, kTkSmemBytes, a, hw, tmap_in);
   } else {
     GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
                  nullptr, dense, f, out);
@@ -1615,7 +1132,7 @@ void model_upload(groot_model* m) {
         const double* W = kb ? wn : ws;
         for (uint32_t nn = 0; nn < 32; ++nn)
           for (uint32_t k = 0; k < 32; ++k) {
-            const float v = static_cast<float>(W[kcol_feature(k) * H + nn]);  // K row k <- feature
+            const float v = static_cast<float>(W[kcol_feature(k) * H + kcol_feature(nn)]);  // K and N permuted
             const float hi = tf32_rna_host(v), lo = v - hi;
             const uint32_t o = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
             std::memcpy(base + kb * 8192 + o, &hi, 4);

@@ -139,6 +139,28 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&r)[32
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Warp-collective load of 16 TMEM lanes x 32 columns (the 16x256b.x4 layout of
+// tmem_st_16x256b_x4): lane 4r+j gets v[4i+2h+e] = TMEM lane (taddr.lane + r +
+// 8h), column taddr.col + 8i + 2j + e. Completes at tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, float (&r)[16]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Compiler-level dependency: the registers of a tcgen05.ld are read only after
+// this point (place it after tmem_wait_ld()).
+__device__ __forceinline__ void tmem_regs_ready(float (&r)[16]) {
+  asm volatile(""
+               : "+f"(r[0]), "+f"(r[1]), "+f"(r[2]), "+f"(r[3]), "+f"(r[4]), "+f"(r[5]), "+f"(r[6]), "+f"(r[7]),
+                 "+f"(r[8]), "+f"(r[9]), "+f"(r[10]), "+f"(r[11]), "+f"(r[12]), "+f"(r[13]), "+f"(r[14]),
+                 "+f"(r[15])::"memory");
+}
+
 // tcgen05.mma with A read from tensor memory (M=128: row i = TMEM lane i,
 // K element k = column a_tmem + k), B from a shared-memory descriptor.
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
