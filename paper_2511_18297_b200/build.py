@@ -38,18 +38,27 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _extra() -> list:
+    # development knob, e.g. GROOT_NVCC_FLAGS=-DGROOT_TRACE_BUILD (timeline stamps)
+    return os.environ.get("GROOT_NVCC_FLAGS", "").split()
+
+
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + \
            [os.path.join(ROOT, "include", "groot.h"), __file__]
-    if not _stale(obj, deps):
+    stamp = obj + ".flags"
+    flags = " ".join(_extra())
+    if not _stale(obj, deps) and os.path.exists(stamp) and open(stamp).read() == flags:
         return obj
-    cmd = [nvcc()] + NVFLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [nvcc()] + NVFLAGS + _extra() + ["-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
     with open(obj + ".ptxas.txt", "w") as f:
         f.write(res.stderr)
+    with open(stamp, "w") as f:
+        f.write(flags)
     if verbose:
         print(f"[build] {src}", file=sys.stderr)
     return obj

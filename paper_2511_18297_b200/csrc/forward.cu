@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 #include <cuda.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -882,6 +883,7 @@ __global__ void hd_flag_kernel(uint32_t n, const uint32_t* __restrict__ rp, uint
 
 void classify_rows(groot_graph* g, uint32_t thr) {
   if (g->hd_threshold == thr && (g->num_hd == 0 || g->hd_rows.p)) return;
+  ProfScope ps("classify_rows");
   DevBuf<uint8_t> flag(g->n);
   DevBuf<uint32_t> out(g->n), cnt(1);
   if (g->n) GROOT_LAUNCH(hd_flag_kernel, blocks_for(g->n, 256), 256, 0, g->n, g->rp.p, thr, flag.p);
@@ -965,9 +967,21 @@ static void set_tc_smem() {
 void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* logits, unsigned long long* confusion) {
   require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
   if (g->n == 0) return;
+  static const bool host_timing = std::getenv("GROOT_HOST_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto h0 = now();
   set_tc_smem();
   classify_rows(g, hd_threshold());
+  const auto h1 = now();
   ensure_activations(g);
+  const auto h2 = now();
+  if (m->depth > 1) build_tile_plan(g, g->hd_threshold);
+  const auto h3 = now();
+  if (host_timing) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[forward] classify %.2f ms, activations %.2f ms, tile plan %.2f ms (host)\n", ms(h0, h1),
+                 ms(h1, h2), ms(h2, h3));
+  }
   const uint32_t n = g->n;
   HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
   const unsigned sms = static_cast<unsigned>(num_sms());
@@ -984,7 +998,6 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
                  *reinterpret_cast<const Layer0W*>(m->l0w));
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
-  if (m->depth > 1) build_tile_plan(g, g->hd_threshold);
   for (uint32_t l = 1; l < m->depth; ++l) {
     const float* hin = g->act[(l - 1) & 1].p;
     float* hout = g->act[l & 1].p;

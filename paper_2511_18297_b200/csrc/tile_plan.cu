@@ -1,17 +1,17 @@
 // tile_plan.cu — builds the per-tile gather plan (tile_plan.cuh) on the device.
 //
-// One CTA per 128-row tile, two passes (count, fill) around two prefix sums:
-//   * LD degree of each row (degree < threshold; HD rows get 0 and a flag),
-//     block scan -> the tile's local row offsets (lrp) and LD nonzero count L;
-//   * out-of-tile columns of the LD rows collected in shared memory, bitonic
-//     sort, unique -> the halo list (ascending global row ids);
-//   * each LD nonzero re-indexed to its local slot: c - row0 inside the tile,
+// One warp per 128-row tile, one pass, no global scans:
+//   * LD degree of each row (degree < threshold; HD rows are flagged and
+//     skipped) -> row offsets into the tile's lcol segment (lrp);
+//   * out-of-tile columns of the LD rows gathered into shared memory (warp
+//     ballots), bitonic sort, unique -> the halo list (ascending global ids),
+//     written to the tile's fixed kTpHaloCap-entry slot;
+//   * each LD nonzero re-indexed to its local slot, stored at its own CSR
+//     position (lcol is aligned with col_idx): c - row0 inside the tile,
 //     128 + rank of c in the halo list otherwise.
 // Deterministic (sorted halo, nonzero order kept). Built once per graph and
 // row-classifier threshold and cached on the graph, like the reference's
 // make_context builds its plans once per graph (src/gnn.cpp:140-170).
-#include <cub/cub.cuh>
-
 #include <cstdlib>
 
 #include "common.cuh"
@@ -21,14 +21,7 @@ namespace groot {
 
 namespace {
 
-constexpr int kTpThreads = 128;
-
-struct TpShared {
-  uint32_t keys[kTpColCap];
-  uint32_t uniq[kTpColCap];
-  typename cub::BlockScan<uint32_t, kTpThreads>::TempStorage scan;
-  uint32_t cnt;
-};
+constexpr int kTpWarps = 4;  // tiles per CTA
 
 __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t len, uint32_t x) {
   uint32_t lo = 0, hi = len;
@@ -39,97 +32,107 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
   return lo;
 }
 
-// kFill = false: lcnt[t] / hcnt[t] = staged lcol / halo-list entries (padded).
-// kFill = true : writes meta, lrp, lcol, halo at the scanned offsets.
-template <bool kFill>
-__global__ void __launch_bounds__(kTpThreads) tile_plan_kernel(uint32_t n, const uint32_t* __restrict__ rp,
-                                                               const uint32_t* __restrict__ col, uint32_t thr,
-                                                               uint32_t halo_cap, uint32_t* lcnt, uint32_t* hcnt,
-                                                               TileMeta* meta, uint16_t* lrp, uint16_t* lcol,
-                                                               uint32_t* halo, uint32_t* slow_count) {
-  __shared__ TpShared sh;
-  const uint32_t tid = threadIdx.x;
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t& total) {
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= static_cast<uint32_t>(o)) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+__global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+                                                                  const uint32_t* __restrict__ col, uint32_t thr,
+                                                                  uint32_t halo_cap, TileMeta* meta, uint16_t* lrp,
+                                                                  uint16_t* lcol, uint32_t* halo,
+                                                                  uint32_t* slow_count) {
+  __shared__ uint32_t keys_all[kTpWarps][kTpColCap];
+  __shared__ uint32_t uniq_all[kTpWarps][kTpHaloCap + 1];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* keys = keys_all[wib];
+  uint32_t* uniq = uniq_all[wib];
   const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
-  using Scan = cub::BlockScan<uint32_t, kTpThreads>;
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint32_t row0 = t * kTpRows, r = row0 + tid;
-    uint32_t b = 0, d = 0;
-    if (r < n) {
-      b = rp[r];
-      d = rp[r + 1] - b;
+  for (uint32_t t = blockIdx.x * kTpWarps + wib; t < ntiles; t += gridDim.x * kTpWarps) {
+    const uint32_t row0 = t * kTpRows;
+    uint32_t b[4], d[4];
+    bool hd[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // rows row0 + 32i + lane: prefix order is i-major
+      const uint32_t r = min(row0 + 32u * i + lane, n);
+      b[i] = rp[r];
+      d[i] = r < n ? rp[r + 1] - b[i] : 0u;
+      hd[i] = d[i] >= thr;
     }
-    const bool hd = d >= thr;
-    const uint32_t dl = hd ? 0u : d;
-    uint32_t off, L;
-    Scan(sh.scan).ExclusiveSum(dl, off, L);
-    bool slow = L > kTpColCap;
+    const uint32_t base = __shfl_sync(0xffffffffu, b[0], 0);
+    const uint32_t end = rp[min(row0 + kTpRows, n)];
+    const uint32_t loff = base & ~7u;
+    const uint32_t lcnt = (end - loff + 7u) & ~7u;
+    bool slow = lcnt > kTpColCap;
     uint32_t H = 0;
     if (!slow) {
-      if (tid == 0) sh.cnt = 0;
-      __syncthreads();
-      for (uint32_t k = 0; k < dl; ++k) {
-        const uint32_t c = col[b + k];
-        if (c - row0 >= kTpRows) sh.keys[atomicAdd(&sh.cnt, 1u)] = c;
+      // out-of-tile columns of the LD rows
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t dl = hd[i] ? 0u : d[i];
+        const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
+        for (uint32_t k = 0; k < dmax; ++k) {
+          const uint32_t c = k < dl ? col[b[i] + k] : row0;
+          const bool out = k < dl && c - row0 >= kTpRows;
+          const uint32_t m = __ballot_sync(0xffffffffu, out);
+          if (out) keys[cnt + __popc(m & ((1u << lane) - 1u))] = c;
+          cnt += __popc(m);
+        }
       }
-      __syncthreads();
-      const uint32_t O = sh.cnt;
-      uint32_t P = 1;
-      while (P < O) P <<= 1;
-      for (uint32_t i = O + tid; i < P; i += kTpThreads) sh.keys[i] = 0xFFFFFFFFu;
-      __syncthreads();
+      uint32_t P = 32;
+      while (P < cnt) P <<= 1;
+      for (uint32_t i = cnt + lane; i < P; i += 32) keys[i] = 0xFFFFFFFFu;
+      __syncwarp();
       for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-          for (uint32_t i = tid; i < P; i += kTpThreads) {
-            const uint32_t ixj = i ^ j;
-            if (ixj > i) {
-              const uint32_t a = sh.keys[i], c = sh.keys[ixj];
-              if ((a > c) == ((i & k) == 0)) {
-                sh.keys[i] = c;
-                sh.keys[ixj] = a;
-              }
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t x = lane; x < P / 2; x += 32) {
+            const uint32_t i = 2 * jj * (x / jj) + (x % jj), p = i + jj;
+            const uint32_t u = keys[i], v = keys[p];
+            if ((u > v) == ((i & k) == 0)) {
+              keys[i] = v;
+              keys[p] = u;
             }
           }
-          __syncthreads();
+          __syncwarp();
         }
-      // unique: thread tid owns keys [tid*per, tid*per + per)
-      const uint32_t per = (O + kTpThreads - 1) / kTpThreads;
-      const uint32_t i0 = min(tid * per, O), i1 = min(i0 + per, O);
+      // unique: lane owns keys [lane*per, lane*per + per)
+      const uint32_t per = (cnt + 31) / 32;
+      const uint32_t i0 = min(lane * per, cnt), i1 = min(i0 + per, cnt);
       uint32_t u = 0;
-      for (uint32_t i = i0; i < i1; ++i) u += (i == 0 || sh.keys[i] != sh.keys[i - 1]);
-      uint32_t uo;
-      Scan(sh.scan).ExclusiveSum(u, uo, H);
-      for (uint32_t i = i0; i < i1; ++i)
-        if (i == 0 || sh.keys[i] != sh.keys[i - 1]) sh.uniq[uo++] = sh.keys[i];
-      __syncthreads();
+      for (uint32_t i = i0; i < i1; ++i) u += (i == 0 || keys[i] != keys[i - 1]);
+      uint32_t pos = warp_excl_scan(u, lane, H);
       slow = H > halo_cap;
+      if (!slow)
+        for (uint32_t i = i0; i < i1; ++i)
+          if (i == 0 || keys[i] != keys[i - 1]) uniq[pos++] = keys[i];
+      __syncwarp();
     }
-    const uint32_t lpad = slow ? 0u : (L + 7u) & ~7u;
-    const uint32_t hpad = slow ? 0u : (H + 3u) & ~3u;
-    if (!kFill) {
-      if (tid == 0) {
-        lcnt[t] = lpad;
-        hcnt[t] = hpad;
-      }
-    } else {
-      const uint32_t lo = lcnt[t], ho = hcnt[t];  // scanned offsets
-      if (tid == 0) {
-        meta[t] = TileMeta{lo, ho, lpad, slow ? kTpSlow : H};
-        if (slow) atomicAdd(slow_count, 1u);
-      }
-      uint16_t* lr = lrp + static_cast<size_t>(t) * kTpLrp;
-      lr[tid] = static_cast<uint16_t>(slow ? 0u : (off | (hd ? kTpHdBit : 0u)));
-      if (tid < kTpLrp - kTpRows) lr[kTpRows + tid] = static_cast<uint16_t>(slow ? 0u : L);
-      if (!slow) {
-        for (uint32_t i = tid; i < hpad; i += kTpThreads) halo[ho + i] = sh.uniq[min(i, H - 1)];
-        for (uint32_t k = 0; k < dl; ++k) {
-          const uint32_t c = col[b + k];
-          const uint32_t loc = (c - row0 < kTpRows) ? c - row0 : kTpRows + lower_bound_u32(sh.uniq, H, c);
-          lcol[lo + off + k] = static_cast<uint16_t>(loc);
-        }
-        for (uint32_t i = L + tid; i < lpad; i += kTpThreads) lcol[lo + i] = 0;
+    if (lane == 0) {
+      meta[t] = TileMeta{loff, t * kTpHaloCap, slow ? 0u : lcnt, slow ? kTpSlow : H};
+      if (slow) atomicAdd(slow_count, 1u);
+    }
+    if (slow) continue;
+    uint16_t* lr = lrp + static_cast<size_t>(t) * kTpLrp;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lr[32 * i + lane] = static_cast<uint16_t>((b[i] - loff) | (hd[i] ? kTpHdBit : 0u));
+    if (lane < kTpLrp - kTpRows) lr[kTpRows + lane] = static_cast<uint16_t>(end - loff);
+    for (uint32_t i = lane; i < ((H + 3u) & ~3u); i += 32) halo[t * kTpHaloCap + i] = uniq[min(i, H - 1)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (hd[i]) continue;
+      for (uint32_t k = 0; k < d[i]; ++k) {
+        const uint32_t c = col[b[i] + k];
+        const uint32_t loc = (c - row0 < kTpRows) ? c - row0 : kTpRows + lower_bound_u32(uniq, H, c);
+        lcol[b[i] + k] = static_cast<uint16_t>(loc);
       }
     }
-    __syncthreads();
   }
 }
 
@@ -150,22 +153,15 @@ void build_tile_plan(groot_graph* g, uint32_t thr) {
   const uint32_t n = g->n;
   const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
   if (ntiles == 0) return;
-  const unsigned grid = std::min<uint32_t>(ntiles, static_cast<uint32_t>(num_sms()) * 16u);
-  DevBuf<uint32_t> lc(ntiles + 1ull), hc(ntiles + 1ull), loff(ntiles + 1ull), hoff(ntiles + 1ull), slow(1);
-  GROOT_LAUNCH(tile_plan_kernel<false>, grid, kTpThreads, 0, n, g->rp.p, g->col.p, thr, cap, lc.p, hc.p, nullptr,
-               nullptr, nullptr, nullptr, nullptr);
-  exclusive_scan_u32(lc.p, loff.p, ntiles);
-  exclusive_scan_u32(hc.p, hoff.p, ntiles);
-  uint32_t tot[2];
-  GROOT_CUDA(cudaMemcpyAsync(&tot[0], loff.p + ntiles, 4, cudaMemcpyDeviceToHost, stream()));
-  GROOT_CUDA(cudaMemcpyAsync(&tot[1], hoff.p + ntiles, 4, cudaMemcpyDeviceToHost, stream()));
-  stream_sync();
+  ProfScope ps("tile_plan");
   g->tp_meta.alloc(4ull * ntiles);
   g->tp_lrp.alloc(static_cast<size_t>(ntiles) * kTpLrp);
-  g->tp_lcol.alloc(tot[0] + 8ull);
-  g->tp_halo.alloc(tot[1] + 4ull);
+  g->tp_lcol.alloc(g->nnz + 16ull);
+  g->tp_halo.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
+  DevBuf<uint32_t> slow(1);
   slow.zero();
-  GROOT_LAUNCH(tile_plan_kernel<true>, grid, kTpThreads, 0, n, g->rp.p, g->col.p, thr, cap, loff.p, hoff.p,
+  const unsigned grid = std::min<uint32_t>((ntiles + kTpWarps - 1) / kTpWarps, static_cast<uint32_t>(num_sms()) * 8u);
+  GROOT_LAUNCH(tile_plan_kernel, grid, kTpWarps * 32, 0, n, g->rp.p, g->col.p, thr, cap,
                reinterpret_cast<TileMeta*>(g->tp_meta.p), g->tp_lrp.p, g->tp_lcol.p, g->tp_halo.p, slow.p);
   slow.download(&g->tp_slow, 1);
   stream_sync();

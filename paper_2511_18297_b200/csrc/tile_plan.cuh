@@ -32,9 +32,13 @@ constexpr uint32_t kTpLrp = 136;       // u16 row offsets per tile (129 used; 27
 constexpr uint32_t kTpSlow = 1u << 31; // meta.w flag: gather from the global CSR
 constexpr uint32_t kTpHdBit = 0x8000u; // lrp entry flag: row is HD (mean computed by the HD kernel)
 
-// Per-tile record (16 B): lcol offset (entries, multiple of 8), halo list
-// offset (entries, multiple of 4), staged lcol entries (multiple of 8),
-// halo row count | kTpSlow.
+// Layout: lcol is aligned with col_idx (entry e = local slot of nonzero e;
+// entries of HD rows are not written), each tile's halo list sits in a fixed
+// kTpHaloCap-entry slot, lrp holds the rows' offsets into the tile's staged
+// lcol segment [lcol_off, lcol_off + lcol_cnt) | kTpHdBit.
+// Per-tile record (16 B): lcol segment start (entries, multiple of 8), halo
+// list offset (= tile * kTpHaloCap), staged lcol entries (multiple of 8; 0 if
+// slow), halo row count | kTpSlow.
 struct TileMeta {
   uint32_t lcol_off, halo_off, lcol_cnt, halo;
 };
