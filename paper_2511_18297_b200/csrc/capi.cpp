@@ -6,6 +6,7 @@
 // ASG1 model format (src/gnn.cpp:330-372). Everything on the data path —
 // features, CSR, batch, partition, regrow, materialize, forward, classify —
 // runs in the CUDA kernels of graph_build.cu / forward.cu.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -712,9 +713,15 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
                        uint64_t* confusion, double* accuracy) {
   return guarded([&] {
     need(m, "groot_classify_aig");
+    static const bool host_timing = std::getenv("GROOT_HOST_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     groot_graph* g1 = encode(ni, na, ands, no, outs, labels);
     groot_graph* g = g1;
     try {
+      if (host_timing) stream_sync();
+      const auto t1 = now();
       if (copies > 1) {
         g = batch(g1, copies);
         delete g1;
@@ -722,14 +729,22 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
       } else if (copies < 1) {
         fail(GROOT_EINVAL, "batch: copy count must be >= 1");
       }
+      if (host_timing) stream_sync();
+      const auto t2 = now();
       DevBuf<uint8_t> cls(g->n);
       DevBuf<unsigned long long> conf(25);
       conf.zero();
       forward_device(m, g, cls.p, nullptr, conf.p);
+      if (host_timing) stream_sync();
+      const auto t3 = now();
       uint64_t h[25];
       conf.download(reinterpret_cast<unsigned long long*>(h), 25);
       if (labels_out) cls.download(labels_out, g->n);
       stream_sync();
+      const auto t4 = now();
+      if (host_timing)
+        std::fprintf(stderr, "[classify_aig] encode %.2f ms, batch %.2f ms, forward %.2f ms, download %.2f ms\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
       finish_confusion(h, g->n, confusion, accuracy);
     } catch (...) {
       delete g1;

@@ -3,12 +3,12 @@
 // One warp per 128-row tile, one pass, no global scans:
 //   * LD degree of each row (degree < threshold; HD rows are flagged and
 //     skipped) -> row offsets into the tile's lcol segment (lrp);
-//   * out-of-tile columns of the LD rows gathered into shared memory (warp
-//     ballots), bitonic sort, unique -> the halo list (ascending global ids),
-//     written to the tile's fixed kTpHaloCap-entry slot;
 //   * each LD nonzero re-indexed to its local slot, stored at its own CSR
-//     position (lcol is aligned with col_idx): c - row0 inside the tile,
-//     128 + rank of c in the halo list otherwise.
+//     position (lcol is aligned with col_idx): c - row0 inside the tile;
+//   * out-of-tile columns collected in a shared-memory hash set (dedup),
+//     compacted and bitonic-sorted -> the halo list (ascending global ids, the
+//     tile's fixed kTpHaloCap-entry slot); each out-of-tile nonzero gets 128 +
+//     the rank of its column (looked up through the set).
 // Deterministic (sorted halo, nonzero order kept). Built once per graph and
 // row-classifier threshold and cached on the graph, like the reference's
 // make_context builds its plans once per graph (src/gnn.cpp:140-170).
@@ -17,30 +17,32 @@
 #include "common.cuh"
 #include "tile_plan.cuh"
 
+static_assert(groot::kTpHaloCap <= 256, "halo list sort buffer");
+
 namespace groot {
 
 namespace {
 
-constexpr int kTpWarps = 4;  // tiles per CTA
+constexpr int kTpWarps = 4;      // tiles per CTA
 
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t len, uint32_t x) {
-  uint32_t lo = 0, hi = len;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
+constexpr uint32_t kHashSlots = 512;  // per-tile open-addressing set of out-of-tile columns
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t hslot(uint32_t c) { return (c * 2654435761u) >> (32 - 9); }
+
+// Insert c (warp-divergent callers allowed); returns its slot.
+__device__ __forceinline__ uint32_t hash_insert(uint32_t* hk, uint32_t c) {
+  uint32_t h = hslot(c);
+  while (true) {
+    const uint32_t old = atomicCAS(&hk[h], kEmpty, c);
+    if (old == kEmpty || old == c) return h;
+    h = (h + 1) & (kHashSlots - 1);
   }
-  return lo;
 }
-
-__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t& total) {
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= static_cast<uint32_t>(o)) x += y;
-  }
-  total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
+__device__ __forceinline__ uint32_t hash_find(const uint32_t* hk, uint32_t c) {
+  uint32_t h = hslot(c);
+  while (hk[h] != c) h = (h + 1) & (kHashSlots - 1);
+  return h;
 }
 
 __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, const uint32_t* __restrict__ rp,
@@ -48,10 +50,12 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
                                                                   uint32_t halo_cap, TileMeta* meta, uint16_t* lrp,
                                                                   uint16_t* lcol, uint32_t* halo,
                                                                   uint32_t* slow_count) {
-  __shared__ uint32_t keys_all[kTpWarps][kTpColCap];
-  __shared__ uint32_t uniq_all[kTpWarps][kTpHaloCap + 1];
+  __shared__ uint32_t hk_all[kTpWarps][kHashSlots];    // set of out-of-tile columns
+  __shared__ uint16_t hv_all[kTpWarps][kHashSlots];    // their rank in the sorted halo list
+  __shared__ uint32_t uniq_all[kTpWarps][256];          // sorted halo list (padded to a power of 2)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint32_t* keys = keys_all[wib];
+  uint32_t* hk = hk_all[wib];
+  uint16_t* hv = hv_all[wib];
   uint32_t* uniq = uniq_all[wib];
   const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
   for (uint32_t t = blockIdx.x * kTpWarps + wib; t < ntiles; t += gridDim.x * kTpWarps) {
@@ -72,67 +76,80 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
     bool slow = lcnt > kTpColCap;
     uint32_t H = 0;
     if (!slow) {
-      // out-of-tile columns of the LD rows
-      uint32_t cnt = 0;
+      // out-of-tile references; more than half the set's slots -> slow tile
+      uint32_t outs = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (!hd[i])
+          for (uint32_t k = 0; k < d[i]; ++k) outs += col[b[i] + k] - row0 >= kTpRows;
+      slow = __reduce_add_sync(0xffffffffu, outs) > kHashSlots / 2;
+    }
+    if (!slow) {
+#pragma unroll
+      for (uint32_t i = lane; i < kHashSlots; i += 32) hk[i] = kEmpty;
+      __syncwarp();
+      // in-tile neighbours get their slot now; out-of-tile columns go into the set
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint32_t dl = hd[i] ? 0u : d[i];
-        const uint32_t dmax = __reduce_max_sync(0xffffffffu, dl);
-        for (uint32_t k = 0; k < dmax; ++k) {
-          const uint32_t c = k < dl ? col[b[i] + k] : row0;
-          const bool out = k < dl && c - row0 >= kTpRows;
-          const uint32_t m = __ballot_sync(0xffffffffu, out);
-          if (out) keys[cnt + __popc(m & ((1u << lane) - 1u))] = c;
-          cnt += __popc(m);
+        if (hd[i]) continue;
+        for (uint32_t k = 0; k < d[i]; ++k) {
+          const uint32_t c = col[b[i] + k];
+          if (c - row0 < kTpRows) lcol[b[i] + k] = static_cast<uint16_t>(c - row0);
+          else hash_insert(hk, c);
         }
       }
-      uint32_t P = 32;
-      while (P < cnt) P <<= 1;
-      for (uint32_t i = cnt + lane; i < P; i += 32) keys[i] = 0xFFFFFFFFu;
       __syncwarp();
-      for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-          for (uint32_t x = lane; x < P / 2; x += 32) {
-            const uint32_t i = 2 * jj * (x / jj) + (x % jj), p = i + jj;
-            const uint32_t u = keys[i], v = keys[p];
-            if ((u > v) == ((i & k) == 0)) {
-              keys[i] = v;
-              keys[p] = u;
-            }
-          }
-          __syncwarp();
-        }
-      // unique: lane owns keys [lane*per, lane*per + per)
-      const uint32_t per = (cnt + 31) / 32;
-      const uint32_t i0 = min(lane * per, cnt), i1 = min(i0 + per, cnt);
-      uint32_t u = 0;
-      for (uint32_t i = i0; i < i1; ++i) u += (i == 0 || keys[i] != keys[i - 1]);
-      uint32_t pos = warp_excl_scan(u, lane, H);
+      // compact the set (slot order), then sort it: the halo list
+#pragma unroll
+      for (uint32_t i0 = 0; i0 < kHashSlots; i0 += 32) {
+        const uint32_t c = hk[i0 + lane];
+        const uint32_t m = __ballot_sync(0xffffffffu, c != kEmpty);
+        const uint32_t at = H + __popc(m & ((1u << lane) - 1u));
+        if (c != kEmpty && at < kTpHaloCap) uniq[at] = c;
+        H += __popc(m);
+      }
       slow = H > halo_cap;
-      if (!slow)
-        for (uint32_t i = i0; i < i1; ++i)
-          if (i == 0 || keys[i] != keys[i - 1]) uniq[pos++] = keys[i];
-      __syncwarp();
+      if (!slow) {
+        uint32_t P = 32;
+        while (P < H) P <<= 1;
+        for (uint32_t i = H + lane; i < P; i += 32) uniq[i] = kEmpty;
+        __syncwarp();
+        for (uint32_t k = 2; k <= P; k <<= 1)
+          for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t x = lane; x < P / 2; x += 32) {
+              const uint32_t i = ((x & ~(jj - 1u)) << 1) | (x & (jj - 1u)), q = i + jj;  // jj is a power of 2
+              const uint32_t u = uniq[i], v = uniq[q];
+              if ((u > v) == ((i & k) == 0)) {
+                uniq[i] = v;
+                uniq[q] = u;
+              }
+            }
+            __syncwarp();
+          }
+        for (uint32_t i = lane; i < H; i += 32) hv[hash_find(hk, uniq[i])] = static_cast<uint16_t>(i);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (hd[i]) continue;
+          for (uint32_t k = 0; k < d[i]; ++k) {
+            const uint32_t c = col[b[i] + k];
+            if (c - row0 >= kTpRows) lcol[b[i] + k] = static_cast<uint16_t>(kTpRows + hv[hash_find(hk, c)]);
+          }
+        }
+      }
     }
     if (lane == 0) {
       meta[t] = TileMeta{loff, t * kTpHaloCap, slow ? 0u : lcnt, slow ? kTpSlow : H};
       if (slow) atomicAdd(slow_count, 1u);
     }
-    if (slow) continue;
-    uint16_t* lr = lrp + static_cast<size_t>(t) * kTpLrp;
+    if (!slow) {
+      uint16_t* lr = lrp + static_cast<size_t>(t) * kTpLrp;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) lr[32 * i + lane] = static_cast<uint16_t>((b[i] - loff) | (hd[i] ? kTpHdBit : 0u));
-    if (lane < kTpLrp - kTpRows) lr[kTpRows + lane] = static_cast<uint16_t>(end - loff);
-    for (uint32_t i = lane; i < ((H + 3u) & ~3u); i += 32) halo[t * kTpHaloCap + i] = uniq[min(i, H - 1)];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (hd[i]) continue;
-      for (uint32_t k = 0; k < d[i]; ++k) {
-        const uint32_t c = col[b[i] + k];
-        const uint32_t loc = (c - row0 < kTpRows) ? c - row0 : kTpRows + lower_bound_u32(uniq, H, c);
-        lcol[b[i] + k] = static_cast<uint16_t>(loc);
-      }
+      for (int i = 0; i < 4; ++i) lr[32 * i + lane] = static_cast<uint16_t>((b[i] - loff) | (hd[i] ? kTpHdBit : 0u));
+      if (lane < kTpLrp - kTpRows) lr[kTpRows + lane] = static_cast<uint16_t>(end - loff);
+      for (uint32_t i = lane; i < ((H + 3u) & ~3u); i += 32) halo[t * kTpHaloCap + i] = uniq[min(i, H - 1)];
     }
+    __syncwarp();
   }
 }
 
@@ -160,7 +177,7 @@ void build_tile_plan(groot_graph* g, uint32_t thr) {
   g->tp_halo.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
   DevBuf<uint32_t> slow(1);
   slow.zero();
-  const unsigned grid = std::min<uint32_t>((ntiles + kTpWarps - 1) / kTpWarps, static_cast<uint32_t>(num_sms()) * 8u);
+  const unsigned grid = std::min<uint32_t>((ntiles + kTpWarps - 1) / kTpWarps, static_cast<uint32_t>(num_sms()) * 16u);
   GROOT_LAUNCH(tile_plan_kernel, grid, kTpWarps * 32, 0, n, g->rp.p, g->col.p, thr, cap,
                reinterpret_cast<TileMeta*>(g->tp_meta.p), g->tp_lrp.p, g->tp_lcol.p, g->tp_halo.p, slow.p);
   slow.download(&g->tp_slow, 1);

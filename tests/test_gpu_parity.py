@@ -411,3 +411,36 @@ def test_shard_device_compute(api, golden_dir):
     oparts = O.regrow(hg, O.topo_chunks(hg.n, k), k)
     opred2, _, _ = O.predict(hg, oparts, prm)
     np.testing.assert_array_equal(pred, opred2)
+
+
+@pytest.mark.parametrize("cap", ["0", "64"])
+def test_forward_slow_tiles(api, golden_dir, cap):
+    """Tile-plan fallback: with the halo capacity forced down (GROOT_TP_HALO_CAP),
+    every tile (cap 0) or the wide-halo tiles (cap 64) gather straight from
+    the global CSR; logits and SpMM must still match the oracle."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+from paper_2511_18297_b200 import api
+from oracle import pyoracle as O
+c = api.gen_csa_multiplier(64); g = api.batch(api.encode(c.aig, c.labels), 2)
+h = O.batch(O.encode(O.gen_csa(64)), 2)
+prm = O.init_model(7)
+lg = api.forward(api.Model.from_params(prm), g)
+ref = O.forward(h, prm)
+err = (np.abs(lg - ref).max(1) / np.maximum(np.abs(ref).max(1), 1e-6)).max()
+assert err <= 1e-5, err
+x = np.random.default_rng(3).uniform(-1, 1, (h.n, 32)).astype(np.float32)
+out = api.spmm_mean(g, x)
+deg = np.diff(h.row_ptr).astype(np.int64)
+rows = np.repeat(np.arange(h.n), deg)
+s = np.zeros((h.n, 32)); np.add.at(s, rows, x[h.col_idx].astype(np.float64))
+ref2 = s / np.maximum(deg, 1)[:, None]
+assert np.abs(out - ref2).max() <= 1e-5 * max(1.0, np.abs(ref2).max())
+print("ok", err)
+"""
+    env = dict(os.environ, GROOT_TP_HALO_CAP=cap)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
