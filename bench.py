@@ -295,7 +295,7 @@ def run_ours(args):
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sage_layer_tc_kernel<false> (fused 32->32 SAGE layer)",
+                "traffic": traffic, "kernel": "sage_tile_kernel<kModeLayer> (tile-planned fused 32->32 SAGE layer)",
                 "algorithmic_bytes_per_launch": bytes_tc, "peak_source": peak_src}
     full_bytes = 114386760032 * (E / 268107776) if args.width == 1024 else None
 

@@ -17,6 +17,14 @@ UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def short_name(k):
+    if "sage_tile_kernel" in k:  # template modes: 0 layer, 1 last layer, 2 standalone SpMM
+        if "<1>" in k or "ILi1E" in k:
+            return "sage_layer_tc_last"
+        if "<2>" in k or "ILi2E" in k:
+            return "spmm_mean32"
+        return "sage_layer_tc"
+    if "tile_plan_kernel" in k:
+        return "tile_plan"
     if "sage_layer_tc_kernel" in k:
         return "sage_layer_tc_last" if ("(bool)1" in k or "<true>" in k or "<1>" in k) else "sage_layer_tc"
     for key in ("sage_layer0", "hd_mean_feat", "hd_mean32", "confusion", "spmm_mean32", "spmm_generic", "naive_layer"):
