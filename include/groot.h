@@ -73,6 +73,12 @@ int groot_csa_sizes(uint32_t width, uint32_t* num_inputs, uint32_t* num_ands,
                     uint32_t* num_outputs);
 int groot_gen_csa(uint32_t width, uint32_t* and_lits /*2*num_ands*/, uint32_t* out_lits,
                   uint8_t* labels);
+/* Radix-4 Booth multiplier AIG (BASELINE config 3; no reference generator
+ * exists): unsigned width x width -> 2*width product bits,
+ * same input/output conventions and label classes as groot_gen_csa; encoder
+ * and selector gates labelled AND, adder roots XOR / MAJ. Constants folded. */
+int groot_booth_sizes(uint32_t width, uint32_t* num_inputs, uint32_t* num_ands, uint32_t* num_outputs);
+int groot_gen_booth(uint32_t width, uint32_t* and_lits /*2*num_ands*/, uint32_t* out_lits, uint8_t* labels);
 /* parse_aiger (src/aig.cpp:47-88), ASCII "aag" text, same validation and error
  * texts. Sizes via *_sizes, then groot_aiger_fill. */
 int groot_aiger_sizes(const char* text, size_t len, uint32_t* num_inputs, uint32_t* num_ands,

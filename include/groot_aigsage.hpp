@@ -154,6 +154,21 @@ struct CsaCircuit {
   std::uint32_t full_adders = 0;
 };
 
+// Radix-4 Booth multiplier (BASELINE config 3; not in the reference):
+// same conventions as gen_csa_multiplier; adder counts are not tracked (0).
+inline CsaCircuit gen_booth_multiplier(std::uint32_t width) {
+  std::uint32_t ni, na, no;
+  detail::check(groot_booth_sizes(width, &ni, &na, &no));
+  std::vector<std::uint32_t> ands(2ull * na), outs(no);
+  CsaCircuit c;
+  c.width = width;
+  c.gt.labels.resize(1ull + ni + na + no);
+  detail::check(groot_gen_booth(width, ands.data(), outs.data(), c.gt.labels.data()));
+  c.aig = Aig::from_lits(ni, ands, outs);
+  for (std::uint32_t k = 0; k < no; ++k) c.gt.po_nodes.push_back(c.aig.num_nodes() + k);
+  return c;
+}
+
 // gen_csa_multiplier (src/circuitgen.cpp:66-133): bit-identical AIG and labels.
 inline CsaCircuit gen_csa_multiplier(std::uint32_t width) {
   std::uint32_t ni, na, no;

@@ -52,6 +52,7 @@ def _declare(L):
         "ref_default_workers": (C.c_uint, []),
         "ref_gen_csa": (P, [u32]),
         "ref_parse_aiger": (P, [C.c_char_p]),
+        "ref_aig_from_lits": (P, [u32, u32, P, u32, P]),
         "ref_aig_sizes": (None, [P, P, P, P]),
         "ref_aig_copy": (None, [P, P, P, P]),
         "ref_aig_free": (None, [P]),
@@ -144,6 +145,19 @@ def gen_csa(width: int):
 
 def parse_aiger(text: str):
     h = _need(lib().ref_parse_aiger(text.encode()))
+    try:
+        aig = _aig_from_handle(h)
+        g = RefGraph(lib().ref_encode(h))
+    finally:
+        lib().ref_aig_free(h)
+    return aig, g
+
+
+def aig_from_lits(num_inputs: int, and_lits: np.ndarray, out_lits: np.ndarray):
+    """Aig built through the reference's Aig::add_and/add_output; returns (Aig, RefGraph of encode)."""
+    ands = np.ascontiguousarray(and_lits, np.uint32)
+    outs = np.ascontiguousarray(out_lits, np.uint32)
+    h = _need(lib().ref_aig_from_lits(num_inputs, ands.shape[0], ptr(ands), outs.shape[0], ptr(outs)))
     try:
         aig = _aig_from_handle(h)
         g = RefGraph(lib().ref_encode(h))

@@ -83,6 +83,23 @@ ref_aig* ref_parse_aiger(const char* text) {
   });
   return out;
 }
+// Aig from literal arrays through the reference's own Aig::add_and / add_output
+// (src/aig.cpp:10-22) — no text parsing; labels as in ref_parse_aiger.
+ref_aig* ref_aig_from_lits(uint32_t ni, uint32_t na, const uint32_t* ands, uint32_t no, const uint32_t* outs) {
+  ref_aig* out = nullptr;
+  guarded([&] {
+    Aig a(ni);
+    for (uint32_t k = 0; k < na; ++k)
+      a.add_and(Literal{ands[2 * k] >> 1, (ands[2 * k] & 1) != 0}, Literal{ands[2 * k + 1] >> 1, (ands[2 * k + 1] & 1) != 0});
+    for (uint32_t k = 0; k < no; ++k) a.add_output(Literal{outs[k] >> 1, (outs[k] & 1) != 0});
+    GroundTruth gt;
+    gt.labels.assign(a.num_nodes() + a.outputs().size(), 3);
+    for (uint32_t i = 1; i <= a.num_inputs(); ++i) gt.labels[i] = 4;
+    for (size_t k = 0; k < a.outputs().size(); ++k) gt.labels[a.num_nodes() + k] = 0;
+    out = new ref_aig{std::move(a), std::move(gt)};
+  });
+  return out;
+}
 void ref_aig_sizes(const ref_aig* a, uint32_t* ni, uint32_t* na, uint32_t* no) {
   *ni = a->aig.num_inputs();
   *na = a->aig.num_ands();

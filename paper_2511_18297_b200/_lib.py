@@ -42,6 +42,8 @@ _SIG = {
     "groot_empty_cache": (i32, []),
     "groot_csa_sizes": (i32, [u32, P, P, P]),
     "groot_gen_csa": (i32, [u32, P, P, P]),
+    "groot_booth_sizes": (i32, [u32, P, P, P]),
+    "groot_gen_booth": (i32, [u32, P, P, P]),
     "groot_aiger_sizes": (i32, [C.c_char_p, C.c_size_t, P, P, P]),
     "groot_aiger_fill": (i32, [C.c_char_p, C.c_size_t, P, P]),
     "groot_encode": (i32, [u32, u32, P, u32, P, P, P]),

@@ -64,6 +64,19 @@ def gen_csa_multiplier(width: int) -> CsaCircuit:
     return CsaCircuit(Aig(ni.value, ands, outs), labels, width)
 
 
+def gen_booth_multiplier(width: int) -> CsaCircuit:
+    """Radix-4 Booth multiplier AIG (BASELINE config 3; the reference has no
+    Booth generator). Same conventions as gen_csa_multiplier:
+    PIs a = 1..w, b = w+1..2w, POs = the 2w product bits, labels PO/MAJ/XOR/AND/PI."""
+    ni, na, no = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib().groot_booth_sizes(width, C.byref(ni), C.byref(na), C.byref(no)))
+    ands = np.empty((na.value, 2), np.uint32)
+    outs = np.empty(no.value, np.uint32)
+    labels = np.empty(1 + ni.value + na.value + no.value, np.uint8)
+    check(lib().groot_gen_booth(width, ptr(ands), ptr(outs), ptr(labels)))
+    return CsaCircuit(Aig(ni.value, ands, outs), labels, width)
+
+
 def parse_aiger(text: str | bytes) -> Aig:
     """src/aig.cpp:47-88 (ASCII 'aag', latches rejected, same error texts)."""
     data = text.encode() if isinstance(text, str) else bytes(text)

@@ -160,6 +160,169 @@ void csa_counts(uint32_t w, uint32_t* na) {
 }
 
 // ---------------------------------------------------------------------------
+// Radix-4 Booth multiplier generator (BASELINE config 3; the reference has no
+// Booth generator, SPEC.md:18,163 — GROOT's paper evaluates Booth AIGs from ABC,
+// PAPER.md:297). Unsigned w x w -> 2w bits, inputs a = PIs 1..w, b = w+1..2w
+// (the CSA generator's order). Structure:
+//   * Booth encoder per digit i = 0..floor(w/2) over (b[2i+1], b[2i], b[2i-1])
+//     (b[-1] = b[w] = b[w+1] = 0): one = b[2i] ^ b[2i-1],
+//     two = b[2i+1] ? ~b[2i] & ~b[2i-1] : b[2i] & b[2i-1], neg = b[2i+1];
+//   * selector per partial-product bit j = 0..w: pp = ((a[j] & one) |
+//     (a[j-1] & two)) ^ neg;
+//   * row i contributes pp bits at columns 2i+j, its two's-complement +1 (neg)
+//     at column 2i and ~sign at column 2i+w+1; the sign extensions are folded
+//     into one constant, -sum_i 2^(2i+w+1) mod 2^(2w), added as constant-true
+//     bits (sign-extension prevention);
+//   * Wallace-style column compression (full adders on bit triples, half
+//     adders on a leftover pair when a column still holds more than two bits),
+//     then a ripple-carry adder over the final two rows.
+// Full/half adders are the reference's gen_full_adder / gen_half_adder (same
+// 7 / 3 AND gates, XOR and MAJ roots labelled as in src/circuitgen.cpp:44-64);
+// the encoder and selector logic is labelled AND. Node creation folds
+// constants (an AND with a constant input or with its own complement is not
+// materialised), so the AIG has no constant fanins.
+// ---------------------------------------------------------------------------
+struct Booth {
+  uint32_t w;
+  uint32_t inputs;
+  std::vector<uint32_t> ands;
+  std::vector<uint8_t> labels;
+  std::vector<uint32_t> outs;
+
+  explicit Booth(uint32_t width) : w(width), inputs(2 * width) {
+    labels.assign(1 + inputs, kAnd);
+    std::fill(labels.begin() + 1, labels.end(), kPi);
+  }
+  uint32_t node(uint32_t l, uint32_t r, uint8_t cls) {
+    if (l == 0 || r == 0 || l == (r ^ 1)) return 0;  // constant false
+    if (l == 1) return r;
+    if (r == 1 || l == r) return l;
+    const uint32_t v = 1 + inputs + static_cast<uint32_t>(ands.size() >> 1);
+    ands.push_back(l);
+    ands.push_back(r);
+    labels.push_back(cls);
+    return v << 1;
+  }
+  uint32_t or2(uint32_t x, uint32_t y) { return node(x ^ 1, y ^ 1, kAnd) ^ 1; }
+  uint32_t xor2(uint32_t x, uint32_t y) {
+    const uint32_t c = node(x, y, kAnd), n = node(x ^ 1, y ^ 1, kAnd);
+    return node(c ^ 1, n ^ 1, kAnd);
+  }
+  uint32_t a(int64_t j) const { return (j < 0 || j >= static_cast<int64_t>(w)) ? 0u : 2u * static_cast<uint32_t>(j + 1); }
+  uint32_t b(int64_t j) const { return (j < 0 || j >= static_cast<int64_t>(w)) ? 0u : 2u * static_cast<uint32_t>(w + j + 1); }
+  // gen_half_adder / gen_full_adder (src/circuitgen.cpp:44-64)
+  void half(uint32_t x, uint32_t y, uint32_t* s, uint32_t* c) {
+    *c = node(x, y, kMaj);
+    const uint32_t nr = node(x ^ 1, y ^ 1, kAnd);
+    *s = node(*c ^ 1, nr ^ 1, kXor);
+  }
+  void full(uint32_t x, uint32_t y, uint32_t cin, uint32_t* s, uint32_t* c) {
+    const uint32_t c1 = node(x, y, kAnd);
+    const uint32_t n1 = node(x ^ 1, y ^ 1, kAnd);
+    const uint32_t x1 = node(c1 ^ 1, n1 ^ 1, kAnd);
+    const uint32_t c2 = node(x1, cin, kAnd);
+    const uint32_t n2 = node(x1 ^ 1, cin ^ 1, kAnd);
+    *s = node(c2 ^ 1, n2 ^ 1, kXor);
+    *c = node(c1 ^ 1, c2 ^ 1, kMaj) ^ 1;
+  }
+  void build() {
+    const uint32_t W = 2 * w;
+    std::vector<std::vector<uint32_t>> col(W);
+    auto put = [&](uint64_t c, uint32_t lit) {
+      if (c < W && lit != 0) col[c].push_back(lit);
+    };
+    const uint32_t digits = w / 2 + 1;
+    std::vector<uint64_t> konst(W, 0);  // -sum_i 2^(2i+w+1) mod 2^W, as bits
+    {
+      std::vector<uint32_t> acc(W + 1, 0);  // subtract each term from 0 in binary
+      for (uint32_t i = 0; i < digits; ++i) {
+        const uint64_t p = 2ull * i + w + 1;
+        if (p >= W) continue;
+        // acc -= 2^p  (mod 2^W): borrow propagation
+        uint64_t q = p;
+        while (q < W) {
+          if (acc[q]) { acc[q] = 0; break; }
+          acc[q] = 1;
+          ++q;
+        }
+      }
+      for (uint32_t c = 0; c < W; ++c) konst[c] = acc[c];
+    }
+    for (uint32_t i = 0; i < digits; ++i) {
+      const int64_t k = 2 * static_cast<int64_t>(i);
+      const uint32_t b0 = b(k - 1), b1 = b(k), b2 = b(k + 1);
+      const uint32_t one = xor2(b1, b0);
+      const uint32_t two = or2(node(b2, node(b1 ^ 1, b0 ^ 1, kAnd), kAnd), node(b2 ^ 1, node(b1, b0, kAnd), kAnd));
+      const uint32_t neg = b2;
+      for (uint32_t j = 0; j <= w; ++j) {
+        const uint32_t sel = or2(node(a(j), one, kAnd), node(a(static_cast<int64_t>(j) - 1), two, kAnd));
+        put(static_cast<uint64_t>(k) + j, xor2(sel, neg));
+      }
+      put(static_cast<uint64_t>(k), neg);
+      put(static_cast<uint64_t>(k) + w + 1, neg ^ 1);
+    }
+    for (uint32_t c = 0; c < W; ++c)
+      if (konst[c]) col[c].push_back(1);
+    // constant-true bits: fold pairs (1 + 1 = carry 1, sum 0) so at most one remains per column
+    for (uint32_t c = 0; c < W; ++c) {
+      uint32_t ones = 0;
+      std::vector<uint32_t> keep;
+      for (uint32_t l : col[c]) {
+        if (l == 1) ++ones;
+        else keep.push_back(l);
+      }
+      col[c] = keep;
+      if (ones & 1) col[c].push_back(1);
+      if (ones >> 1 && c + 1 < W)
+        for (uint32_t t = 0; t < (ones >> 1); ++t) col[c + 1].push_back(1);
+    }
+    // Wallace layers
+    while (true) {
+      bool done = true;
+      for (uint32_t c = 0; c < W; ++c) done &= col[c].size() <= 2;
+      if (done) break;
+      std::vector<std::vector<uint32_t>> nxt(W);
+      for (uint32_t c = 0; c < W; ++c) {
+        const std::vector<uint32_t>& v = col[c];
+        size_t i = 0;
+        for (; i + 3 <= v.size(); i += 3) {
+          uint32_t sm, cy;
+          full(v[i], v[i + 1], v[i + 2], &sm, &cy);
+          nxt[c].push_back(sm);
+          if (c + 1 < W) nxt[c + 1].push_back(cy);
+        }
+        const size_t left = v.size() - i;
+        if (left == 2 && v.size() > 3) {
+          uint32_t sm, cy;
+          half(v[i], v[i + 1], &sm, &cy);
+          nxt[c].push_back(sm);
+          if (c + 1 < W) nxt[c + 1].push_back(cy);
+        } else {
+          for (; i < v.size(); ++i) nxt[c].push_back(v[i]);
+        }
+      }
+      col.swap(nxt);
+    }
+    // ripple-carry adder over the last two rows
+    outs.assign(W, 0);
+    uint32_t carry = 0;
+    for (uint32_t c = 0; c < W; ++c) {
+      std::vector<uint32_t> v = col[c];
+      if (carry) v.push_back(carry);
+      carry = 0;
+      if (v.empty()) { outs[c] = 0; continue; }
+      if (v.size() == 1) { outs[c] = v[0]; continue; }
+      uint32_t sm, cy;
+      if (v.size() == 2) half(v[0], v[1], &sm, &cy);
+      else full(v[0], v[1], v[2], &sm, &cy);
+      outs[c] = sm;
+      carry = cy;
+    }
+    labels.insert(labels.end(), outs.size(), kPo);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // ASCII AIGER (src/aig.cpp:47-88) — same validation order and messages.
 // ---------------------------------------------------------------------------
 struct ParsedAig {
@@ -305,6 +468,29 @@ int groot_gen_csa(uint32_t width, uint32_t* and_lits, uint32_t* out_lits, uint8_
     if (and_lits) std::copy(c.ands.begin(), c.ands.end(), and_lits);
     if (out_lits) std::copy(c.outs.begin(), c.outs.end(), out_lits);
     if (labels) std::copy(c.labels.begin(), c.labels.end(), labels);
+  });
+}
+
+int groot_booth_sizes(uint32_t width, uint32_t* ni, uint32_t* na, uint32_t* no) {
+  return guarded([&] {
+    if (width < 2) fail(GROOT_EINVAL, "gen_booth_multiplier: width must be >= 2");
+    need(ni, "groot_booth_sizes");
+    Booth bt(width);
+    bt.build();
+    *ni = 2 * width;
+    *na = static_cast<uint32_t>(bt.ands.size() / 2);
+    *no = 2 * width;
+  });
+}
+
+int groot_gen_booth(uint32_t width, uint32_t* and_lits, uint32_t* out_lits, uint8_t* labels) {
+  return guarded([&] {
+    if (width < 2) fail(GROOT_EINVAL, "gen_booth_multiplier: width must be >= 2");
+    Booth bt(width);
+    bt.build();
+    if (and_lits) std::copy(bt.ands.begin(), bt.ands.end(), and_lits);
+    if (out_lits) std::copy(bt.outs.begin(), bt.outs.end(), out_lits);
+    if (labels) std::copy(bt.labels.begin(), bt.labels.end(), labels);
   });
 }
 

@@ -437,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         for (int h = 0; h < 2; ++h) {
           const uint32_t w0 = lr[li + 8 * h], w1 = lr[li + 8 * h + 1];
           lo[h] = w0 & 0x7FFFu;
-          d[h] = (w1 & 0x7FFFu) - lo[h];
           hd[h] = (w0 & kTpHdBit) != 0;
+          d[h] = hd[h] ? 0u : (w1 & 0x7FFFu) - lo[h];  // HD rows: mean from the HD kernel
         }
         // rows one after the other (4 neighbour rows in flight per row keeps
         // the producers inside 128 registers)

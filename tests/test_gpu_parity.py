@@ -444,3 +444,27 @@ print("ok", err)
     env = dict(os.environ, GROOT_TP_HALO_CAP=cap)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("width,copies", [(16, 1), (64, 4)])
+def test_booth_graph_parity(api, width, copies):
+    """BASELINE config 3 family (Booth AIGs): device encode/batch bit-exact vs the
+    oracle, topo regrow bit-exact, logits within tolerance, classes match."""
+    c = api.gen_booth_multiplier(width)
+    g = api.encode(c.aig, c.labels)
+    gb = api.batch(g, copies) if copies > 1 else g
+    h = O.encode(O.Aig(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits, c.labels))
+    hb = O.batch(h, copies) if copies > 1 else h
+    assert_graph_equal(gb, hb)
+    k = 3
+    parts = api.regrow(gb, api.partition_topo_chunks(gb, k))
+    oparts = O.regrow(hb, O.topo_chunks(hb.n, k), k)
+    for p in range(k):
+        np.testing.assert_array_equal(parts[p].edges, oparts[p].edges)
+        np.testing.assert_array_equal(parts[p].boundary_nodes, oparts[p].boundary_nodes)
+    prm = O.init_model(7)
+    ref = O.forward(hb, prm)
+    lg = api.forward(api.Model.from_params(prm), gb)
+    check_logits(lg, ref, f"booth{width} b{copies}")
+    pred = api.predict_full(api.Model.from_params(prm), gb)
+    check_classes(pred.labels, ref, "booth predict_full")
