@@ -7,7 +7,7 @@ pinned by what a multiplier must do and by the reference's own code downstream:
 * well-formed: the reference's own Aig::add_and / add_output accept it (fanins
   strictly below the node), its encode equals the oracle's, and our AIGER text
   round-trips through our parser;
-* deterministic: sha256 of the generated arrays pinned in tests/golden/digests.json.
+* deterministic: sha256 of the generated arrays pinned in tests/golden/booth_digests.json.
 Device-side parity (encode / batch / regrow / forward on Booth graphs) is in
 tests/test_gpu_parity.py.
 """
@@ -123,8 +123,8 @@ def test_booth_reference_aig_and_encode(api):
 
 
 def test_booth_digests(api, golden_dir):
-    with open(os.path.join(golden_dir, "digests.json")) as f:
-        dig = json.load(f).get("booth", {})
+    with open(os.path.join(golden_dir, "booth_digests.json")) as f:
+        dig = json.load(f)
     assert dig, "booth digests missing"
     for w, want in dig.items():
         c = api.gen_booth_multiplier(int(w))
