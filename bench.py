@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--width", type=int, default=1024)
+    p.add_argument("--circuit", choices=["csa", "booth"], default="csa",
+                   help="multiplier family (booth = BASELINE config 3's radix-4 Booth AIG)")
     p.add_argument("--batch", type=int, default=16, help="copies per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -130,7 +132,7 @@ class RefSample:
     predicted with the reference's partition-parallel predict (default_pool =
     all host threads). Edges counted = fwd_edges whose head node lies in the sample."""
 
-    def __init__(self, width: int):
+    def __init__(self, width: int, circuit: str = "csa"):
         from oracle import pyoracle as O
         from oracle import pyref as R
         self.R = R
@@ -143,7 +145,12 @@ class RefSample:
             self.k *= 2
         self.first = self.k // 8
         self.count = self.workers
-        _, self.g = R.gen_csa(width)
+        if circuit == "booth":  # the reference's own Aig + encode on our Booth AIG (no reference generator)
+            from paper_2511_18297_b200 import api
+            c = api.gen_booth_multiplier(width)
+            _, self.g = R.aig_from_lits(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits)
+        else:
+            _, self.g = R.gen_csa(width)
         part = R.topo_chunks(self.g, self.k)
         self.parts = R.RefParts(self.g, part, self.k, True)
         edges = self.g.to_host().fwd_edges
@@ -151,7 +158,7 @@ class RefSample:
         self.edges = int(((hp >= self.first) & (hp < self.first + self.count)).sum())
         self.params = O.load_model(MODEL_FILE)[0]
         self.desc = (f"{self.count} consecutive regrown topo parts (k={self.k}, parts {self.first}.."
-                     f"{self.first + self.count - 1}) of one {width}-bit CSA copy = {self.edges} edges; "
+                     f"{self.first + self.count - 1}) of one {width}-bit {circuit.upper()} copy = {self.edges} edges; "
                      f"reference predict (src/gnn.cpp:280) with aggregation by the compiled spmm::execute, "
                      f"dense h*W restated (Eigen absent)")
 
@@ -166,7 +173,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     try:
-        s = RefSample(args.width)
+        s = RefSample(args.width, args.circuit)
     except Exception as e:  # pragma: no cover
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU path not loadable: {e}"}))
         return
@@ -179,8 +186,8 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (deterministic CSA generator)",
-        "config": {"workload": f"{args.width}-bit CSA multiplier AIG, batch {args.batch} per GPU (sampled)",
+        "data": f"synthetic (deterministic {args.circuit.upper()} generator)",
+        "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {args.batch} per GPU (sampled)",
                    "width": args.width, "batch": args.batch, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": s.workers, "kind": s.kind, "sample": s.desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -208,7 +215,7 @@ def run_ours(args):
     L = lib()
 
     # ---- setup (untimed): AIG on host, encode + batch on device ----
-    circ = api.gen_csa_multiplier(args.width)
+    circ = (api.gen_booth_multiplier if args.circuit == "booth" else api.gen_csa_multiplier)(args.width)
     g1 = api.encode(circ.aig, circ.labels)
     g = api.batch(g1, args.batch) if args.batch > 1 else g1
     n, nnz, E = g.n, g.nnz, g.num_undirected_edges()
@@ -297,7 +304,7 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "sage_tile_kernel<kModeLayer> (tile-planned fused 32->32 SAGE layer)",
                 "algorithmic_bytes_per_launch": bytes_tc, "peak_source": peak_src}
-    full_bytes = 114386760032 * (E / 268107776) if args.width == 1024 else None
+    full_bytes = 114386760032 * (E / 268107776) if (args.width == 1024 and args.circuit == "csa") else None
 
     # standalone SpMM (mean aggregation, f=32): the metric's "SpMM HBM GB/s"
     dense = torch.randn(n, 32, device="cuda")
@@ -355,7 +362,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = RefSample(args.width)
+            s = RefSample(args.width, args.circuit)
             s.step()
             reps = 4
             tt = sum(s.step() for _ in range(reps))
@@ -371,8 +378,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate)",
-            "data": "synthetic (deterministic CSA multiplier generator; trained 8-bit ASG1 weights)",
-            "config": {"workload": f"{args.width}-bit CSA multiplier AIG, batch {args.batch} per GPU "
+            "data": f"synthetic (deterministic {args.circuit.upper()} multiplier generator; trained 8-bit ASG1 weights)",
+            "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {args.batch} per GPU "
                                    f"(4-layer GraphSAGE 4-32-32-32-32 + 32->5 head, predict_full)",
                        "width": args.width, "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                        "nodes_per_gpu": n, "edges_per_gpu": E, "nnz_per_gpu": nnz,
