@@ -191,6 +191,15 @@ int groot_predict_parts(const groot_model* m, const groot_graph* g, const groot_
  * confusion_dev u64[25] (NULL = skip; accumulated, caller zeroes). */
 int groot_predict_full_dev(const groot_model* m, const groot_graph* g, uint8_t* labels_dev,
                            float* logits_dev, uint64_t* confusion_dev);
+
+/* One layer of run_forward (src/gnn.cpp:37-52) on a resident graph, device
+ * buffers, enqueued on the library stream (the building block of the
+ * exact-halo multi-GPU mode, paper_2511_18297_b200/shard.py):
+ *   layer 0: node features -> hout (n x hidden);  0 < layer < depth-1: hin -> hout;
+ *   layer depth-1: hin -> head + first-max argmax -> labels_dev (u8[n]), logits_dev
+ *   (n x classes, may be NULL). Every row is computed from its own neighbour list. */
+int groot_layer_dev(const groot_model* m, const groot_graph* g, uint32_t layer, const float* hin_dev,
+                    float* hout_dev, uint8_t* labels_dev, float* logits_dev);
 /* End-to-end from AIG host arrays: encode -> batch -> predict_full, classes to
  * host (the drop-in for run_cell's encode/batch/predict chain). */
 int groot_classify_aig(const groot_model* m, uint32_t num_inputs, uint32_t num_ands,

@@ -82,6 +82,7 @@ _SIG = {
     "groot_predict_full": (i32, [P, P, P, P, P]),
     "groot_predict": (i32, [P, P, P, P, P, P]),
     "groot_predict_full_dev": (i32, [P, P, P, P, P]),
+    "groot_layer_dev": (i32, [P, P, u32, P, P, P, P]),
     "groot_predict_parts": (i32, [P, P, P, P, u32, P]),
     "groot_classify_aig": (i32, [P, u32, u32, P, u32, P, P, u32, P, P, P]),
     "groot_build_plan": (i32, [P, u32, u32, u32, P, P, P, P, P, P]),

@@ -483,6 +483,15 @@ def forward(model: Model, g: EdaGraph) -> np.ndarray:
     return out
 
 
+def layer_dev(model: Model, g: EdaGraph, layer: int, hin=None, hout=None, labels=None, logits=None):
+    """One layer of run_forward (src/gnn.cpp:37-52) on device tensors (torch),
+    enqueued on the library stream: layer 0 reads the node features; the last
+    layer writes labels (u8[n]) and optionally logits. See groot_layer_dev."""
+    def dp(t):
+        return None if t is None else C.c_void_p(t.data_ptr())
+    check(lib().groot_layer_dev(model.handle, g.handle, layer, dp(hin), dp(hout), dp(labels), dp(logits)))
+
+
 def forward_naive(model: Model, g: EdaGraph):
     """Differential-test path (thread-per-row kernels). Returns (logits, labels)."""
     c = model.info()["classes"]

@@ -55,6 +55,8 @@ groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<
                             const std::vector<uint32_t>*);
 void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
 void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
+void layer_device(const groot_model*, groot_graph*, uint32_t, const float*, float*, uint8_t*, float*);
+void layer_prepare(const groot_model*, groot_graph*);
 void forward_naive_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void spmm_mean_device(groot_graph*, const float*, uint32_t, float*);
 void spmm_csr_device(uint32_t, const uint32_t*, const uint32_t*, const float*, const float*, uint32_t, float*);
@@ -836,6 +838,22 @@ int groot_predict_full_dev(const groot_model* m, const groot_graph* g, uint8_t* 
     need(labels_dev, "groot_predict_full_dev");
     forward_device(m, const_cast<groot_graph*>(g), labels_dev, logits_dev,
                    reinterpret_cast<unsigned long long*>(confusion_dev));
+  });
+}
+
+int groot_layer_dev(const groot_model* m, const groot_graph* g, uint32_t layer, const float* hin_dev, float* hout_dev,
+                    uint8_t* labels_dev, float* logits_dev) {
+  return guarded([&] {
+    need(m, "groot_layer_dev");
+    need(g, "groot_layer_dev");
+    if (layer >= m->depth) fail(GROOT_EINVAL, "layer: index out of range");
+    const bool last = layer + 1 == m->depth;
+    if (layer > 0 && !hin_dev) fail(GROOT_EINVAL, "layer: input activations required for layer >= 1");
+    if ((!last || m->depth == 1) && !hout_dev) fail(GROOT_EINVAL, "layer: output activations required");
+    if (last && !labels_dev) fail(GROOT_EINVAL, "layer: class output required for the last layer");
+    groot_graph* gg = const_cast<groot_graph*>(g);
+    layer_prepare(m, gg);
+    layer_device(m, gg, layer, hin_dev, hout_dev, labels_dev, logits_dev);
   });
 }
 

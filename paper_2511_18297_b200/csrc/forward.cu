@@ -962,93 +962,115 @@ static void set_tc_smem() {
   done = true;
 }
 
-// Full forward + classify on a resident graph. cls: u8[n] device; logits:
-// f32[n*classes] device or null; confusion: u64[25] device or null.
-void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* logits, unsigned long long* confusion) {
+// Per-graph preparation shared by the whole forward and the layer API:
+// row classifier (HD band) and, for models with tensor-core layers, the tile plan.
+static void prepare_graph(const groot_model* m, groot_graph* g) {
   require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
-  if (g->n == 0) return;
   static const bool host_timing = std::getenv("GROOT_HOST_TIMING") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto h0 = now();
   set_tc_smem();
   classify_rows(g, hd_threshold());
   const auto h1 = now();
-  ensure_activations(g);
-  const auto h2 = now();
   if (m->depth > 1) build_tile_plan(g, g->hd_threshold);
-  const auto h3 = now();
+  const auto h2 = now();
   if (host_timing) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "[forward] classify %.2f ms, activations %.2f ms, tile plan %.2f ms (host)\n", ms(h0, h1),
-                 ms(h1, h2), ms(h2, h3));
+    std::fprintf(stderr, "[forward] classify %.2f ms, tile plan %.2f ms (host)\n", ms(h0, h1), ms(h1, h2));
   }
+}
+
+// One layer of run_forward (src/gnn.cpp:37-52) on a resident graph:
+//   l = 0            features (u8) -> hout (n x 32)
+//   0 < l < depth-1  hin (n x 32)  -> hout (n x 32)
+//   l = depth-1      hin -> head + first-max argmax: cls (u8[n]), logits (n x classes, optional)
+// (depth 1: layer 0 writes hout, then the head kernel). Rows are computed for
+// every row of g, each from its own neighbour list in g.
+void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float* hin, float* hout, uint8_t* cls,
+                  float* logits) {
   const uint32_t n = g->n;
+  if (n == 0) return;
   HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
   const unsigned sms = static_cast<unsigned>(num_sms());
-  // layer 0
-  if (g->num_hd) {
-    ProfScope ps("hd_mean_feat");
-    GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
-                 g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
-  }
-  Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), hd, g->act[0].p};
-  {
-    ProfScope ps("sage_layer0");
-    GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, kL0Threads, sms * 8), kL0Threads, 0, l0,
-                 *reinterpret_cast<const Layer0W*>(m->l0w));
+  if (l == 0) {
+    if (g->num_hd) {
+      ProfScope ps("hd_mean_feat");
+      GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
+                   g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
+    }
+    Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), hd, hout};
+    {
+      ProfScope ps("sage_layer0");
+      GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, kL0Threads, sms * 8), kL0Threads, 0, l0,
+                   *reinterpret_cast<const Layer0W*>(m->l0w));
+    }
+    if (m->depth == 1)
+      GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, hout, m->head.p, m->classes, cls, logits,
+                   g->labels.p, nullptr);
+    return;
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
-  for (uint32_t l = 1; l < m->depth; ++l) {
-    const float* hin = g->act[(l - 1) & 1].p;
-    float* hout = g->act[l & 1].p;
-    if (g->num_hd) {
-      ProfScope ps("hd_mean32");
-      GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
-                   g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
-    }
-    LayerArgs a = plan_args(g, hin, hd);
-    a.hout = hout;
-    a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
-    a.classes = m->classes;
-    a.cls = cls;
-    a.logits = logits;
-    const unsigned grid = std::min<uint32_t>(ntiles, sms);
-    const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
-    HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
-    std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
-    static const char* trace_path = std::getenv("GROOT_TRACE");
-    DevBuf<unsigned long long> trace;
-    if (trace_path && l == 1) {
-      trace.alloc(64 * 16);
-      trace.zero();
-      a.trace = trace.p;
-    }
-    if (l + 1 == m->depth) {
-      ProfScope ps("sage_layer_tc_last");
-      GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
-    } else {
-      ProfScope ps("sage_layer_tc");
-      GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
-    }
-    if (a.trace) {
-      std::vector<unsigned long long> h(64 * 16);
-      trace.download(h.data(), h.size());
-      stream_sync();
-      if (FILE* fp = std::fopen(trace_path, "w")) {
-        for (int i = 0; i < 64; ++i) {
-          for (int k = 0; k < 16; ++k) std::fprintf(fp, "%llu ", h[i * 16 + k]);
-          std::fprintf(fp, "\n");
-        }
-        std::fclose(fp);
+  if (g->num_hd) {
+    ProfScope ps("hd_mean32");
+    GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
+                 g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
+  }
+  LayerArgs a = plan_args(g, hin, hd);
+  a.hout = hout;
+  a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
+  a.classes = m->classes;
+  a.cls = cls;
+  a.logits = logits;
+  const unsigned grid = std::min<uint32_t>(ntiles, sms);
+  const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
+  HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
+  std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
+  static const char* trace_path = std::getenv("GROOT_TRACE");
+  DevBuf<unsigned long long> trace;
+  if (trace_path && l == 1) {
+    trace.alloc(64 * 16);
+    trace.zero();
+    a.trace = trace.p;
+  }
+  if (l + 1 == m->depth) {
+    ProfScope ps("sage_layer_tc_last");
+    GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+  } else {
+    ProfScope ps("sage_layer_tc");
+    GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+  }
+  if (a.trace) {
+    std::vector<unsigned long long> h(64 * 16);
+    trace.download(h.data(), h.size());
+    stream_sync();
+    if (FILE* fp = std::fopen(trace_path, "w")) {
+      for (int i = 0; i < 64; ++i) {
+        for (int k = 0; k < 16; ++k) std::fprintf(fp, "%llu ", h[i * 16 + k]);
+        std::fprintf(fp, "\n");
       }
+      std::fclose(fp);
     }
   }
-  if (m->depth == 1)
-    GROOT_LAUNCH(head_kernel, blocks_for(n, 256), 256, 0, n, g->act[0].p, m->head.p, m->classes, cls, logits,
-                 g->labels.p, nullptr);
+}
+
+void layer_prepare(const groot_model* m, groot_graph* g) {
+  if (g->n) prepare_graph(m, g);
+}
+
+// Full forward + classify on a resident graph. cls: u8[n] device; logits:
+// f32[n*classes] device or null; confusion: u64[25] device or null.
+void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* logits, unsigned long long* confusion) {
+  require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
+  if (g->n == 0) return;
+  prepare_graph(m, g);
+  ensure_activations(g);
+  for (uint32_t l = 0; l < m->depth; ++l)
+    layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, l + 1 < m->depth || m->depth == 1 ? g->act[l & 1].p : nullptr,
+                 cls, logits);
   if (confusion) {
     ProfScope ps("confusion");
-    GROOT_LAUNCH(confusion_kernel, blocks_for(n, 256, sms * 8), 256, 0, n, cls, g->labels.p, confusion);
+    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
+                 g->labels.p, confusion);
   }
 }
 

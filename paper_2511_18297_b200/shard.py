@@ -146,3 +146,107 @@ def device_parts_compute(model, graph, parts):
         ids = np.concatenate([parts[p].core_nodes for p in part_ids]) if part_ids else np.zeros(0, np.uint32)
         return ids, labels[ids]
     return compute
+
+
+# ---------------------------------------------------------------------------
+# Exact-halo mode X: whole-graph (predict_full) results for
+# partitions that straddle ranks. Rank r owns part r of a k = world partition
+# and forwards the materialized regrown part (cores first, then the 1-hop
+# boundary, src/partition.cpp:428-438 local ids). Every core row has its full
+# neighbour list there, so a layer is exact on core rows once the boundary
+# rows hold their owners' values of the previous layer: after each layer but
+# the last, every rank sends the core rows its peers have as boundary rows
+# (one all-to-all per layer; NCCL over NVLink on the box). Boundary rows'
+# own outputs are partial and are overwritten by the exchange. Contrast mode
+# R (predict_parts above, the reference's semantics): no exchange, boundary
+# rows keep their partial neighbourhoods through every layer.
+# ---------------------------------------------------------------------------
+@dataclass
+class HaloPlan:
+    """One rank's exchange plan. send[q]: local core indices rank q needs, in
+    ascending global order; recv[q]: local boundary indices that rank q's rows
+    fill, in the same order."""
+    rank: int
+    world: int
+    num_core: int
+    num_local: int
+    core_nodes: np.ndarray
+    send: list
+    recv: list
+
+    @property
+    def send_counts(self):
+        return [int(x.shape[0]) for x in self.send]
+
+    @property
+    def recv_counts(self):
+        return [int(x.shape[0]) for x in self.recv]
+
+
+def halo_plans(part_of: np.ndarray, cores: Sequence[np.ndarray], boundaries: Sequence[np.ndarray]) -> list:
+    """Exchange plans of all k ranks from the regrown parts (core_nodes and
+    boundary_nodes, both ascending global ids, as regrow returns them)."""
+    k = len(cores)
+    part_of = np.asarray(part_of)
+    plans = []
+    for r in range(k):
+        core_r = np.asarray(cores[r], np.int64)
+        bnd_r = np.asarray(boundaries[r], np.int64)
+        owner = part_of[bnd_r] if bnd_r.size else np.zeros(0, np.int64)
+        recv = [core_r.shape[0] + np.nonzero(owner == q)[0] for q in range(k)]
+        send = []
+        for q in range(k):
+            bq = np.asarray(boundaries[q], np.int64)
+            mine = bq[part_of[bq] == r] if bq.size else bq
+            send.append(np.searchsorted(core_r, mine))
+        plans.append(HaloPlan(r, k, core_r.shape[0], core_r.shape[0] + bnd_r.shape[0], core_r, send, recv))
+    for r in range(k):  # every row sent is a core row of its sender, in the receiver's order
+        for q in range(k):
+            assert plans[r].send[q].shape == plans[q].recv[r].shape
+    return plans
+
+
+def exchange_halo(h, plan: HaloPlan):
+    """All-to-all of the boundary rows of a (num_local x f) torch tensor, in place."""
+    import torch
+    dist = _dist()
+    f = h.shape[1]
+    dev = h.device
+    send_idx = torch.as_tensor(np.concatenate(plan.send) if plan.send else np.zeros(0, np.int64), device=dev)
+    recv_idx = torch.as_tensor(np.concatenate(plan.recv) if plan.recv else np.zeros(0, np.int64), device=dev)
+    out = torch.empty((int(recv_idx.shape[0]), f), dtype=h.dtype, device=dev)
+    inp = h.index_select(0, send_idx.long()).contiguous()
+    dist.all_to_all_single(out, inp, plan.recv_counts, plan.send_counts)
+    h.index_copy_(0, recv_idx.long(), out)
+    return h
+
+
+def predict_exact(plan: HaloPlan, depth: int, layer: Callable, exchange: Callable = exchange_halo):
+    """Mode-X forward of one rank: layer(l, h_in) -> h_out (num_local x hidden),
+    or for the last layer the (num_local x classes) logits; exchange after every
+    layer but the last. Returns the logits of the rank's core rows."""
+    h = None
+    for l in range(depth):
+        h = layer(l, h)
+        if l + 1 < depth:
+            h = exchange(h, plan)
+    return h[: plan.num_core]
+
+
+def device_layer_fn(model, local_graph, hidden: int = 32):
+    """layer(l, h) over the device path (groot_layer_dev) on a rank's local graph."""
+    import torch
+    from . import api
+    n = local_graph.n
+    info = model.info()
+
+    def layer(l, h):
+        if l + 1 < info["depth"]:
+            out = torch.empty((n, hidden), dtype=torch.float32, device="cuda")
+            api.layer_dev(model, local_graph, l, h, out, None, None)
+            return out
+        cls = torch.empty(n, dtype=torch.uint8, device="cuda")
+        logits = torch.empty((n, info["classes"]), dtype=torch.float32, device="cuda")
+        api.layer_dev(model, local_graph, l, h, None, cls, logits)
+        return logits
+    return layer

@@ -468,3 +468,39 @@ def test_booth_graph_parity(api, width, copies):
     check_logits(lg, ref, f"booth{width} b{copies}")
     pred = api.predict_full(api.Model.from_params(prm), gb)
     check_classes(pred.labels, ref, "booth predict_full")
+
+
+@pytest.mark.parametrize("circuit,width,k", [("csa", 32, 3), ("booth", 16, 4)])
+def test_exact_halo_mode_device(api, circuit, width, k):
+    """Mode X on the device (groot_layer_dev per rank-local regrown part) with a
+    loopback all-to-all between k logical ranks on one GPU: core-row logits
+    equal the whole-graph forward of the oracle (predict_full semantics)."""
+    import torch
+    from paper_2511_18297_b200 import shard
+    c = (api.gen_booth_multiplier if circuit == "booth" else api.gen_csa_multiplier)(width)
+    g = api.encode(c.aig, c.labels)
+    pa = api.partition_topo_chunks(g, k)
+    parts = api.regrow(g, pa)
+    plans = shard.halo_plans(pa.part_of, [parts[p].core_nodes for p in range(k)],
+                             [parts[p].boundary_nodes for p in range(k)])
+    prm = O.init_model(7)
+    model = api.Model.from_params(prm)
+    locs = [api.materialize(g, parts, r) for r in range(k)]
+    layers = [shard.device_layer_fn(model, locs[r]) for r in range(k)]
+    hs = [None] * k
+    for l in range(4):
+        hs = [layers[r](l, hs[r]) for r in range(k)]
+        if l < 3:
+            for r in range(k):
+                for q in range(k):
+                    if plans[r].send[q].size:
+                        src = torch.as_tensor(plans[r].send[q], device="cuda").long()
+                        dst = torch.as_tensor(plans[q].recv[r], device="cuda").long()
+                        hs[q].index_copy_(0, dst, hs[r].index_select(0, src))
+    torch.cuda.synchronize()
+    h = O.encode(O.Aig(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits, c.labels))
+    ref = O.forward(h, prm)
+    got = np.zeros_like(ref)
+    for r in range(k):
+        got[parts[r].core_nodes] = hs[r][: plans[r].num_core].cpu().numpy()
+    check_logits(got, ref, f"mode X {circuit}{width} k{k}")
