@@ -190,7 +190,7 @@ constexpr int kTkRowStages = 4;
 constexpr int kTkMetaStages = 8;
 constexpr int kTkMetaLead = kTkMetaStages - kTkRowStages;
 constexpr uint32_t kCopiersMma = 2;   // warps 14, 15
-constexpr uint32_t kCopiersSpmm = 7;  // warps 0-3, 12, 14, 15
+constexpr uint32_t kCopiersSpmm = 2;  // warps 14, 15 (7 copiers measured no faster)
 constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;
 constexpr uint32_t kTkLrpOff = 0;
 constexpr uint32_t kTkLcolOff = kTpLrp * 2u + 16u;
@@ -281,10 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   ptx::tc_fence_after();
   const uint32_t tmem_base = kMma ? *sTmem : 0u;
 
-  // halo copier warps: the two spare warps (and, in SpMM mode, the idle
-  // epilogue and MMA warps)
-  const int copier = kMma ? (warp > kLoadWarp ? warp - (kLoadWarp + 1) : -1)
-                          : (warp < kEpiWarps ? warp : warp == kMmaWarp ? kEpiWarps : warp > kLoadWarp ? warp - 9 : -1);
+  // halo copier warps: the two spare warps 14, 15
+  static_assert(kCopiersMma == 2 && kCopiersSpmm == 2, "copier warps are 14 and 15");
+  const int copier = warp > kLoadWarp ? warp - (kLoadWarp + 1) : -1;
   if (warp == kLoadWarp) {
     // ===== loader: plan records and tile rows (one lane) =====
     if (lane == 0) {
