@@ -57,6 +57,8 @@ void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const
 void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void layer_device(const groot_model*, groot_graph*, uint32_t, const float*, float*, uint8_t*, float*);
 void layer_prepare(const groot_model*, groot_graph*);
+groot_graph* batch_padded(const groot_graph*, uint32_t, uint32_t);
+bool replicate_forward_plan(groot_graph*, groot_graph*, uint32_t, uint32_t);
 void forward_naive_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void spmm_mean_device(groot_graph*, const float*, uint32_t, float*);
 void spmm_csr_device(uint32_t, const uint32_t*, const uint32_t*, const float*, const float*, uint32_t, float*);
@@ -926,12 +928,25 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
     try {
       if (host_timing) stream_sync();
       const auto t1 = now();
+      if (copies < 1) fail(GROOT_EINVAL, "batch: copy count must be >= 1");
+      // Batch copies on tile-aligned row strides (padding rows in between), so the
+      // row classifier and tile plan of one copy are replicated rather than
+      // rebuilt over the whole batch; the classes are read back per copy in the
+      // reference's numbering (node v of copy k = k*n1 + v).
+      const uint32_t n1 = g1->n;
+      uint32_t P = n1;
       if (copies > 1) {
-        g = batch(g1, copies);
+        const uint32_t Pa = (n1 + 127u) / 128u * 128u;
+        groot_graph* gp = batch_padded(g1, copies, Pa);
+        if (m->depth > 1 && replicate_forward_plan(g1, gp, copies, Pa)) {
+          g = gp;
+          P = Pa;
+        } else {
+          delete gp;
+          g = batch(g1, copies);
+        }
         delete g1;
         g1 = nullptr;
-      } else if (copies < 1) {
-        fail(GROOT_EINVAL, "batch: copy count must be >= 1");
       }
       if (host_timing) stream_sync();
       const auto t2 = now();
@@ -943,13 +958,16 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
       const auto t3 = now();
       uint64_t h[25];
       conf.download(reinterpret_cast<unsigned long long*>(h), 25);
-      if (labels_out) cls.download(labels_out, g->n);
+      if (labels_out)
+        for (uint32_t k = 0; k < copies; ++k)
+          GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls.p + static_cast<size_t>(k) * P, n1,
+                                     cudaMemcpyDeviceToHost, stream()));
       stream_sync();
       const auto t4 = now();
       if (host_timing)
         std::fprintf(stderr, "[classify_aig] encode %.2f ms, batch %.2f ms, forward %.2f ms, download %.2f ms\n",
                      ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
-      finish_confusion(h, g->n, confusion, accuracy);
+      finish_confusion(h, n1 * copies, confusion, accuracy);
     } catch (...) {
       delete g1;
       if (g != g1) delete g;

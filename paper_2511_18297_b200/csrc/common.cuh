@@ -132,6 +132,9 @@ void build_csr(uint32_t n, uint64_t ne, const uint32_t* d_edges, uint32_t* d_rp,
 // Exclusive prefix sum of u32 counts into u32 offsets (count+1 outputs).
 void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, uint64_t count);
 void exclusive_scan_u64(const uint64_t* d_in, uint64_t* d_out, uint64_t count);
+// dst[k*len + i] = src[i] + k*offset (graph_build.cu)
+__global__ void replicate_offset_kernel(uint64_t len, uint32_t copies, uint32_t offset, const uint32_t* src,
+                                        uint32_t* dst);
 
 }  // namespace groot
 

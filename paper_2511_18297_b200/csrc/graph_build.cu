@@ -512,6 +512,56 @@ groot_graph* batch(const groot_graph* g, uint32_t copies) {
   return o;
 }
 
+// Tile-aligned batch for the end-to-end pipeline (groot_classify_aig): copy k
+// occupies rows [k*P, k*P + n) with P = n rounded up to the 128-row tile, the
+// rows in between are isolated padding rows (degree 0, features 0, label 255,
+// never referenced). Node v of copy k is row k*P + v instead of k*n + v, so
+// every copy covers the same tiles as copy 0 and the tile plan and HD list of
+// one copy can be replicated (replicate_forward_plan) instead of rebuilt over
+// the whole batch. fwd_edges are not materialised (the forward does not read them).
+__global__ void batch_padded_rows_kernel(uint32_t n, uint32_t P, uint32_t copies, uint32_t nnz,
+                                         const uint32_t* __restrict__ rp, const uint32_t* __restrict__ feat,
+                                         const uint8_t* __restrict__ lab, uint32_t* __restrict__ orp,
+                                         uint32_t* __restrict__ ofeat, uint8_t* __restrict__ olab) {
+  const uint64_t total = (uint64_t)P * copies;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = static_cast<uint32_t>(i / P), v = static_cast<uint32_t>(i - (uint64_t)k * P);
+    const bool real = v < n;
+    orp[i] = k * nnz + (real ? rp[v] : nnz);
+    ofeat[i] = real ? feat[v] : 0u;
+    olab[i] = real ? lab[v] : 0xFFu;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) orp[total] = nnz * copies;
+}
+
+groot_graph* batch_padded(const groot_graph* g, uint32_t copies, uint32_t P) {
+  require(copies >= 1 && P >= g->n, "batch_padded: bad arguments");
+  const uint64_t n64 = static_cast<uint64_t>(P) * copies;
+  require(n64 < 0xFFFFFFFFull && g->nnz * copies < 0xFFFFFFFFull, "batch_padded: graph too large");
+  auto* o = new groot_graph;
+  try {
+    GROOT_CUDA(cudaGetDevice(&o->device));
+    o->n = static_cast<uint32_t>(n64);
+    o->nnz = g->nnz * copies;
+    o->ne = 0;
+    o->rp.alloc(n64 + 1);
+    o->col.alloc(o->nnz);
+    o->feat.alloc(4 * n64);
+    o->labels.alloc(n64);
+    GROOT_LAUNCH(batch_padded_rows_kernel, blocks_for(n64, 256), 256, 0, g->n, P, copies,
+                 static_cast<uint32_t>(g->nnz), g->rp.p, reinterpret_cast<const uint32_t*>(g->feat.p),
+                 g->labels.p, o->rp.p, reinterpret_cast<uint32_t*>(o->feat.p), o->labels.p);
+    if (g->nnz)
+      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->nnz * copies / 4 + 1, 256), 256, 0, g->nnz, copies, P,
+                   g->col.p, o->col.p);
+  } catch (...) {
+    delete o;
+    throw;
+  }
+  return o;
+}
+
 groot_graph* graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col,
                              const uint8_t* feat, const uint8_t* lab, uint64_t ne,
                              const uint32_t* edges) {

@@ -340,12 +340,18 @@ def test_predict_partitioned(api, golden_dir, width, copies, k):
                                       api.predict_full(model, g).labels)
 
 
-def test_classify_aig_end_to_end(api, golden_dir):
-    c = api.gen_csa_multiplier(32)
+@pytest.mark.parametrize("circuit,width,copies", [("csa", 32, 3), ("csa", 33, 2), ("csa", 64, 4), ("booth", 16, 3),
+                                                   ("csa", 8, 1)])
+def test_classify_aig_end_to_end(api, golden_dir, circuit, width, copies):
+    """groot_classify_aig (the e2e call): copies go on tile-aligned strides with a
+    replicated tile plan when nnz1 % 8 == 0 (else the plain batch); classes and
+    confusion come back in the reference's numbering either way."""
+    c = (api.gen_booth_multiplier if circuit == "booth" else api.gen_csa_multiplier)(width)
     prm = trained_params(golden_dir)
     model = api.Model.from_params(prm)
-    pred = api.classify_aig(model, c.aig, c.labels, copies=3)
-    h = ora_graph(32, 3)
+    pred = api.classify_aig(model, c.aig, c.labels, copies=copies)
+    h1 = O.encode(O.Aig(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits, c.labels))
+    h = O.batch(h1, copies) if copies > 1 else h1
     opred, oconf, oacc, _ = O.predict_full(h, prm)
     np.testing.assert_array_equal(pred.labels, opred)
     np.testing.assert_array_equal(pred.confusion, oconf)
