@@ -156,6 +156,7 @@ struct groot_graph {
   groot::DevBuf<float> act[2];      // n x 32 ping-pong activations
   // Per-tile gather plan of the fused layer / SpMM (tile_plan.cuh), built lazily.
   uint32_t tp_threshold = 0, tp_halo_cap = 0, tp_slow = 0;
+  uint32_t tp_period = 0, tp_period_rows = 0;  // > 0: periodic plan of one batch copy (see forward.cu)
   groot::DevBuf<uint32_t> tp_meta;  // TileMeta per tile (4 x u32)
   groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
   groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots

@@ -159,6 +159,8 @@ struct LayerArgs {
   const uint32_t* halo;
   float* spmm_out;       // SpMM mode: n x 32 neighbour means (LD rows)
   unsigned long long* trace;  // diagnostic timeline of CTA 0 (GROOT_TRACE): [64 tiles][16 clock64 stamps]
+  uint32_t plan_period;       // > 0: the plan is one copy's (tiles 0..period-1), tile t uses t % period
+  uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
 };
 
 // Timeline stamp of CTA 0 for tile iteration it (< 64), event slot k (< 16).
@@ -289,7 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     if (lane == 0) {
       constexpr int kQ = 4;  // TileMeta records prefetched into registers beyond the plan ring
       auto meta_of = [&](uint32_t tt) -> uint4 {
-        return tt < ntiles ? __ldg(reinterpret_cast<const uint4*>(a.tmeta) + tt) : make_uint4(0, 0, 0, 0);
+        const uint32_t pt = a.plan_period ? tt % a.plan_period : tt;
+        return tt < ntiles ? __ldg(reinterpret_cast<const uint4*>(a.tmeta) + pt) : make_uint4(0, 0, 0, 0);
       };
       auto issue_plan = [&](uint32_t i, uint32_t t, const uint4& m) {
         const uint32_t ms = i % kTkMetaStages;
@@ -299,7 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const bool slow = (m.w & kTpSlow) != 0;
         const uint32_t hpad = slow ? 0u : (m.w + 3u) & ~3u;
         ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u);
-        ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(t) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
+        const uint32_t pt = a.plan_period ? t % a.plan_period : t;
+        ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(pt) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
         if (m.z) ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
         if (hpad) ptx::bulk_load(sp + kTkHaloOff, a.halo + m.y, hpad * 4u, &m_full[ms]);
       };
@@ -340,6 +344,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       const uint32_t hc = sMeta[ms].w;
       if (gl == 0) tstamp(a.trace, it, 1);
       if (!(hc & kTpSlow)) {
+        const uint32_t shift = a.plan_period ? (t / a.plan_period) * a.period_rows : 0u;
+        const float* hin_c = a.hin + static_cast<size_t>(shift) * kF + 4 * c;
         const uint32_t* hl = reinterpret_cast<const uint32_t*>(sPlan + ms * kTkMetaBytes + kTkHaloOff);
         const uint32_t sbase = sRows_s + rs * kTkRowBytes + kTpRows * 128u + c * 16u;
         // 4 halo ids per batch read before the copies are issued (the asm
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t slot = b0 + u * kStride;
-            if (slot < hc) ptx::cp_async16(sbase + slot * 128u, a.hin + static_cast<size_t>(row[u]) * kF + 4 * c);
+            if (slot < hc) ptx::cp_async16(sbase + slot * 128u, hin_c + static_cast<size_t>(row[u]) * kF);
           }
         }
       }
@@ -918,6 +924,8 @@ static LayerArgs plan_args(const groot_graph* g, const float* hin, const HdInfo&
   a.lrp = g->tp_lrp.p;
   a.lcol = g->tp_lcol.p;
   a.halo = g->tp_halo.p;
+  a.plan_period = g->tp_period;
+  a.period_rows = g->tp_period_rows;
   return a;
 }
 

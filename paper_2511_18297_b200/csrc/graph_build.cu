@@ -5,6 +5,10 @@
 // scans use CUB (plumbing) where a general primitive is needed.
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <fstream>
 #include <string>
@@ -120,21 +124,24 @@ __device__ __forceinline__ void sort_row_regs(uint32_t* __restrict__ col, uint32
     if ((uint32_t)i < d) col[b + i] = a[i];
 }
 
-// Thread per row for rows of degree <= 16; longer rows are queued.
+// Thread per row for rows of degree <= 16; longer rows are queued: up to
+// kSmemSortMax for the shared-memory sort, beyond as (start, degree) pairs for
+// a per-row radix sort.
 __global__ void sort_small_rows_kernel(uint32_t n, const uint32_t* __restrict__ rp,
                                        uint32_t* __restrict__ col, uint32_t* big_rows,
-                                       uint32_t* big_count) {
+                                       uint32_t* big_count, uint2* huge_rows, uint32_t* huge_count) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const uint32_t b = rp[r], d = rp[r + 1] - b;
     if (d <= 1) continue;
     if (d <= 4) sort_row_regs<4>(col, b, d);
     else if (d <= 8) sort_row_regs<8>(col, b, d);
     else if (d <= 16) sort_row_regs<16>(col, b, d);
-    else big_rows[atomicAdd(big_count, 1u)] = r;
+    else if (d <= 4096) big_rows[atomicAdd(big_count, 1u)] = r;
+    else huge_rows[atomicAdd(huge_count, 1u)] = make_uint2(b, d);
   }
 }
 
-constexpr int kSmemSortMax = 4096;
+constexpr int kSmemSortMax = 4096;  // == the sort_small_rows_kernel split
 
 // CTA per row: shared-memory bitonic sort of rows with 16 < degree <= 4096.
 __global__ void __launch_bounds__(512) sort_mid_rows_kernel(const uint32_t* __restrict__ rows,
@@ -178,23 +185,25 @@ void build_csr(uint32_t n, uint64_t ne, const uint32_t* d_edges, uint32_t* d_rp,
   GROOT_CUDA(cudaMemcpyAsync(cnt.p, d_rp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream()));
   GROOT_LAUNCH(scatter_kernel, blocks_for(ne, 256), 256, 0, ne, e, cnt.p, d_col);
   DevBuf<uint32_t> big(static_cast<size_t>(n));
-  DevBuf<uint32_t> nbig(1);
-  nbig.zero();
-  GROOT_LAUNCH(sort_small_rows_kernel, blocks_for(n, 256), 256, 0, n, d_rp, d_col, big.p, nbig.p);
-  const uint32_t nb = read_scalar(nbig.p);
-  if (nb == 0) return;
-  GROOT_LAUNCH(sort_mid_rows_kernel, std::min<uint32_t>(nb, 148 * 8), 512, 0, big.p, nb, d_rp, d_col);
+  DevBuf<uint2> huge(static_cast<size_t>(n));
+  DevBuf<uint32_t> counts(2);
+  counts.zero();
+  GROOT_LAUNCH(sort_small_rows_kernel, blocks_for(n, 256), 256, 0, n, d_rp, d_col, big.p, counts.p, huge.p,
+               counts.p + 1);
+  uint32_t cnt2[2];
+  counts.download(cnt2, 2);
+  stream_sync();
+  const uint32_t nb = cnt2[0], nh = cnt2[1];
+  if (nb) GROOT_LAUNCH(sort_mid_rows_kernel, std::min<uint32_t>(nb, 148 * 8), 512, 0, big.p, nb, d_rp, d_col);
+  if (nh == 0) return;
   // Rows longer than the shared-memory sort: per-row radix sort (rare; wide fanout).
-  std::vector<uint32_t> rows(nb);
-  big.download(rows.data(), nb);
-  std::vector<uint32_t> rph(n + 1);
-  GROOT_CUDA(cudaMemcpyAsync(rph.data(), d_rp, sizeof(uint32_t) * (n + 1), cudaMemcpyDeviceToHost, stream()));
+  std::vector<uint2> rows(nh);
+  huge.download(rows.data(), nh);
   stream_sync();
   DevBuf<uint32_t> tmp;
   DevBuf<uint8_t> work;
-  for (uint32_t r : rows) {
-    const uint32_t b = rph[r], d = rph[r + 1] - b;
-    if (d <= static_cast<uint32_t>(kSmemSortMax)) continue;
+  for (const uint2& bd : rows) {
+    const uint32_t b = bd.x, d = bd.y;
     if (tmp.n < d) tmp.alloc(d);
     size_t bytes = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_col + b, tmp.p, d, 0, 32, stream());
@@ -463,6 +472,10 @@ groot_graph* encode(uint32_t ni, uint32_t na, const uint32_t* h_ands, uint32_t n
   require(n64 < 0xFFFFFFFFull, "encode: node count exceeds 2^32-1");
   const uint32_t n = static_cast<uint32_t>(n64);
   const uint64_t ne = 2ull * na + no;
+  static const bool host_timing = std::getenv("GROOT_HOST_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   groot_graph* g = graph_alloc(n, ne);
   try {
     DevBuf<uint32_t> ands(2ull * na), outs(no), bad(1);
@@ -471,12 +484,18 @@ groot_graph* encode(uint32_t ni, uint32_t na, const uint32_t* h_ands, uint32_t n
     const uint32_t none = 0xFFFFFFFFu;
     bad.upload(&none, 1);
     if (h_labels) g->labels.upload(h_labels, n); else g->labels.zero();
+    if (host_timing) stream_sync();
+    const auto t1 = now();
     GROOT_LAUNCH(encode_kernel, blocks_for(n, 256), 256, 0, ni, na, ands.p, no, outs.p,
                  reinterpret_cast<uint32_t*>(g->feat.p), reinterpret_cast<uint2*>(g->edges.p), bad.p);
     const uint32_t b = read_scalar(bad.p);
     if (b != none) fail(GROOT_EINVAL, "Aig::add_and: fanin index must be strictly below the new node");
+    const auto t2 = now();
     build_csr(n, ne, g->edges.p, g->rp.p, g->col.p);
     stream_sync();
+    if (host_timing)
+      std::fprintf(stderr, "[encode] upload %.2f ms, encode %.2f ms, csr %.2f ms\n", ms(t0, t1), ms(t1, t2),
+                   ms(t2, now()));
   } catch (...) {
     delete g;
     throw;

@@ -155,36 +155,6 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
 
 }  // namespace
 
-// Replication of one copy's plan onto a tile-aligned batch (batch_padded):
-// tile k*T + t of the batch is tile t of copy 0 with its lcol segment moved by
-// k*nnz and its halo rows by k*P; lrp and the u16 slots are identical.
-__global__ void replicate_plan_kernel(uint32_t T, uint32_t copies, uint32_t nnz1, uint32_t P,
-                                      const TileMeta* __restrict__ meta1, const uint32_t* __restrict__ halo1,
-                                      TileMeta* __restrict__ meta, uint32_t* __restrict__ halo) {
-  const uint64_t total = (uint64_t)T * copies * kTpHaloCap;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t tile = i / kTpHaloCap;
-    const uint32_t e = static_cast<uint32_t>(i - tile * kTpHaloCap);
-    const uint32_t k = static_cast<uint32_t>(tile / T), t = static_cast<uint32_t>(tile - (uint64_t)k * T);
-    halo[i] = halo1[(uint64_t)t * kTpHaloCap + e] + k * P;
-    if (e == 0) {
-      TileMeta m = meta1[t];
-      m.lcol_off += k * nnz1;
-      m.halo_off = static_cast<uint32_t>(tile) * kTpHaloCap;
-      meta[tile] = m;
-    }
-  }
-}
-
-__global__ void replicate_u16_kernel(uint64_t len, uint32_t copies, const uint16_t* __restrict__ src,
-                                     uint16_t* __restrict__ dst) {
-  const uint64_t total = len * copies;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = src[i % len];
-}
-
 uint32_t tile_halo_cap() {
   static uint32_t cap = [] {
     const char* e = std::getenv("GROOT_TP_HALO_CAP");  // test knob: force slow tiles
@@ -223,40 +193,36 @@ void classify_rows(groot_graph* g, uint32_t thr);
 uint32_t hd_threshold();
 
 // Give the tile-aligned batch `dst` (batch_padded(src, copies, P)) the row
-// classifier output and tile plan of `src`, replicated; false if the layout
-// does not allow it (the forward then builds them itself).
+// classifier output of `src` replicated and the tile plan of `src` as a
+// periodic plan: tile k*T + t of the batch reads plan tile t of copy 0 (same
+// row offsets and local slots, lcol segments inside copy 0's nonzeros) and
+// shifts its halo rows by k*P. False if the layout does not allow it (the
+// forward then builds its own plan).
 bool replicate_forward_plan(groot_graph* src, groot_graph* dst, uint32_t copies, uint32_t P) {
   const uint32_t T = (src->n + kTpRows - 1) / kTpRows;
-  if (src->n == 0 || P != T * kTpRows || (src->nnz & 7u) != 0) return false;
+  if (src->n == 0 || P != T * kTpRows) return false;
   const uint32_t thr = hd_threshold();
   classify_rows(src, thr);
   build_tile_plan(src, thr);
-  ProfScope ps("replicate_plan");
-  const unsigned sms = static_cast<unsigned>(num_sms());
+  // (slow tiles need nothing per copy: they gather from the batch's own CSR)
   // row classifier: HD rows of copy 0, shifted per copy (stays ascending)
   dst->num_hd = src->num_hd * copies;
   dst->hd_rows.alloc(dst->num_hd);
   if (dst->num_hd)
-    GROOT_LAUNCH(replicate_offset_kernel, blocks_for(dst->num_hd / 4 + 1, 256, sms * 8), 256, 0,
+    GROOT_LAUNCH(replicate_offset_kernel, blocks_for(dst->num_hd / 4 + 1, 256), 256, 0,
                  static_cast<uint64_t>(src->num_hd), copies, P, src->hd_rows.p, dst->hd_rows.p);
   dst->hd_mean.alloc(static_cast<size_t>(dst->num_hd) * 32);
   dst->hd_threshold = thr;
-  // tile plan
-  const uint64_t tiles = static_cast<uint64_t>(T) * copies;
-  dst->tp_meta.alloc(4 * tiles);
-  dst->tp_lrp.alloc(tiles * kTpLrp);
-  dst->tp_lcol.alloc(dst->nnz + 16ull);
-  dst->tp_halo.alloc(tiles * kTpHaloCap);
-  GROOT_LAUNCH(replicate_plan_kernel, blocks_for(tiles * kTpHaloCap, 256, sms * 16), 256, 0, T, copies,
-               static_cast<uint32_t>(src->nnz), P, reinterpret_cast<const TileMeta*>(src->tp_meta.p),
-               src->tp_halo.p, reinterpret_cast<TileMeta*>(dst->tp_meta.p), dst->tp_halo.p);
-  GROOT_LAUNCH(replicate_u16_kernel, blocks_for(tiles * kTpLrp, 256, sms * 16), 256, 0,
-               static_cast<uint64_t>(T) * kTpLrp, copies, src->tp_lrp.p, dst->tp_lrp.p);
-  GROOT_LAUNCH(replicate_u16_kernel, blocks_for(dst->nnz, 256, sms * 16), 256, 0, src->nnz, copies, src->tp_lcol.p,
-               dst->tp_lcol.p);
+  dst->tp_meta = std::move(src->tp_meta);
+  dst->tp_lrp = std::move(src->tp_lrp);
+  dst->tp_lcol = std::move(src->tp_lcol);
+  dst->tp_halo = std::move(src->tp_halo);
   dst->tp_threshold = src->tp_threshold;
   dst->tp_halo_cap = src->tp_halo_cap;
   dst->tp_slow = src->tp_slow * copies;
+  dst->tp_period = T;
+  dst->tp_period_rows = P;
+  src->tp_threshold = 0;  // src no longer owns a plan
   return true;
 }
 }  // namespace groot
