@@ -157,6 +157,7 @@ struct groot_graph {
   // Per-tile gather plan of the fused layer / SpMM (tile_plan.cuh), built lazily.
   uint32_t tp_threshold = 0, tp_halo_cap = 0, tp_slow = 0;
   uint32_t tp_period = 0, tp_period_rows = 0;  // > 0: periodic plan of one batch copy (see forward.cu)
+  groot::DevBuf<uint32_t> tile_ctr;            // dynamic tile scheduler counter of the tile kernels
   groot::DevBuf<uint32_t> tp_meta;  // TileMeta per tile (4 x u32)
   groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
   groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots
