@@ -158,6 +158,11 @@ struct groot_graph {
   uint32_t tp_threshold = 0, tp_halo_cap = 0, tp_slow = 0;
   uint32_t tp_period = 0, tp_period_rows = 0;  // > 0: periodic plan of one batch copy (see forward.cu)
   groot::DevBuf<uint32_t> tile_ctr;            // dynamic tile scheduler counter of the tile kernels
+  // HD plan (forward.cu, hd_chunk_kernel): chunk units sorted by first neighbour
+  bool hdp_valid = false;
+  uint32_t hdp_nunits = 0;
+  groot::DevBuf<uint32_t> hdp_base, hdp_slot, hdp_k, hdp_units;
+  groot::DevBuf<float> hdp_partial;
   groot::DevBuf<uint32_t> tp_meta;  // TileMeta per tile (4 x u32)
   groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
   groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots

@@ -774,23 +774,39 @@ __global__ void __launch_bounds__(kL0Threads) sage_layer0_kernel(const Layer0Arg
 }
 
 // ---------------------------------------------------------------------------
-// HD rows: CTA per row, 32 groups of 8 lanes stride the neighbour list; fixed
-// order reduction over groups (deterministic). out row = slot (or row id).
+// HD rows, L2-ordered (hd_chunk_kernel + hd_reduce_kernel): each HD row's
+// neighbour list is cut into chunks of kHdChunk nonzeros, and the chunks of
+// all HD rows are processed in the order of their first neighbour's row id
+// (the per-graph HD plan, build_hd_plan). In a multiplier the PIs' neighbours
+// are the partial products: a_i's are one array row, b_j's one per array
+// row; ordered by position, the chunks that read the same partial-product
+// rows run together, so each is fetched from DRAM about once instead of twice.
+// A warp sums one chunk in nonzero order (4 row groups of 8 lanes, combined in
+// fixed order) into a partial row; hd_reduce_kernel adds a row's partials in
+// chunk order and scales by 1/deg: deterministic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) hd_mean32_kernel(const uint32_t* __restrict__ hd_rows, uint32_t count,
-                                                        const uint32_t* __restrict__ rp,
-                                                        const uint32_t* __restrict__ col,
-                                                        const float* __restrict__ H, float* __restrict__ out,
-                                                        int out_by_row) {
-  __shared__ float red[32][kF + 1];
-  const int gid = threadIdx.x >> 3, j = threadIdx.x & 7;
-  for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
-    const uint32_t r = hd_rows[slot], b = rp[r], d = rp[r + 1] - b;
+constexpr uint32_t kHdChunk = 64;
+
+__global__ void __launch_bounds__(256) hd_chunk_kernel(const uint32_t* __restrict__ units, uint32_t nunits,
+                                                       const uint32_t* __restrict__ unit_slot,
+                                                       const uint32_t* __restrict__ unit_k,
+                                                       const uint32_t* __restrict__ hd_rows,
+                                                       const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                                       const float* __restrict__ H, float* __restrict__ partial,
+                                                       const uint32_t* __restrict__ unit_base) {
+  const uint32_t lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nunits; w += warps) {
+    const uint32_t u = units[w];
+    const uint32_t slot = unit_slot[u], k = unit_k[u];
+    const uint32_t r = hd_rows[slot];
+    const uint32_t b = rp[r] + k * kHdChunk;
+    const uint32_t e = min(b + kHdChunk, rp[r + 1]);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t e = gid;
-    for (; e + 96 < d; e += 128) {
-      const uint32_t c0 = __ldg(col + b + e), c1 = __ldg(col + b + e + 32);
-      const uint32_t c2 = __ldg(col + b + e + 64), c3 = __ldg(col + b + e + 96);
+    // group g takes nonzeros b+g, b+g+4, ...; 4 rows in flight per group
+    uint32_t q = b + g;
+    for (; q + 12 < e; q += 16) {
+      const uint32_t c0 = __ldg(col + q), c1 = __ldg(col + q + 4), c2 = __ldg(col + q + 8), c3 = __ldg(col + q + 12);
       const float4 v0 = ptx::ldg_f4(H + static_cast<size_t>(c0) * kF + 4 * j);
       const float4 v1 = ptx::ldg_f4(H + static_cast<size_t>(c1) * kF + 4 * j);
       const float4 v2 = ptx::ldg_f4(H + static_cast<size_t>(c2) * kF + 4 * j);
@@ -798,19 +814,60 @@ __global__ void __launch_bounds__(256) hd_mean32_kernel(const uint32_t* __restri
       acc = f4add(f4add(acc, v0), v1);
       acc = f4add(f4add(acc, v2), v3);
     }
-    for (; e < d; e += 32) acc = f4add(acc, ptx::ldg_f4(H + static_cast<size_t>(__ldg(col + b + e)) * kF + 4 * j));
-    red[gid][4 * j] = acc.x;
-    red[gid][4 * j + 1] = acc.y;
-    red[gid][4 * j + 2] = acc.z;
-    red[gid][4 * j + 3] = acc.w;
-    __syncthreads();
-    if (threadIdx.x < kF) {
-      float s = 0.f;
-      for (int q = 0; q < 32; ++q) s += red[q][threadIdx.x];
-      const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
-      out[static_cast<size_t>(out_by_row ? r : slot) * kF + threadIdx.x] = s * inv;
+    for (; q < e; q += 4) acc = f4add(acc, ptx::ldg_f4(H + static_cast<size_t>(__ldg(col + q)) * kF + 4 * j));
+    // fixed-order combine of the 4 groups: lane j of group 0 adds groups 1..3
+    float4 o1, o2, o3;
+    o1.x = __shfl_down_sync(0xffffffffu, acc.x, 8); o1.y = __shfl_down_sync(0xffffffffu, acc.y, 8);
+    o1.z = __shfl_down_sync(0xffffffffu, acc.z, 8); o1.w = __shfl_down_sync(0xffffffffu, acc.w, 8);
+    o2.x = __shfl_down_sync(0xffffffffu, acc.x, 16); o2.y = __shfl_down_sync(0xffffffffu, acc.y, 16);
+    o2.z = __shfl_down_sync(0xffffffffu, acc.z, 16); o2.w = __shfl_down_sync(0xffffffffu, acc.w, 16);
+    o3.x = __shfl_down_sync(0xffffffffu, acc.x, 24); o3.y = __shfl_down_sync(0xffffffffu, acc.y, 24);
+    o3.z = __shfl_down_sync(0xffffffffu, acc.z, 24); o3.w = __shfl_down_sync(0xffffffffu, acc.w, 24);
+    if (g == 0) {
+      const float4 sum = f4add(f4add(f4add(acc, o1), o2), o3);
+      *reinterpret_cast<float4*>(partial + static_cast<size_t>(unit_base[slot] + k) * kF + 4 * j) = sum;
     }
-    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) hd_reduce_kernel(uint32_t count, const uint32_t* __restrict__ hd_rows,
+                                                        const uint32_t* __restrict__ rp,
+                                                        const uint32_t* __restrict__ unit_base,
+                                                        const float* __restrict__ partial, float* __restrict__ out,
+                                                        int out_by_row) {
+  // 8 lanes per HD row (float4 each)
+  const uint32_t groups = gridDim.x * (blockDim.x >> 3);
+  const uint32_t j = threadIdx.x & 7;
+  for (uint32_t slot = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); slot < count; slot += groups) {
+    const uint32_t r = hd_rows[slot], d = rp[r + 1] - rp[r];
+    const uint32_t u0 = unit_base[slot], u1 = unit_base[slot + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t u = u0; u < u1; ++u) acc = f4add(acc, *reinterpret_cast<const float4*>(partial + static_cast<size_t>(u) * kF + 4 * j));
+    const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
+    *reinterpret_cast<float4*>(out + static_cast<size_t>(out_by_row ? r : slot) * kF + 4 * j) = f4scale(acc, inv);
+  }
+}
+
+__global__ void hd_units_kernel(uint32_t count, const uint32_t* __restrict__ hd_rows, const uint32_t* __restrict__ rp,
+                                const uint32_t* __restrict__ col, const uint32_t* __restrict__ unit_base,
+                                uint32_t* __restrict__ unit_slot, uint32_t* __restrict__ unit_k,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  for (uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x; slot < count; slot += gridDim.x * blockDim.x) {
+    const uint32_t r = hd_rows[slot], b = rp[r];
+    for (uint32_t u = unit_base[slot], k = 0; u < unit_base[slot + 1]; ++u, ++k) {
+      unit_slot[u] = slot;
+      unit_k[u] = k;
+      keys[u] = col[b + k * kHdChunk];  // first neighbour of the chunk (rows are sorted)
+      ids[u] = u;
+    }
+  }
+}
+
+__global__ void hd_chunk_count_kernel(uint32_t count, const uint32_t* __restrict__ hd_rows,
+                                      const uint32_t* __restrict__ rp, uint32_t* __restrict__ chunks) {
+  for (uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x; slot < count; slot += gridDim.x * blockDim.x) {
+    const uint32_t r = hd_rows[slot];
+    chunks[slot] = (rp[r + 1] - rp[r] + kHdChunk - 1) / kHdChunk;
   }
 }
 
@@ -965,6 +1022,7 @@ void classify_rows(groot_graph* g, uint32_t thr) {
   cnt.download(&num, 1);
   stream_sync();
   g->num_hd = num;
+  g->hdp_valid = false;
   g->hd_rows.alloc(num);
   if (num)
     GROOT_CUDA(cudaMemcpyAsync(g->hd_rows.p, out.p, num * 4ull, cudaMemcpyDeviceToDevice, stream()));
@@ -995,6 +1053,46 @@ static LayerArgs plan_args(groot_graph* g, const float* hin, const HdInfo& hd) {
   if (a.tile_counter) GROOT_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), stream()));
   a.period_rows = g->tp_period_rows;
   return a;
+}
+
+// Per-graph HD plan (see hd_chunk_kernel): chunk units of every HD row,
+// sorted by their first neighbour's row id. Cached on the graph.
+static void build_hd_plan(groot_graph* g) {
+  if (g->hdp_valid || g->num_hd == 0) return;
+  const uint32_t count = g->num_hd;
+  g->hdp_base.alloc(count + 1ull);
+  DevBuf<uint32_t> chunks(count + 1ull);
+  GROOT_LAUNCH(hd_chunk_count_kernel, blocks_for(count, 256), 256, 0, count, g->hd_rows.p, g->rp.p, chunks.p);
+  exclusive_scan_u32(chunks.p, g->hdp_base.p, count);
+  uint32_t nunits = 0;
+  GROOT_CUDA(cudaMemcpyAsync(&nunits, g->hdp_base.p + count, 4, cudaMemcpyDeviceToHost, stream()));
+  stream_sync();
+  DevBuf<uint32_t> keys(nunits), keys2(nunits), ids(nunits);
+  g->hdp_slot.alloc(nunits);
+  g->hdp_k.alloc(nunits);
+  g->hdp_units.alloc(nunits);
+  GROOT_LAUNCH(hd_units_kernel, blocks_for(count, 256), 256, 0, count, g->hd_rows.p, g->rp.p, g->col.p,
+               g->hdp_base.p, g->hdp_slot.p, g->hdp_k.p, keys.p, ids.p);
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, ids.p, g->hdp_units.p, nunits, 0, 32, stream());
+  DevBuf<uint8_t> tmp(bytes);
+  GROOT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, keys2.p, ids.p, g->hdp_units.p, nunits, 0, 32,
+                                             stream()));
+  g->hdp_partial.alloc(static_cast<size_t>(nunits) * kF);
+  g->hdp_nunits = nunits;
+  stream_sync();
+  g->hdp_valid = true;
+}
+
+// HD rows' 32-wide neighbour means of H (L2-ordered chunks + fixed-order reduce).
+static void hd_means32(groot_graph* g, const float* H, float* out, int out_by_row) {
+  build_hd_plan(g);
+  const unsigned sms = static_cast<unsigned>(num_sms());
+  GROOT_LAUNCH(hd_chunk_kernel, blocks_for(g->hdp_nunits * 32ull, 256, sms * 8), 256, 0, g->hdp_units.p,
+               g->hdp_nunits, g->hdp_slot.p, g->hdp_k.p, g->hd_rows.p, g->rp.p, g->col.p, H, g->hdp_partial.p,
+               g->hdp_base.p);
+  GROOT_LAUNCH(hd_reduce_kernel, blocks_for(g->num_hd * 8ull, 256, sms * 8), 256, 0, g->num_hd, g->hd_rows.p, g->rp.p,
+               g->hdp_base.p, g->hdp_partial.p, out, out_by_row);
 }
 
 static void ensure_activations(groot_graph* g) {
@@ -1087,8 +1185,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   if (g->num_hd) {
     ProfScope ps("hd_mean32");
-    GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
-                 g->rp.p, g->col.p, hin, g->hd_mean.p, 0);
+    hd_means32(g, hin, g->hd_mean.p, 0);
   }
   LayerArgs a = plan_args(g, hin, hd);
   a.hout = hout;
@@ -1180,8 +1277,7 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
     const unsigned sms = static_cast<unsigned>(num_sms());
     if (g->num_hd) {
       ProfScope ps("spmm_hd_mean32");
-      GROOT_LAUNCH(hd_mean32_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
-                   g->rp.p, g->col.p, dense, out, 1);
+      hd_means32(g, dense, out, 1);
     }
     set_tc_smem();
     build_tile_plan(g, hd.threshold);
