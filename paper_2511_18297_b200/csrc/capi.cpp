@@ -55,7 +55,10 @@ groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<
                             const std::vector<uint32_t>*);
 void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
 void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
-void layer_device(const groot_model*, groot_graph*, uint32_t, const float*, float*, uint8_t*, float*);
+void layer_device(const groot_model*, groot_graph*, uint32_t, const float*, float*, uint8_t*, float*, uint32_t, uint32_t,
+                  bool);
+void forward_classify_to_host(const groot_model*, groot_graph*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
+                              uint32_t, uint8_t*);
 void layer_prepare(const groot_model*, groot_graph*);
 groot_graph* batch_padded(const groot_graph*, uint32_t, uint32_t);
 bool replicate_forward_plan(groot_graph*, groot_graph*, uint32_t, uint32_t);
@@ -855,7 +858,7 @@ int groot_layer_dev(const groot_model* m, const groot_graph* g, uint32_t layer, 
     if (last && !labels_dev) fail(GROOT_EINVAL, "layer: class output required for the last layer");
     groot_graph* gg = const_cast<groot_graph*>(g);
     layer_prepare(m, gg);
-    layer_device(m, gg, layer, hin_dev, hout_dev, labels_dev, logits_dev);
+    layer_device(m, gg, layer, hin_dev, hout_dev, labels_dev, logits_dev, 0, ~0u, true);
   });
 }
 
@@ -953,19 +956,14 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
       DevBuf<uint8_t> cls(g->n);
       DevBuf<unsigned long long> conf(25);
       conf.zero();
-      forward_device(m, g, cls.p, nullptr, conf.p);
-      if (host_timing) stream_sync();
+      forward_classify_to_host(m, g, cls.p, conf.p, copies, n1, P, labels_out);
       const auto t3 = now();
       uint64_t h[25];
       conf.download(reinterpret_cast<unsigned long long*>(h), 25);
-      if (labels_out)
-        for (uint32_t k = 0; k < copies; ++k)
-          GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls.p + static_cast<size_t>(k) * P, n1,
-                                     cudaMemcpyDeviceToHost, stream()));
       stream_sync();
       const auto t4 = now();
       if (host_timing)
-        std::fprintf(stderr, "[classify_aig] encode %.2f ms, batch %.2f ms, forward %.2f ms, download %.2f ms\n",
+        std::fprintf(stderr, "[classify_aig] encode %.2f ms, batch %.2f ms, forward (enqueue) %.2f ms, forward+download %.2f ms\n",
                      ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
       finish_confusion(h, n1 * copies, confusion, accuracy);
     } catch (...) {

@@ -162,6 +162,7 @@ struct LayerArgs {
   uint32_t plan_period;       // > 0: the plan is one copy's (tiles 0..period-1), tile t uses t % period
   uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
+  uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
 };
 
 // Timeline stamp of CTA 0 for tile iteration it (< 64), event slot k (< 16).
@@ -310,12 +311,12 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         uint32_t t;
         if (a.tile_counter) {
           if (grabbed % kGrab == 0) chunk = atomicAdd(a.tile_counter, kGrab);
-          t = chunk + grabbed % kGrab;
+          t = a.tile_begin + chunk + grabbed % kGrab;
         } else {
-          t = blockIdx.x + grabbed * G;
+          t = a.tile_begin + blockIdx.x + grabbed * G;
         }
         ++grabbed;
-        return t < ntiles ? t : kEndTile;
+        return t < a.tile_end ? t : kEndTile;
       };
       auto meta_of = [&](uint32_t tt) -> uint4 {
         if (tt == kEndTile) return make_uint4(0, 0, 0, 0);
@@ -1160,7 +1161,7 @@ static void prepare_graph(const groot_model* m, groot_graph* g) {
 // (depth 1: layer 0 writes hout, then the head kernel). Rows are computed for
 // every row of g, each from its own neighbour list in g.
 void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float* hin, float* hout, uint8_t* cls,
-                  float* logits) {
+                  float* logits, uint32_t tile_begin, uint32_t tile_end, bool hd_means) {
   const uint32_t n = g->n;
   if (n == 0) return;
   HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
@@ -1183,17 +1184,19 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
     return;
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
-  if (g->num_hd) {
+  if (g->num_hd && hd_means) {
     ProfScope ps("hd_mean32");
     hd_means32(g, hin, g->hd_mean.p, 0);
   }
   LayerArgs a = plan_args(g, hin, hd);
+  a.tile_begin = std::min(tile_begin, ntiles);
+  a.tile_end = std::min(tile_end, ntiles);
   a.hout = hout;
   a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
   a.classes = m->classes;
   a.cls = cls;
   a.logits = logits;
-  const unsigned grid = std::min<uint32_t>(ntiles, sms);
+  const unsigned grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.tile_end - a.tile_begin, sms));
   const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
   HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
   std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
@@ -1238,7 +1241,68 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
   ensure_activations(g);
   for (uint32_t l = 0; l < m->depth; ++l)
     layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, l + 1 < m->depth || m->depth == 1 ? g->act[l & 1].p : nullptr,
-                 cls, logits);
+                 cls, logits, 0, ~0u, true);
+  if (confusion) {
+    ProfScope ps("confusion");
+    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
+                 g->labels.p, confusion);
+  }
+}
+
+// Forward + classify of a tile-aligned batch (batch_padded: copy k at rows
+// k*P .. k*P + n1) with the class read-back overlapped: the last layer runs
+// as two launches over the two halves of the tiles, and the classes of the
+// copies the first half completes go to the host on a side stream while the
+// second half computes. labels_out is in the reference's numbering (k*n1 + v).
+void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls, unsigned long long* confusion,
+                              uint32_t copies, uint32_t n1, uint32_t P, uint8_t* labels_out) {
+  require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
+  if (g->n == 0) return;
+  prepare_graph(m, g);
+  ensure_activations(g);
+  const uint32_t D = m->depth;
+  for (uint32_t l = 0; l + 1 < D; ++l)
+    layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, g->act[l & 1].p, cls, nullptr, 0, ~0u, true);
+  static cudaStream_t side = [] {
+    cudaStream_t st;
+    GROOT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    return st;
+  }();
+  static cudaEvent_t ev_half = [] {
+    cudaEvent_t e;
+    GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }();
+  static cudaEvent_t ev_side = [] {
+    cudaEvent_t e;
+    GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }();
+  uint32_t k1 = 0;
+  if (D == 1) {
+    layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true);
+  } else {
+    const float* hin = g->act[(D - 2) & 1].p;
+    const uint32_t ntiles = (g->n + kTileM - 1) / kTileM, half = ntiles / 2;
+    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, 0, half, true);
+    const uint64_t rows_done = static_cast<uint64_t>(half) * kTileM;
+    while (k1 < copies && static_cast<uint64_t>(k1) * P + n1 <= rows_done) ++k1;
+    if (labels_out && k1) {
+      GROOT_CUDA(cudaEventRecord(ev_half, stream()));
+      GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
+      for (uint32_t k = 0; k < k1; ++k)
+        GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
+                                   cudaMemcpyDeviceToHost, side));
+      GROOT_CUDA(cudaEventRecord(ev_side, side));
+    }
+    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, half, ~0u, false);
+  }
+  if (labels_out) {
+    for (uint32_t k = k1; k < copies; ++k)
+      GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
+                                 cudaMemcpyDeviceToHost, stream()));
+    if (k1) GROOT_CUDA(cudaStreamWaitEvent(stream(), ev_side, 0));
+  }
   if (confusion) {
     ProfScope ps("confusion");
     GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
@@ -1284,6 +1348,8 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
     ProfScope ps("spmm_mean32");
     LayerArgs a = plan_args(g, dense, hd);
     a.spmm_out = out;
+    a.tile_begin = 0;
+    a.tile_end = (g->n + kTileM - 1) / kTileM;
     const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(dense), g->n, kTileM);
     const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
     HeadW hw{};
