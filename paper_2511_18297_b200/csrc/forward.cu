@@ -1085,6 +1085,41 @@ static void build_hd_plan(groot_graph* g) {
   g->hdp_valid = true;
 }
 
+__global__ void replicate_hd_units_kernel(uint32_t nunits1, uint32_t nhd1, uint32_t copies,
+                                          const uint32_t* __restrict__ units1, const uint32_t* __restrict__ slot1,
+                                          const uint32_t* __restrict__ k1, uint32_t* __restrict__ units,
+                                          uint32_t* __restrict__ slot, uint32_t* __restrict__ kk) {
+  const uint64_t total = static_cast<uint64_t>(nunits1) * copies;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(i / nunits1), u = static_cast<uint32_t>(i - static_cast<uint64_t>(c) * nunits1);
+    units[i] = units1[u] + c * nunits1;  // copy c's chunks come after copy c-1's in first-neighbour order
+    slot[i] = slot1[u] + c * nhd1;
+    kk[i] = k1[u];
+  }
+}
+
+// HD plan of a tile-aligned batch from its copy 0's (see replicate_forward_plan).
+void replicate_hd_plan(groot_graph* src, groot_graph* dst, uint32_t copies) {
+  if (src->num_hd == 0 || dst->num_hd != src->num_hd * copies) return;
+  build_hd_plan(src);
+  const uint32_t nu1 = src->hdp_nunits;
+  dst->hdp_nunits = nu1 * copies;
+  dst->hdp_base.alloc(dst->num_hd + 1ull);
+  GROOT_LAUNCH(replicate_offset_kernel, blocks_for(dst->num_hd / 4 + 1, 256), 256, 0,
+               static_cast<uint64_t>(src->num_hd), copies, nu1, src->hdp_base.p, dst->hdp_base.p);
+  const uint32_t last = dst->hdp_nunits;
+  GROOT_CUDA(cudaMemcpyAsync(dst->hdp_base.p + dst->num_hd, &last, 4, cudaMemcpyHostToDevice, stream()));
+  dst->hdp_slot.alloc(dst->hdp_nunits);
+  dst->hdp_k.alloc(dst->hdp_nunits);
+  dst->hdp_units.alloc(dst->hdp_nunits);
+  GROOT_LAUNCH(replicate_hd_units_kernel, blocks_for(dst->hdp_nunits, 256), 256, 0, nu1, src->num_hd, copies,
+               src->hdp_units.p, src->hdp_slot.p, src->hdp_k.p, dst->hdp_units.p, dst->hdp_slot.p, dst->hdp_k.p);
+  dst->hdp_partial.alloc(static_cast<size_t>(dst->hdp_nunits) * kF);
+  stream_sync();  // `last` lives on this stack frame
+  dst->hdp_valid = true;
+}
+
 // HD rows' 32-wide neighbour means of H (L2-ordered chunks + fixed-order reduce).
 static void hd_means32(groot_graph* g, const float* H, float* out, int out_by_row) {
   build_hd_plan(g);

@@ -191,6 +191,7 @@ void build_tile_plan(groot_graph* g, uint32_t thr) {
 namespace groot {
 void classify_rows(groot_graph* g, uint32_t thr);
 uint32_t hd_threshold();
+void replicate_hd_plan(groot_graph* src, groot_graph* dst, uint32_t copies);
 
 // Give the tile-aligned batch `dst` (batch_padded(src, copies, P)) the row
 // classifier output of `src` replicated and the tile plan of `src` as a
@@ -213,6 +214,7 @@ bool replicate_forward_plan(groot_graph* src, groot_graph* dst, uint32_t copies,
                  static_cast<uint64_t>(src->num_hd), copies, P, src->hd_rows.p, dst->hd_rows.p);
   dst->hd_mean.alloc(static_cast<size_t>(dst->num_hd) * 32);
   dst->hd_threshold = thr;
+  replicate_hd_plan(src, dst, copies);
   dst->tp_meta = std::move(src->tp_meta);
   dst->tp_lrp = std::move(src->tp_lrp);
   dst->tp_lcol = std::move(src->tp_lcol);
