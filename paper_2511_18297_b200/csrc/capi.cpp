@@ -56,7 +56,7 @@ groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<
 void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
 void forward_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void layer_device(const groot_model*, groot_graph*, uint32_t, const float*, float*, uint8_t*, float*, uint32_t, uint32_t,
-                  bool);
+                  bool, bool keyed_in = false);
 void forward_classify_to_host(const groot_model*, groot_graph*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
                               uint32_t, uint8_t*);
 void layer_prepare(const groot_model*, groot_graph*);

@@ -167,6 +167,13 @@ struct groot_graph {
   groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
   groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots
   groot::DevBuf<uint32_t> tp_halo;  // halo rows per tile
+  // Keyed layer 0 (forward.cu, l0_key_kernel): per-row records and entry ids,
+  // the record dictionary and the entry rows; l0_mode 0 unknown, 1 keyable, 2 not
+  int l0_mode = 0;
+  groot::DevBuf<unsigned long long> l0_key, l0_dict;
+  groot::DevBuf<uint8_t> l0_id, l0_idmap;
+  groot::DevBuf<float> l0_table;
+  groot::DevBuf<uint32_t> l0_flags;
 };
 
 struct groot_assignment {

@@ -163,6 +163,8 @@ struct LayerArgs {
   uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
+  const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused), see l0_key_kernel
+  const float* ktable;        //                kTkTableRows x 32 rows of the entries
 };
 
 // Timeline stamp of CTA 0 for tile iteration it (< 64), event slot k (< 16).
@@ -205,7 +207,9 @@ constexpr uint32_t kTkMetaBytes = ((kTkHaloOff + kTpHaloCap * 4u + 127u) / 128u)
 #endif
 constexpr uint32_t kTileRing = 32;     // tile ids of the CTA's iterations (dynamic scheduler)
 constexpr uint32_t kEndTile = 0xFFFFFFFFu;
-constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kBBytes + (256 + 32 + kTileRing) * 4 +
+constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8)
+constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kTkTableRows * 128 + kBBytes +
+                                  (256 + 32 + kTileRing) * 4 +
                                   16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
                                   16 + 1024;
 static_assert(kTkRowBytes % 1024 == 0, "row stages keep 1024-B alignment");
@@ -236,7 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows
   uint8_t* sPlan = sRows + kTkRowStages * kTkRowBytes;   // [kTkMetaStages] lrp | lcol | halo list
-  uint8_t* sB = sPlan + kTkMetaStages * kTkMetaBytes;
+  uint8_t* sTable = sPlan + kTkMetaStages * kTkMetaBytes;  // keyed layer 1: entry rows
+  uint8_t* sB = sTable + kTkTableRows * 128;
   float* sInv = reinterpret_cast<float*>(sB + kBBytes);  // 1/d, d < 256
   float* sBias = sInv + 256;                              // layer bias by output feature
   uint32_t* sTile = reinterpret_cast<uint32_t*>(sBias + 32);  // [kTileRing] tile of iteration i (kEndTile: done)
@@ -261,6 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   if (kMma)
     for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
       reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
+  if (a.keys)
+    for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
+      reinterpret_cast<uint4*>(sTable)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
   for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
   if (kMma) {
     for (uint32_t i = threadIdx.x; i < 32; i += kThreads) sBias[i] = hw.bias[i];
@@ -378,6 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const uint32_t rs = it % kTkRowStages;
         ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
         tstamp(a.trace, it, 0);
+        if (a.keys) {  // keyed: the copiers expand the tile rows too
+          ptx::mbar_arrive(&r_full[rs]);
+          continue;
+        }
         ptx::mbar_arrive_expect_tx(&r_full[rs], kTpRows * 128u);
         ptx::tma_load_2d(&tmap_in, sRows + rs * kTkRowBytes, &r_full[rs], 0, static_cast<int32_t>(t * kTileM));
       }
@@ -397,6 +409,42 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_wait_sleep(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, 100);
       const uint32_t hc = sMeta[ms].w;
       if (gl == 0) tstamp(a.trace, it, 1);
+      if (a.keys) {
+        // keyed layer 1: rows are entry rows of the table (16 B per lane,
+        // 8 lanes per row); tile rows past n are never read as neighbours
+        uint8_t* dst = sRows + rs * kTkRowBytes + c * 16u;
+        const uint8_t* src = sTable + c * 16u;
+        const uint32_t row0 = t * kTileM;
+        uint32_t id[kTpRows / kStride];
+#pragma unroll
+        for (uint32_t u = 0; u < kTpRows / kStride; ++u) {
+          const uint32_t r = row0 + s0 + u * kStride;
+          id[u] = r < n ? __ldg(a.keys + r) : 0u;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kTpRows / kStride; ++u)
+          *reinterpret_cast<uint4*>(dst + (s0 + u * kStride) * 128u) = *reinterpret_cast<const uint4*>(src + id[u] * 128u);
+        if (!(hc & kTpSlow)) {
+          const uint32_t shift = a.plan_period ? (t / a.plan_period) * a.period_rows : 0u;
+          const uint8_t* keys_c = a.keys + shift;
+          const uint32_t* hl = reinterpret_cast<const uint32_t*>(sPlan + ms * kTkMetaBytes + kTkHaloOff);
+          uint8_t* hdst = dst + kTpRows * 128u;
+          for (uint32_t b0 = s0; b0 < hc; b0 += 4 * kStride) {
+            uint32_t hid[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hid[u] = b0 + u * kStride < hc ? __ldg(keys_c + hl[b0 + u * kStride]) : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t slot = b0 + u * kStride;
+              if (slot < hc)
+                *reinterpret_cast<uint4*>(hdst + slot * 128u) = *reinterpret_cast<const uint4*>(src + hid[u] * 128u);
+            }
+          }
+        }
+        if (gl == 0) tstamp(a.trace, it, 2);
+        ptx::mbar_arrive(&r_full[rs]);
+        continue;
+      }
       if (!(hc & kTpSlow)) {
         const uint32_t shift = a.plan_period ? (t / a.plan_period) * a.period_rows : 0u;
         const float* hin_c = a.hin + static_cast<size_t>(shift) * kF + 4 * c;
@@ -546,7 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         for (int h = 0; h < 2; ++h)
           for (uint32_t k = 0; k < d[h]; ++k) {
             float4 x0, x1;
-            ptx::ldg_f8(hin_j + static_cast<size_t>(__ldg(a.col + b[h] + k)) * kF, x0, x1);
+            const uint32_t cc = __ldg(a.col + b[h] + k);
+            ptx::ldg_f8(a.keys ? a.ktable + static_cast<size_t>(__ldg(a.keys + cc)) * kF + 8 * j
+                               : hin_j + static_cast<size_t>(cc) * kF,
+                        x0, x1);
             acc_row(m[h], x0, x1);
           }
       }
@@ -794,8 +845,13 @@ __global__ void __launch_bounds__(256) hd_chunk_kernel(const uint32_t* __restric
                                                        const uint32_t* __restrict__ hd_rows,
                                                        const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
                                                        const float* __restrict__ H, float* __restrict__ partial,
-                                                       const uint32_t* __restrict__ unit_base) {
+                                                       const uint32_t* __restrict__ unit_base,
+                                                       const uint8_t* __restrict__ keys) {
   const uint32_t lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+  // keys != null: row c of H is entry row keys[c] (keyed layer 1)
+  auto row_of = [&](uint32_t c) -> const float* {
+    return H + static_cast<size_t>(keys ? static_cast<uint32_t>(__ldg(keys + c)) : c) * kF + 4 * j;
+  };
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nunits; w += warps) {
     const uint32_t u = units[w];
@@ -808,14 +864,14 @@ __global__ void __launch_bounds__(256) hd_chunk_kernel(const uint32_t* __restric
     uint32_t q = b + g;
     for (; q + 12 < e; q += 16) {
       const uint32_t c0 = __ldg(col + q), c1 = __ldg(col + q + 4), c2 = __ldg(col + q + 8), c3 = __ldg(col + q + 12);
-      const float4 v0 = ptx::ldg_f4(H + static_cast<size_t>(c0) * kF + 4 * j);
-      const float4 v1 = ptx::ldg_f4(H + static_cast<size_t>(c1) * kF + 4 * j);
-      const float4 v2 = ptx::ldg_f4(H + static_cast<size_t>(c2) * kF + 4 * j);
-      const float4 v3 = ptx::ldg_f4(H + static_cast<size_t>(c3) * kF + 4 * j);
+      const float4 v0 = ptx::ldg_f4(row_of(c0));
+      const float4 v1 = ptx::ldg_f4(row_of(c1));
+      const float4 v2 = ptx::ldg_f4(row_of(c2));
+      const float4 v3 = ptx::ldg_f4(row_of(c3));
       acc = f4add(f4add(acc, v0), v1);
       acc = f4add(f4add(acc, v2), v3);
     }
-    for (; q < e; q += 4) acc = f4add(acc, ptx::ldg_f4(H + static_cast<size_t>(__ldg(col + q)) * kF + 4 * j));
+    for (; q < e; q += 4) acc = f4add(acc, ptx::ldg_f4(row_of(__ldg(col + q))));
     // fixed-order combine of the 4 groups: lane j of group 0 adds groups 1..3
     float4 o1, o2, o3;
     o1.x = __shfl_down_sync(0xffffffffu, acc.x, 8); o1.y = __shfl_down_sync(0xffffffffu, acc.y, 8);
@@ -900,6 +956,241 @@ __global__ void __launch_bounds__(256) hd_mean_feat_kernel(const uint32_t* __res
       out[static_cast<size_t>(slot) * 4 + threadIdx.x] = static_cast<float>(s) * inv;
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Keyed layer 0. A layer-0 row is a function of an exact integer record: own
+// features, per-feature neighbour counts, degree (mean = count x 1/deg). AIG
+// features are bits (node type, PI/PO, fan-in polarity), so a multiplier has a
+// few dozen distinct records however many nodes it has. Per forward, on every
+// row: the record (the layer-0 aggregation: CSR walk + feature gathers), a
+// dictionary of the distinct records, layer 0's 4 -> 32 transform of each
+// entry (the same FFMA sequence as sage_layer0_kernel: the rows are
+// bit-identical), and a u8 entry id per row. Layer 1 expands ids into rows in
+// shared memory instead of reading n x 128 B of materialized H1 that layer 0
+// would have written. Graphs with non-binary features, HD degree > 4094 or
+// more than 255 distinct records take the materialized path.
+// Record: x (4 bits) | deg (12 bits) | count_k (12 bits each, k = 0..3).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kDictCap = 255;     // entry ids are u8
+constexpr uint32_t kDictSlots = 2048;  // global open-addressing table of records
+constexpr uint32_t kDictLocal = 512;   // per-CTA table
+constexpr uint32_t kDictLocalMax = 384;
+constexpr unsigned long long kDictEmpty = ~0ull;
+
+__device__ __forceinline__ uint32_t dict_hash(unsigned long long k) {
+  return static_cast<uint32_t>((k * 0x9E3779B97F4A7C15ull) >> 40);
+}
+__device__ __forceinline__ unsigned long long l0_record(uint32_t x, uint32_t d, const uint32_t (&s)[4]) {
+  const uint32_t x4 = (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+  return x4 | (static_cast<unsigned long long>(d) << 4) | (static_cast<unsigned long long>(s[0]) << 16) |
+         (static_cast<unsigned long long>(s[1]) << 28) | (static_cast<unsigned long long>(s[2]) << 40) |
+         (static_cast<unsigned long long>(s[3]) << 52);
+}
+// flags[0]: not keyable (overflow / non-binary feature / degree); flags[1]: entries
+__device__ void dict_insert_global(unsigned long long* tab, uint32_t* flags, unsigned long long k) {
+  uint32_t h = dict_hash(k) & (kDictSlots - 1);
+  for (uint32_t p = 0; p < kDictSlots; ++p, h = (h + 1) & (kDictSlots - 1)) {
+    const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tab + h);
+    if (cur == k) return;
+    if (cur == kDictEmpty) {
+      const unsigned long long prev = atomicCAS(tab + h, kDictEmpty, k);
+      if (prev == kDictEmpty) {
+        if (atomicAdd(flags + 1, 1u) >= kDictCap) flags[0] = 1;
+        return;
+      }
+      if (prev == k) return;
+    }
+  }
+  flags[0] = 1;
+}
+
+// LD rows: thread per row (the gather of sage_layer0_kernel), warp-deduplicated
+// records into a per-CTA table, merged into the global table at the end.
+__global__ void __launch_bounds__(256) l0_key_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+                                                     const uint32_t* __restrict__ col,
+                                                     const uint32_t* __restrict__ feat, uint32_t thr,
+                                                     unsigned long long* __restrict__ keys,
+                                                     unsigned long long* __restrict__ gtab, uint32_t* flags) {
+  __shared__ unsigned long long ltab[kDictLocal];
+  __shared__ uint32_t lcount, lbad;
+  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x) ltab[i] = kDictEmpty;
+  if (threadIdx.x == 0) lcount = lbad = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n; base += warps * 32) {
+    const uint32_t row = base + lane;
+    uint32_t b = 0, d = 0;
+    if (row < n) {
+      b = __ldg(rp + row);
+      d = __ldg(rp + row + 1) - b;
+    }
+    unsigned long long key = kDictEmpty;
+    if (row < n && d < thr) {
+      uint32_t packed = 0;
+      uint32_t c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = (static_cast<uint32_t>(k) < d) ? __ldg(col + b + k) : 0u;
+      uint32_t f[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = (static_cast<uint32_t>(k) < d) ? __ldg(feat + c[k]) : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) packed += f[k];
+      for (uint32_t k = 8; k < d; ++k) packed += __ldg(feat + __ldg(col + b + k));
+      const uint32_t x = __ldg(feat + row);
+      // every node's own word is checked here or in hd_key_kernel, so byte
+      // counters of binary features (d < 256) are exact
+      if ((x & 0xFEFEFEFEu) != 0u) lbad = 1;
+      const uint32_t s[4] = {packed & 0xFFu, (packed >> 8) & 0xFFu, (packed >> 16) & 0xFFu, packed >> 24};
+      key = l0_record(x, d, s);
+      keys[row] = key;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (key != kDictEmpty && (__ffs(peers) - 1) == lane) {
+      uint32_t h = dict_hash(key) & (kDictLocal - 1);
+      for (;; h = (h + 1) & (kDictLocal - 1)) {
+        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ltab + h);
+        if (cur == key) break;
+        if (cur == kDictEmpty) {
+          if (*reinterpret_cast<volatile uint32_t*>(&lcount) >= kDictLocalMax) {
+            lbad = 1;
+            break;
+          }
+          const unsigned long long prev = atomicCAS(ltab + h, kDictEmpty, key);
+          if (prev == kDictEmpty) {
+            atomicAdd(&lcount, 1u);
+            break;
+          }
+          if (prev == key) break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && lbad) flags[0] = 1;
+  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x)
+    if (ltab[i] != kDictEmpty) dict_insert_global(gtab, flags, ltab[i]);
+}
+
+// HD rows: CTA per row, exact integer counts (as hd_mean_feat_kernel).
+__global__ void __launch_bounds__(256) hd_key_kernel(const uint32_t* __restrict__ hd_rows, uint32_t count,
+                                                     const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                                     const uint32_t* __restrict__ feat,
+                                                     unsigned long long* __restrict__ keys,
+                                                     unsigned long long* __restrict__ gtab, uint32_t* flags) {
+  __shared__ uint32_t red[8][4];
+  for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
+    const uint32_t r = hd_rows[slot], b = rp[r], d = rp[r + 1] - b;
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) {
+      const uint32_t x = __ldg(feat + __ldg(col + b + e));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] += (x >> (8 * k)) & 0xFFu;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[threadIdx.x >> 5][k] = c[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t s[4] = {0, 0, 0, 0};
+      for (int w = 0; w < 8; ++w)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s[k] += red[w][k];
+      const uint32_t x = __ldg(feat + r);
+      if ((x & 0xFEFEFEFEu) != 0u || d > 4094u) {
+        flags[0] = 1;
+      } else {
+        const unsigned long long key = l0_record(x, d, s);
+        keys[r] = key;
+        dict_insert_global(gtab, flags, key);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// One CTA: entries sorted by record (ids are deterministic), slot -> id map,
+// and H1 of every entry with sage_layer0_kernel's arithmetic.
+__global__ void __launch_bounds__(1024) dict_finalize_kernel(const unsigned long long* __restrict__ gtab,
+                                                             const uint32_t* __restrict__ flags, const Layer0W w,
+                                                             float* __restrict__ table, uint8_t* __restrict__ idmap) {
+  __shared__ unsigned long long ent[kDictCap], sorted[kDictCap];
+  __shared__ uint32_t cnt;
+  if (flags[0]) return;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kDictSlots; i += blockDim.x) {
+    const unsigned long long k = gtab[i];
+    if (k != kDictEmpty) {
+      const uint32_t e = atomicAdd(&cnt, 1u);
+      if (e < kDictCap) ent[e] = k;
+    }
+  }
+  __syncthreads();
+  const uint32_t m = cnt;
+  if (m > kDictCap) return;  // flags[0] is set too
+  for (uint32_t i = threadIdx.x; i < kDictSlots; i += blockDim.x) {
+    const unsigned long long k = gtab[i];
+    if (k == kDictEmpty) continue;
+    uint32_t rank = 0;
+    for (uint32_t e = 0; e < m; ++e) rank += ent[e] < k;
+    idmap[i] = static_cast<uint8_t>(rank);
+    sorted[rank] = k;
+  }
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < m * kF; e += blockDim.x) {
+    const uint32_t id = e / kF, o = e % kF;
+    const unsigned long long k = sorted[id];
+    const uint32_t d = static_cast<uint32_t>(k >> 4) & 0xFFFu;
+    const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float xk = static_cast<float>((k >> q) & 1u);
+      const float mk = static_cast<float>(static_cast<uint32_t>(k >> (16 + 12 * q)) & 0xFFFu) * inv;
+      s1 = fmaf(xk, w.ws[q][o], s1);
+      s2 = fmaf(mk, w.wn[q][o], s2);
+    }
+    table[id * kF + o] = fmaxf((s1 + s2) + w.b[o], 0.f);
+  }
+}
+
+// u8 entry id of every row (4 rows per thread, one 32-bit store).
+__global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, const unsigned long long* __restrict__ keys,
+                                                     const unsigned long long* __restrict__ gtab,
+                                                     const uint8_t* __restrict__ idmap,
+                                                     const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
+  __shared__ unsigned long long t[kDictSlots];
+  __shared__ uint8_t im[kDictSlots];
+  if (flags[0]) return;
+  for (uint32_t i = threadIdx.x; i < kDictSlots; i += blockDim.x) {
+    t[i] = gtab[i];
+    im[i] = idmap[i];
+  }
+  __syncthreads();
+  const uint32_t quads = (n + 3) / 4;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t row = 4 * q + u;
+      if (row < n) {
+        const unsigned long long k = __ldg(keys + row);
+        uint32_t h = dict_hash(k) & (kDictSlots - 1);
+        while (t[h] != k) h = (h + 1) & (kDictSlots - 1);
+        out |= static_cast<uint32_t>(im[h]) << (8 * u);
+      }
+    }
+    if (4 * q + 3 < n) {
+      reinterpret_cast<uint32_t*>(ids)[q] = out;
+    } else {
+      for (int u = 0; u < 4 && 4 * q + u < n; ++u) ids[4 * q + u] = static_cast<uint8_t>(out >> (8 * u));
+    }
   }
 }
 
@@ -1121,12 +1412,12 @@ void replicate_hd_plan(groot_graph* src, groot_graph* dst, uint32_t copies) {
 }
 
 // HD rows' 32-wide neighbour means of H (L2-ordered chunks + fixed-order reduce).
-static void hd_means32(groot_graph* g, const float* H, float* out, int out_by_row) {
+static void hd_means32(groot_graph* g, const float* H, float* out, int out_by_row, const uint8_t* keys = nullptr) {
   build_hd_plan(g);
   const unsigned sms = static_cast<unsigned>(num_sms());
   GROOT_LAUNCH(hd_chunk_kernel, blocks_for(g->hdp_nunits * 32ull, 256, sms * 8), 256, 0, g->hdp_units.p,
                g->hdp_nunits, g->hdp_slot.p, g->hdp_k.p, g->hd_rows.p, g->rp.p, g->col.p, H, g->hdp_partial.p,
-               g->hdp_base.p);
+               g->hdp_base.p, keys);
   GROOT_LAUNCH(hd_reduce_kernel, blocks_for(g->num_hd * 8ull, 256, sms * 8), 256, 0, g->num_hd, g->hd_rows.p, g->rp.p,
                g->hdp_base.p, g->hdp_partial.p, out, out_by_row);
 }
@@ -1195,10 +1486,53 @@ static void prepare_graph(const groot_model* m, groot_graph* g) {
 //   l = depth-1      hin -> head + first-max argmax: cls (u8[n]), logits (n x classes, optional)
 // (depth 1: layer 0 writes hout, then the head kernel). Rows are computed for
 // every row of g, each from its own neighbour list in g.
+// Keyed layer 0 (see l0_key_kernel) of a forward: records, dictionary, entry
+// rows and ids. Returns false (nothing materialized) when the graph is not
+// keyable; the first forward on a graph finds that out (one host sync).
+static bool layer0_keyed(const groot_model* m, groot_graph* g) {
+  const char* e = std::getenv("GROOT_L0_KEYED");
+  if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2) return false;
+  const uint32_t n = g->n;
+  if (g->l0_key.n < n) g->l0_key.alloc(n);
+  if (g->l0_id.n < n) g->l0_id.alloc(n);
+  if (!g->l0_dict.p) {
+    g->l0_dict.alloc(kDictSlots);
+    g->l0_idmap.alloc(kDictSlots);
+    g->l0_table.alloc(kTkTableRows * kF);
+    g->l0_table.zero();
+    g->l0_flags.alloc(2);
+  }
+  const unsigned sms = static_cast<unsigned>(num_sms());
+  const uint32_t* feat = reinterpret_cast<const uint32_t*>(g->feat.p);
+  {
+    ProfScope ps("l0_keys");
+    GROOT_CUDA(cudaMemsetAsync(g->l0_dict.p, 0xFF, kDictSlots * sizeof(unsigned long long), stream()));
+    GROOT_CUDA(cudaMemsetAsync(g->l0_flags.p, 0, 2 * sizeof(uint32_t), stream()));
+    if (g->num_hd)
+      GROOT_LAUNCH(hd_key_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd, g->rp.p,
+                   g->col.p, feat, g->l0_key.p, g->l0_dict.p, g->l0_flags.p);
+    GROOT_LAUNCH(l0_key_kernel, blocks_for(n, 256, sms * 8), 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold,
+                 g->l0_key.p, g->l0_dict.p, g->l0_flags.p);
+    GROOT_LAUNCH(dict_finalize_kernel, 1, 1024, 0, g->l0_dict.p, g->l0_flags.p, *reinterpret_cast<const Layer0W*>(m->l0w),
+                 g->l0_table.p, g->l0_idmap.p);
+    GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, g->l0_key.p, g->l0_dict.p,
+                 g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
+  }
+  if (g->l0_mode == 0) {
+    uint32_t fl[2] = {0, 0};
+    g->l0_flags.download(fl, 2);
+    stream_sync();
+    g->l0_mode = fl[0] ? 2 : 1;
+  }
+  return g->l0_mode == 1;
+}
+
 void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float* hin, float* hout, uint8_t* cls,
-                  float* logits, uint32_t tile_begin, uint32_t tile_end, bool hd_means) {
+                  float* logits, uint32_t tile_begin, uint32_t tile_end, bool hd_means, bool keyed_in) {
   const uint32_t n = g->n;
   if (n == 0) return;
+  keyed_in = keyed_in && l == 1;
+  if (keyed_in) hin = g->l0_table.p;
   HdInfo hd{g->hd_rows.p, g->num_hd, g->hd_threshold, g->hd_mean.p};
   const unsigned sms = static_cast<unsigned>(num_sms());
   if (l == 0) {
@@ -1221,9 +1555,13 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   if (g->num_hd && hd_means) {
     ProfScope ps("hd_mean32");
-    hd_means32(g, hin, g->hd_mean.p, 0);
+    hd_means32(g, hin, g->hd_mean.p, 0, keyed_in ? g->l0_id.p : nullptr);
   }
   LayerArgs a = plan_args(g, hin, hd);
+  if (keyed_in) {
+    a.keys = g->l0_id.p;
+    a.ktable = g->l0_table.p;
+  }
   a.tile_begin = std::min(tile_begin, ntiles);
   a.tile_end = std::min(tile_end, ntiles);
   a.hout = hout;
@@ -1232,7 +1570,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   a.cls = cls;
   a.logits = logits;
   const unsigned grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.tile_end - a.tile_begin, sms));
-  const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), n, kTileM);
+  const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(hin), keyed_in ? kTkTableRows : n, kTileM);
   HeadW hw = *reinterpret_cast<const HeadW*>(m->headw);
   std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
   static const char* trace_path = std::getenv("GROOT_TRACE");
@@ -1274,9 +1612,10 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
   if (g->n == 0) return;
   prepare_graph(m, g);
   ensure_activations(g);
-  for (uint32_t l = 0; l < m->depth; ++l)
+  const bool keyed = layer0_keyed(m, g);
+  for (uint32_t l = keyed ? 1 : 0; l < m->depth; ++l)
     layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, l + 1 < m->depth || m->depth == 1 ? g->act[l & 1].p : nullptr,
-                 cls, logits, 0, ~0u, true);
+                 cls, logits, 0, ~0u, true, keyed);
   if (confusion) {
     ProfScope ps("confusion");
     GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
@@ -1296,8 +1635,9 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   prepare_graph(m, g);
   ensure_activations(g);
   const uint32_t D = m->depth;
-  for (uint32_t l = 0; l + 1 < D; ++l)
-    layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, g->act[l & 1].p, cls, nullptr, 0, ~0u, true);
+  const bool keyed = layer0_keyed(m, g);
+  for (uint32_t l = keyed ? 1 : 0; l + 1 < D; ++l)
+    layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, g->act[l & 1].p, cls, nullptr, 0, ~0u, true, keyed);
   static cudaStream_t side = [] {
     cudaStream_t st;
     GROOT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1315,11 +1655,11 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   }();
   uint32_t k1 = 0;
   if (D == 1) {
-    layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true);
+    layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true, false);
   } else {
     const float* hin = g->act[(D - 2) & 1].p;
     const uint32_t ntiles = (g->n + kTileM - 1) / kTileM, half = ntiles / 2;
-    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, 0, half, true);
+    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, 0, half, true, keyed);
     const uint64_t rows_done = static_cast<uint64_t>(half) * kTileM;
     while (k1 < copies && static_cast<uint64_t>(k1) * P + n1 <= rows_done) ++k1;
     if (labels_out && k1) {
@@ -1330,7 +1670,7 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
                                    cudaMemcpyDeviceToHost, side));
       GROOT_CUDA(cudaEventRecord(ev_side, side));
     }
-    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, half, ~0u, false);
+    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, half, ~0u, false, keyed);
   }
   if (labels_out) {
     for (uint32_t k = k1; k < copies; ++k)

@@ -1,0 +1,127 @@
+"""Keyed layer 0 (forward.cu, l0_key_kernel / dict_finalize_kernel): layer 1
+reads entry rows of a record dictionary instead of materialized layer-0 rows.
+
+The entry rows are computed with the layer-0 kernel's own arithmetic, so the
+keyed forward must be BIT-identical to the materialized one (GROOT_L0_KEYED=0),
+and both within the oracle tolerance. Graphs that are not keyable (non-binary
+features, more than 255 distinct records) must fall back to the materialized
+path and still match the oracle.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2511_18297_b200 import api as A
+    return A
+
+
+def profiled_names(fn):
+    """Run fn with the library's per-kernel profiler on; return the scope names."""
+    from paper_2511_18297_b200 import _lib
+    L = _lib.lib()
+    L.groot_profile_enable(1)
+    out = fn()
+    maxk = 64
+    names = C.create_string_buffer(48 * maxk)
+    tot = (C.c_double * maxk)()
+    cnt = (C.c_uint64 * maxk)()
+    nk = C.c_uint32()
+    assert L.groot_profile_read(maxk, names, tot, cnt, C.byref(nk)) == 0
+    L.groot_profile_enable(0)
+    got = {names.raw[48 * i:48 * (i + 1)].split(b"\0")[0].decode() for i in range(min(nk.value, maxk))}
+    return out, got
+
+
+def with_env(key, val, fn):
+    old = os.environ.get(key)
+    os.environ[key] = val
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[key]
+        else:
+            os.environ[key] = old
+
+
+def rel_err(a, ref):
+    return float((np.abs(a.astype(np.float64) - ref).max(1) / np.maximum(np.abs(ref).max(1), 1e-6)).max())
+
+
+@pytest.mark.parametrize("circuit,width,copies,depth", [("csa", 64, 2, 4), ("csa", 256, 1, 2), ("booth", 16, 3, 3),
+                                                        ("csa", 8, 1, 4)])
+def test_keyed_bit_identical_to_materialized(api, circuit, width, copies, depth):
+    c = api.gen_csa_multiplier(width) if circuit == "csa" else api.gen_booth_multiplier(width)
+    g = api.encode(c.aig, c.labels)
+    if copies > 1:
+        g = api.batch(g, copies)
+    prm = O.init_model(5, depth=depth)
+    model = api.Model.from_params(prm, depth=depth)
+    keyed, names = profiled_names(lambda: api.forward(model, g))
+    assert "l0_keys" in names and "sage_layer0" not in names, names
+    plain = with_env("GROOT_L0_KEYED", "0", lambda: api.forward(model, g))
+    np.testing.assert_array_equal(keyed, plain)
+    p1 = api.predict_full(model, g)
+    p0 = with_env("GROOT_L0_KEYED", "0", lambda: api.predict_full(model, g))
+    np.testing.assert_array_equal(p1.labels, p0.labels)
+    h = O.encode(O.Aig(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits, c.labels))
+    if copies > 1:
+        h = O.batch(h, copies)
+    assert rel_err(keyed, O.forward(h, prm, depth=depth)) <= 1e-5
+
+
+def test_keyed_classify_aig_matches_materialized(api, golden_dir):
+    """groot_classify_aig (tile-aligned batch, periodic plan, split last layer)."""
+    model = api.load_model(os.path.join(golden_dir, "trained_csa8.asg1"))
+    c = api.gen_csa_multiplier(64)
+    r1 = api.classify_aig(model, c.aig, c.labels, 5)
+    r0 = with_env("GROOT_L0_KEYED", "0", lambda: api.classify_aig(model, c.aig, c.labels, 5))
+    np.testing.assert_array_equal(r1.labels, r0.labels)
+    np.testing.assert_array_equal(r1.confusion, r0.confusion)
+
+
+def random_graph(n, max_deg, seed, feat_max=1):
+    rng = np.random.default_rng(seed)
+    e = []
+    for v in range(1, n):
+        for u in rng.integers(0, v, rng.integers(1, max_deg)):
+            e.append((int(u), v))
+    e = np.array(e, np.uint32)
+    rp, ci = O.build_csr(n, e)
+    feat = rng.integers(0, feat_max + 1, (n, 4)).astype(np.uint8)
+    return rp, ci, feat
+
+
+@pytest.mark.parametrize("case", ["non_binary", "many_records", "keyable_random"])
+def test_keyed_fallback(api, case):
+    if case == "non_binary":
+        rp, ci, feat = random_graph(3000, 6, 1, feat_max=2)
+    elif case == "many_records":  # ~2100 distinct records
+        rp, ci, feat = random_graph(3000, 3, 3)
+    else:  # sparse binary features: ~90 distinct records
+        rp, ci, feat = random_graph(3000, 3, 3)
+        feat[:] = 0
+        feat[::7, 0] = 1
+    n = feat.shape[0]
+    g = api.EdaGraph.from_host(n, rp, ci, feat, np.zeros(n, np.uint8))
+    prm = O.init_model(9)
+    model = api.Model.from_params(prm)
+    lg, names = profiled_names(lambda: api.forward(model, g))
+    h = O.HostGraph(n, rp, ci, feat, np.zeros(n, np.uint8), np.diff(rp).astype(np.uint32), np.zeros((0, 2), np.uint32))
+    assert rel_err(lg, O.forward(h, prm)) <= 1e-5
+    keyed = case == "keyable_random"
+    assert ("sage_layer0" in names) != keyed, names
+    if keyed:
+        np.testing.assert_array_equal(lg, with_env("GROOT_L0_KEYED", "0", lambda: api.forward(model, g)))
