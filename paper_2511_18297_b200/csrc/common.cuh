@@ -171,7 +171,7 @@ struct groot_graph {
   // the record dictionary and the entry rows; l0_mode 0 unknown, 1 keyable, 2 not
   int l0_mode = 0;
   groot::DevBuf<unsigned long long> l0_key, l0_dict;
-  groot::DevBuf<uint8_t> l0_id, l0_idmap;
+  groot::DevBuf<uint8_t> l0_id, l0_idmap, l0_hid;
   groot::DevBuf<float> l0_table;
   groot::DevBuf<uint32_t> l0_flags;
 };

@@ -163,7 +163,8 @@ struct LayerArgs {
   uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
-  const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused), see l0_key_kernel
+  const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused; tiles x 128), see l0_key_kernel
+  const uint8_t* hids;        //                entry ids of the halo rows (tiles x kTpHaloCap, as the halo list)
   const float* ktable;        //                kTkTableRows x 32 rows of the entries
 };
 
@@ -201,7 +202,9 @@ constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;
 constexpr uint32_t kTkLrpOff = 0;
 constexpr uint32_t kTkLcolOff = kTpLrp * 2u + 16u;
 constexpr uint32_t kTkHaloOff = kTkLcolOff + kTpColCap * 2u;
-constexpr uint32_t kTkMetaBytes = ((kTkHaloOff + kTpHaloCap * 4u + 127u) / 128u) * 128u;
+constexpr uint32_t kTkKidOff = kTkHaloOff + kTpHaloCap * 4u;  // keyed: entry ids of the tile rows
+constexpr uint32_t kTkHidOff = kTkKidOff + kTpRows;             //        and of the halo rows
+constexpr uint32_t kTkMetaBytes = ((kTkHidOff + kTpHaloCap + 127u) / 128u) * 128u;
 #ifndef GROOT_GRAB
 #define GROOT_GRAB 8
 #endif
@@ -213,7 +216,9 @@ constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * k
                                   16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
                                   16 + 1024;
 static_assert(kTkRowBytes % 1024 == 0, "row stages keep 1024-B alignment");
-static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0, "bulk-copy destinations must be 16-B aligned");
+static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0 && kTkKidOff % 16 == 0 && kTkHidOff % 16 == 0 &&
+                  kTpHaloCap % 16 == 0,
+              "bulk-copy destinations and keyed halo-id sources must be 16-B aligned");
 static_assert(kTkSmemBytes <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
 
 __device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const float4& x1) {
@@ -232,7 +237,7 @@ __device__ __forceinline__ void swap_halves(float2 (&m)[4], bool sw) {
   }
 }
 
-template <int kMode>
+template <int kMode, bool kKeyed = false>
 __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
                                                                 const __grid_constant__ CUtensorMap tmap_in) {
   constexpr bool kMma = kMode != kModeSpmm;
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   if (kMma)
     for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
       reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
-  if (a.keys)
+  if (kKeyed)
     for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
       reinterpret_cast<uint4*>(sTable)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
   for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
@@ -347,7 +352,12 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         sMeta[ms] = m;
         const bool slow = (m.w & kTpSlow) != 0;
         const uint32_t hpad = slow ? 0u : (m.w + 3u) & ~3u;
-        ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u);
+        const uint32_t kpad = kKeyed ? (slow ? 0u : (m.w + 15u) & ~15u) : 0u;
+        ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u + (kKeyed ? kTpRows + kpad : 0u));
+        if (kKeyed) {
+          ptx::bulk_load(sp + kTkKidOff, a.keys + static_cast<size_t>(t) * kTpRows, kTpRows, &m_full[ms]);
+          if (kpad) ptx::bulk_load(sp + kTkHidOff, a.hids + static_cast<size_t>(t) * kTpHaloCap, kpad, &m_full[ms]);
+        }
         const uint32_t pt = a.plan_period ? t % a.plan_period : t;
         ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(pt) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
         if (m.z) ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
@@ -386,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const uint32_t rs = it % kTkRowStages;
         ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
         tstamp(a.trace, it, 0);
-        if (a.keys) {  // keyed: the copiers expand the tile rows too
+        if (kKeyed) {  // keyed: rows are read from the entry table
           ptx::mbar_arrive(&r_full[rs]);
           continue;
         }
@@ -409,39 +419,22 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_wait_sleep(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, 100);
       const uint32_t hc = sMeta[ms].w;
       if (gl == 0) tstamp(a.trace, it, 1);
-      if (a.keys) {
-        // keyed layer 1: rows are entry rows of the table (16 B per lane,
-        // 8 lanes per row); tile rows past n are never read as neighbours
-        uint8_t* dst = sRows + rs * kTkRowBytes + c * 16u;
-        const uint8_t* src = sTable + c * 16u;
-        const uint32_t row0 = t * kTileM;
-        uint32_t id[kTpRows / kStride];
-#pragma unroll
-        for (uint32_t u = 0; u < kTpRows / kStride; ++u) {
-          const uint32_t r = row0 + s0 + u * kStride;
-          id[u] = r < n ? __ldg(a.keys + r) : 0u;
+      if (kKeyed) {
+        // keyed layer 1: no rows to copy (producers read the entry table);
+        // rewrite the tile's local slots into entry ids in place, so the
+        // producers' gather has the plain path's dependency chain
+        uint16_t* lc = reinterpret_cast<uint16_t*>(sPlan + ms * kTkMetaBytes + kTkLcolOff);
+        const uint8_t* kid = sPlan + ms * kTkMetaBytes + kTkKidOff;
+        const uint32_t cnt = sMeta[ms].z;
+#pragma unroll 4
+        // (the window also spans HD rows' and alignment entries, never read: unset)
+        for (uint32_t k = gl; k < cnt; k += 32 * kCopiers) {
+          const uint32_t v = lc[k];
+          lc[k] = v < kTpRows + kTpHaloCap ? kid[v] : 0u;
         }
-#pragma unroll
-        for (uint32_t u = 0; u < kTpRows / kStride; ++u)
-          *reinterpret_cast<uint4*>(dst + (s0 + u * kStride) * 128u) = *reinterpret_cast<const uint4*>(src + id[u] * 128u);
-        if (!(hc & kTpSlow)) {
-          const uint32_t shift = a.plan_period ? (t / a.plan_period) * a.period_rows : 0u;
-          const uint8_t* keys_c = a.keys + shift;
-          const uint32_t* hl = reinterpret_cast<const uint32_t*>(sPlan + ms * kTkMetaBytes + kTkHaloOff);
-          uint8_t* hdst = dst + kTpRows * 128u;
-          for (uint32_t b0 = s0; b0 < hc; b0 += 4 * kStride) {
-            uint32_t hid[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) hid[u] = b0 + u * kStride < hc ? __ldg(keys_c + hl[b0 + u * kStride]) : 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t slot = b0 + u * kStride;
-              if (slot < hc)
-                *reinterpret_cast<uint4*>(hdst + slot * 128u) = *reinterpret_cast<const uint4*>(src + hid[u] * 128u);
-            }
-          }
-        }
-        if (gl == 0) tstamp(a.trace, it, 2);
+        // the stage is refilled by bulk copies (async proxy) once the producers
+        // release it: order these generic-proxy writes before that
+        ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&r_full[rs]);
         continue;
       }
@@ -539,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       tstamp(tr, it, 4);
       const uint8_t* st = sRows + rs * kTkRowBytes;
       const uint8_t* sp = sPlan + ms * kTkMetaBytes;
+      // neighbour rows: staged rows, or (keyed) entry rows: the copiers have
+      // rewritten the local slots into entry ids
+      const uint8_t* rbase = kKeyed ? sTable : st;
       const bool slow = (sMeta[ms].w & kTpSlow) != 0;
       float2 m[2][4];
       uint32_t d[2];
@@ -570,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (k0 + u < d[h]) {
-                const uint8_t* rowp = st + loc[u] * 128u;
+                const uint8_t* rowp = rbase + loc[u] * 128u;
                 x[u][0] = *reinterpret_cast<const float4*>(rowp + off0);
                 x[u][1] = *reinterpret_cast<const float4*>(rowp + off1);
               }
@@ -595,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           for (uint32_t k = 0; k < d[h]; ++k) {
             float4 x0, x1;
             const uint32_t cc = __ldg(a.col + b[h] + k);
-            ptx::ldg_f8(a.keys ? a.ktable + static_cast<size_t>(__ldg(a.keys + cc)) * kF + 8 * j
+            ptx::ldg_f8(kKeyed ? a.ktable + static_cast<size_t>(__ldg(a.keys + cc)) * kF + 8 * j
                                : hin_j + static_cast<size_t>(cc) * kF,
                         x0, x1);
             acc_row(m[h], x0, x1);
@@ -605,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       if (kMma) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint8_t* rowp = st + (li + 8 * h) * 128u;
+          const uint8_t* rowp = kKeyed ? sTable + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
           const float4 f0 = *reinterpret_cast<const float4*>(rowp + off0);
           const float4 f1 = *reinterpret_cast<const float4*>(rowp + off1);
           hs[h][0] = gp ? f1 : f0;
@@ -1194,6 +1190,26 @@ __global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, const unsigned 
   }
 }
 
+// Entry ids of every tile's halo rows, laid out like the halo list (tile t at
+// t * kTpHaloCap), so the fused layer's loader stages them with the plan.
+// Periodic plans: tile t uses plan tile t % period, rows shifted per period.
+__global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const uint4* __restrict__ tmeta,
+                                                          const uint32_t* __restrict__ halo, uint32_t period,
+                                                          uint32_t period_rows, const uint8_t* __restrict__ ids,
+                                                          const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids) {
+  if (flags[0]) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
+    const uint32_t pt = period ? t % period : t;
+    const uint32_t shift = period ? (t / period) * period_rows : 0u;
+    const uint4 m = __ldg(tmeta + pt);
+    if (m.w & kTpSlow) continue;
+    for (uint32_t k = lane; k < m.w; k += 32)
+      hids[static_cast<size_t>(t) * kTpHaloCap + k] = __ldg(ids + shift + __ldg(halo + m.y + k));
+  }
+}
+
 // General CSR SpMM (spmm::execute over CsrMatrix<float>): 8 lanes per row,
 // columns strided by 8, nonzeros accumulated in order. vals == nullptr -> 1/deg.
 __global__ void __launch_bounds__(256) spmm_generic_kernel(uint32_t rows, const uint32_t* __restrict__ rp,
@@ -1459,6 +1475,8 @@ static void set_tc_smem() {
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
   done = true;
 }
 
@@ -1493,8 +1511,10 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   const char* e = std::getenv("GROOT_L0_KEYED");
   if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2) return false;
   const uint32_t n = g->n;
+  const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   if (g->l0_key.n < n) g->l0_key.alloc(n);
-  if (g->l0_id.n < n) g->l0_id.alloc(n);
+  if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
+  if (g->l0_hid.n < static_cast<size_t>(ntiles) * kTpHaloCap) g->l0_hid.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
   if (!g->l0_dict.p) {
     g->l0_dict.alloc(kDictSlots);
     g->l0_idmap.alloc(kDictSlots);
@@ -1517,6 +1537,9 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
                  g->l0_table.p, g->l0_idmap.p);
     GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, g->l0_key.p, g->l0_dict.p,
                  g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
+    GROOT_LAUNCH(l0_halo_ids_kernel, blocks_for(ntiles * 32ull, 256, sms * 8), 256, 0, ntiles,
+                 reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_halo.p, g->tp_period, g->tp_period_rows,
+                 g->l0_id.p, g->l0_flags.p, g->l0_hid.p);
   }
   if (g->l0_mode == 0) {
     uint32_t fl[2] = {0, 0};
@@ -1560,6 +1583,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   LayerArgs a = plan_args(g, hin, hd);
   if (keyed_in) {
     a.keys = g->l0_id.p;
+    a.hids = g->l0_hid.p;
     a.ktable = g->l0_table.p;
   }
   a.tile_begin = std::min(tile_begin, ntiles);
@@ -1582,10 +1606,16 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   }
   if (l + 1 == m->depth) {
     ProfScope ps("sage_layer_tc_last");
-    GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+    if (keyed_in)
+      GROOT_LAUNCH((sage_tile_kernel<kModeLast, true>), grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+    else
+      GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
   } else {
-    ProfScope ps("sage_layer_tc");
-    GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+    ProfScope ps(keyed_in ? "sage_layer_tc_keyed" : "sage_layer_tc");
+    if (keyed_in)
+      GROOT_LAUNCH((sage_tile_kernel<kModeLayer, true>), grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+    else
+      GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
   }
   if (a.trace) {
     std::vector<unsigned long long> h(64 * 16);
