@@ -304,7 +304,17 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "sage_tile_kernel<kModeLayer> (tile-planned fused 32->32 SAGE layer)",
                 "algorithmic_bytes_per_launch": bytes_tc, "peak_source": peak_src}
-    full_bytes = 114386760032 * (E / 268107776) if (args.width == 1024 and args.circuit == "csa") else None
+    # whole forward: CSR / plan structure, layer inputs and outputs, u8 classes.
+    # Keyed layer 0 (records -> u8 entry ids) replaces the n x 128 B layer-0 rows written by
+    # layer 0 and read back by layer 1 with one byte per row each way.
+    keyed = "l0_keys" in kernels
+    depth = 4
+    csr, ld = 4 * (n + 1) + 4 * nnz, 4 * (n + 1) + 4 * ld_nnz
+    l0 = csr + 4 * n + (n if keyed else 128 * n)
+    l1 = ld + (n if keyed else 128 * n) + 128 * n + 128 * num_hd
+    mid = ld + 128 * n + 128 * n + 128 * num_hd
+    last = ld + 128 * n + n + 128 * num_hd
+    full_bytes = l0 + l1 + mid * (depth - 3) + last + 2 * n
 
     # standalone SpMM (mean aggregation, f=32): the metric's "SpMM HBM GB/s"
     dense = torch.randn(n, 32, device="cuda")
@@ -387,7 +397,7 @@ def run_ours(args):
                        "l2": "inputs (>40 GB resident) far exceed L2; no flush"},
             "roofline": roof,
             "forward_roofline": ({"algorithmic_bytes": full_bytes, "achieved_gbs": full_bytes / ms / 1e6,
-                                  "frac": full_bytes / ms / 1e6 / peak} if full_bytes else None),
+                                  "frac": full_bytes / ms / 1e6 / peak, "keyed_layer0": keyed} if full_bytes else None),
             "spmm": spmm,
             "kernels": kernels,
             "cpu_baseline": cpu,

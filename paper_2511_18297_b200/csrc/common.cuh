@@ -170,8 +170,9 @@ struct groot_graph {
   // Keyed layer 0 (forward.cu, l0_key_kernel): per-row records and entry ids,
   // the record dictionary and the entry rows; l0_mode 0 unknown, 1 keyable, 2 not
   int l0_mode = 0;
-  groot::DevBuf<unsigned long long> l0_key, l0_dict;
-  groot::DevBuf<uint8_t> l0_id, l0_idmap, l0_hid;
+  groot::DevBuf<unsigned long long> l0_key, l0_dict, l0_ctab;  // l0_key: HD rows' records
+  groot::DevBuf<uint16_t> l0_slot;                             // LD rows: slot in their CTA's table
+  groot::DevBuf<uint8_t> l0_id, l0_idmap, l0_hid, l0_xlat;
   groot::DevBuf<float> l0_table;
   groot::DevBuf<uint32_t> l0_flags;
 };

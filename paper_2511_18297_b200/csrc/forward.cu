@@ -1002,12 +1002,18 @@ __device__ void dict_insert_global(unsigned long long* tab, uint32_t* flags, uns
   flags[0] = 1;
 }
 
-// LD rows: thread per row (the gather of sage_layer0_kernel), warp-deduplicated
-// records into a per-CTA table, merged into the global table at the end.
+// LD rows: kL0KeyRows rows per thread with their gathers interleaved (a row's
+// chain row_ptr -> col -> features is three dependent memory round trips), the
+// gather of sage_layer0_kernel; warp-deduplicated records go into a per-CTA
+// table. A row stores its u16 slot in its CTA's table (the CTA is a function
+// of the row: l0_ids_kernel); the tables stay in global memory and are merged
+// into the global dictionary.
+constexpr uint32_t kL0KeyRows = 1;  // rows per thread (measured: 4 rows per thread with 40 registers is slower: occupancy, not the chain, bounds the loads in flight)
 __global__ void __launch_bounds__(256) l0_key_kernel(uint32_t n, const uint32_t* __restrict__ rp,
                                                      const uint32_t* __restrict__ col,
                                                      const uint32_t* __restrict__ feat, uint32_t thr,
-                                                     unsigned long long* __restrict__ keys,
+                                                     uint16_t* __restrict__ lslot,
+                                                     unsigned long long* __restrict__ ctab,
                                                      unsigned long long* __restrict__ gtab, uint32_t* flags) {
   __shared__ unsigned long long ltab[kDictLocal];
   __shared__ uint32_t lcount, lbad;
@@ -1016,65 +1022,90 @@ __global__ void __launch_bounds__(256) l0_key_kernel(uint32_t n, const uint32_t*
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n; base += warps * 32) {
-    const uint32_t row = base + lane;
-    uint32_t b = 0, d = 0;
-    if (row < n) {
-      b = __ldg(rp + row);
-      d = __ldg(rp + row + 1) - b;
+  constexpr uint32_t kR = kL0KeyRows;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32 * kR; base < n;
+       base += warps * 32 * kR) {
+    uint32_t b[kR], d[kR];
+#pragma unroll
+    for (uint32_t r = 0; r < kR; ++r) {
+      const uint32_t row = base + 32 * r + lane;
+      b[r] = row < n ? __ldg(rp + row) : 0u;
+      d[r] = row < n ? __ldg(rp + row + 1) - b[r] : 0u;
+      if (d[r] >= thr) d[r] = 0xFFFFFFFFu;  // HD row: hd_key_kernel
     }
-    unsigned long long key = kDictEmpty;
-    if (row < n && d < thr) {
-      uint32_t packed = 0;
-      uint32_t c[8];
+    uint32_t c[kR][8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = (static_cast<uint32_t>(k) < d) ? __ldg(col + b + k) : 0u;
-      uint32_t f[8];
+    for (uint32_t r = 0; r < kR; ++r)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) f[k] = (static_cast<uint32_t>(k) < d) ? __ldg(feat + c[k]) : 0u;
+      for (uint32_t k = 0; k < 8; ++k) c[r][k] = (d[r] != 0xFFFFFFFFu && k < d[r]) ? __ldg(col + b[r] + k) : 0u;
+    uint32_t packed[kR], x[kR];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) packed += f[k];
-      for (uint32_t k = 8; k < d; ++k) packed += __ldg(feat + __ldg(col + b + k));
-      const uint32_t x = __ldg(feat + row);
-      // every node's own word is checked here or in hd_key_kernel, so byte
-      // counters of binary features (d < 256) are exact
-      if ((x & 0xFEFEFEFEu) != 0u) lbad = 1;
-      const uint32_t s[4] = {packed & 0xFFu, (packed >> 8) & 0xFFu, (packed >> 16) & 0xFFu, packed >> 24};
-      key = l0_record(x, d, s);
-      keys[row] = key;
+    for (uint32_t r = 0; r < kR; ++r) {
+      const uint32_t row = base + 32 * r + lane;
+      x[r] = row < n ? __ldg(feat + row) : 0u;
+      packed[r] = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k)
+        packed[r] += (d[r] != 0xFFFFFFFFu && k < d[r]) ? __ldg(feat + c[r][k]) : 0u;
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    if (key != kDictEmpty && (__ffs(peers) - 1) == lane) {
-      uint32_t h = dict_hash(key) & (kDictLocal - 1);
-      for (;; h = (h + 1) & (kDictLocal - 1)) {
-        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ltab + h);
-        if (cur == key) break;
-        if (cur == kDictEmpty) {
-          if (*reinterpret_cast<volatile uint32_t*>(&lcount) >= kDictLocalMax) {
-            lbad = 1;
-            break;
-          }
-          const unsigned long long prev = atomicCAS(ltab + h, kDictEmpty, key);
-          if (prev == kDictEmpty) {
-            atomicAdd(&lcount, 1u);
-            break;
-          }
-          if (prev == key) break;
-        }
+#pragma unroll
+    for (uint32_t r = 0; r < kR; ++r) {
+      const uint32_t row = base + 32 * r + lane;
+      const bool ld = row < n && d[r] != 0xFFFFFFFFu;
+      if (ld)
+        for (uint32_t k = 8; k < d[r]; ++k) packed[r] += __ldg(feat + __ldg(col + b[r] + k));
+      unsigned long long key = kDictEmpty;
+      if (ld) {
+        // every node's own word is checked here or in hd_key_kernel, so byte
+        // counters of binary features (d < 256) are exact
+        if ((x[r] & 0xFEFEFEFEu) != 0u) lbad = 1;
+        const uint32_t s[4] = {packed[r] & 0xFFu, (packed[r] >> 8) & 0xFFu, (packed[r] >> 16) & 0xFFu,
+                               packed[r] >> 24};
+        key = l0_record(x[r], d[r], s);
       }
+      // warp-level dedup: the first lane of each record finds / inserts its slot
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      uint32_t slot = 0xFFFFu;
+      if (key != kDictEmpty && leader == lane) {
+        uint32_t h = dict_hash(key) & (kDictLocal - 1);
+        for (;; h = (h + 1) & (kDictLocal - 1)) {
+          const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ltab + h);
+          if (cur == key) break;
+          if (cur == kDictEmpty) {
+            if (*reinterpret_cast<volatile uint32_t*>(&lcount) >= kDictLocalMax) {
+              lbad = 1;
+              h = 0xFFFFu;
+              break;
+            }
+            const unsigned long long prev = atomicCAS(ltab + h, kDictEmpty, key);
+            if (prev == kDictEmpty) {
+              atomicAdd(&lcount, 1u);
+              break;
+            }
+            if (prev == key) break;
+          }
+        }
+        slot = h;
+      }
+      slot = __shfl_sync(0xffffffffu, slot, leader);
+      if (row < n) lslot[row] = static_cast<uint16_t>(key != kDictEmpty ? slot : 0xFFFFu);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && lbad) flags[0] = 1;
-  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x)
-    if (ltab[i] != kDictEmpty) dict_insert_global(gtab, flags, ltab[i]);
+  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x) {
+    const unsigned long long k = ltab[i];
+    ctab[static_cast<size_t>(blockIdx.x) * kDictLocal + i] = k;
+    if (k != kDictEmpty) dict_insert_global(gtab, flags, k);
+  }
 }
 
 // HD rows: CTA per row, exact integer counts (as hd_mean_feat_kernel).
 __global__ void __launch_bounds__(256) hd_key_kernel(const uint32_t* __restrict__ hd_rows, uint32_t count,
                                                      const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
                                                      const uint32_t* __restrict__ feat,
-                                                     unsigned long long* __restrict__ keys,
+                                                     unsigned long long* __restrict__ hdkey,
                                                      unsigned long long* __restrict__ gtab, uint32_t* flags) {
   __shared__ uint32_t red[8][4];
   for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
@@ -1102,7 +1133,7 @@ __global__ void __launch_bounds__(256) hd_key_kernel(const uint32_t* __restrict_
         flags[0] = 1;
       } else {
         const unsigned long long key = l0_record(x, d, s);
-        keys[r] = key;
+        hdkey[slot] = key;
         dict_insert_global(gtab, flags, key);
       }
     }
@@ -1156,38 +1187,59 @@ __global__ void __launch_bounds__(1024) dict_finalize_kernel(const unsigned long
   }
 }
 
-// u8 entry id of every row (4 rows per thread, one 32-bit store).
-__global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, const unsigned long long* __restrict__ keys,
-                                                     const unsigned long long* __restrict__ gtab,
-                                                     const uint8_t* __restrict__ idmap,
-                                                     const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
-  __shared__ unsigned long long t[kDictSlots];
-  __shared__ uint8_t im[kDictSlots];
+__device__ __forceinline__ uint32_t dict_lookup(const unsigned long long* t, unsigned long long k) {
+  uint32_t h = dict_hash(k) & (kDictSlots - 1);
+  while (t[h] != k) h = (h + 1) & (kDictSlots - 1);
+  return h;
+}
+
+// Per-CTA slot -> entry id (kDictLocal per l0_key_kernel CTA).
+__global__ void __launch_bounds__(256) l0_xlat_kernel(uint32_t ctas, const unsigned long long* __restrict__ ctab,
+                                                      const unsigned long long* __restrict__ gtab,
+                                                      const uint8_t* __restrict__ idmap,
+                                                      const uint32_t* __restrict__ flags, uint8_t* __restrict__ xlat) {
   if (flags[0]) return;
-  for (uint32_t i = threadIdx.x; i < kDictSlots; i += blockDim.x) {
-    t[i] = gtab[i];
-    im[i] = idmap[i];
+  const uint32_t total = ctas * kDictLocal;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = ctab[i];
+    xlat[i] = k == kDictEmpty ? 0u : idmap[dict_lookup(gtab, k)];
   }
-  __syncthreads();
+}
+
+// u8 entry id of every LD row (4 rows per thread, one 32-bit store): the row's
+// l0_key_kernel CTA (warp-strided row groups: CTA = ((row / (32 kL0KeyRows)) % warps) / 8) and
+// its slot there. HD rows are written afterwards by l0_hd_ids_kernel.
+__global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, uint32_t key_warps, const uint16_t* __restrict__ lslot,
+                                                     const uint8_t* __restrict__ xlat,
+                                                     const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
+  if (flags[0]) return;
   const uint32_t quads = (n + 3) / 4;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+    const uint32_t cta = (((4 * q) / (32 * kL0KeyRows)) % key_warps) >> 3;  // the 4 rows share a row group
+    const uint8_t* xl = xlat + static_cast<size_t>(cta) * kDictLocal;
     uint32_t out = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t row = 4 * q + u;
-      if (row < n) {
-        const unsigned long long k = __ldg(keys + row);
-        uint32_t h = dict_hash(k) & (kDictSlots - 1);
-        while (t[h] != k) h = (h + 1) & (kDictSlots - 1);
-        out |= static_cast<uint32_t>(im[h]) << (8 * u);
-      }
-    }
     if (4 * q + 3 < n) {
+      const uint2 sl = *reinterpret_cast<const uint2*>(lslot + 4 * q);
+      const uint32_t s4[4] = {sl.x & 0xFFFFu, sl.x >> 16, sl.y & 0xFFFFu, sl.y >> 16};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out |= static_cast<uint32_t>(s4[u] < kDictLocal ? __ldg(xl + s4[u]) : 0u) << (8 * u);
       reinterpret_cast<uint32_t*>(ids)[q] = out;
     } else {
-      for (int u = 0; u < 4 && 4 * q + u < n; ++u) ids[4 * q + u] = static_cast<uint8_t>(out >> (8 * u));
+      for (uint32_t r = 4 * q; r < n; ++r) {
+        const uint32_t sl = lslot[r];
+        ids[r] = sl < kDictLocal ? __ldg(xl + sl) : 0u;
+      }
     }
   }
+}
+
+__global__ void l0_hd_ids_kernel(uint32_t count, const uint32_t* __restrict__ hd_rows,
+                                 const unsigned long long* __restrict__ hdkey,
+                                 const unsigned long long* __restrict__ gtab, const uint8_t* __restrict__ idmap,
+                                 const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
+  if (flags[0]) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    ids[hd_rows[i]] = idmap[dict_lookup(gtab, hdkey[i])];
 }
 
 // Entry ids of every tile's halo rows, laid out like the halo list (tile t at
@@ -1198,6 +1250,7 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
                                                           uint32_t period_rows, const uint8_t* __restrict__ ids,
                                                           const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids) {
   if (flags[0]) return;
+  constexpr uint32_t kPer = kTpHaloCap / 32;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
@@ -1205,8 +1258,15 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     const uint32_t shift = period ? (t / period) * period_rows : 0u;
     const uint4 m = __ldg(tmeta + pt);
     if (m.w & kTpSlow) continue;
-    for (uint32_t k = lane; k < m.w; k += 32)
-      hids[static_cast<size_t>(t) * kTpHaloCap + k] = __ldg(ids + shift + __ldg(halo + m.y + k));
+    uint32_t hv[kPer];
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) hv[u] = lane + 32 * u < m.w ? __ldg(halo + m.y + lane + 32 * u) : 0u;
+    uint32_t iv[kPer];
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) iv[u] = lane + 32 * u < m.w ? __ldg(ids + shift + hv[u]) : 0u;
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u)
+      if (lane + 32 * u < m.w) hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
   }
 }
 
@@ -1512,9 +1572,16 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2) return false;
   const uint32_t n = g->n;
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
-  if (g->l0_key.n < n) g->l0_key.alloc(n);
+  const unsigned sms = static_cast<unsigned>(num_sms());
+  const unsigned key_ctas = blocks_for((n + kL0KeyRows - 1) / kL0KeyRows, 256, sms * 8);
+  if (g->l0_slot.n < n) g->l0_slot.alloc(n);
   if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
   if (g->l0_hid.n < static_cast<size_t>(ntiles) * kTpHaloCap) g->l0_hid.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
+  if (g->l0_ctab.n < static_cast<size_t>(key_ctas) * kDictLocal) {
+    g->l0_ctab.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
+    g->l0_xlat.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
+  }
+  if (g->l0_key.n < std::max<uint32_t>(g->num_hd, 1u)) g->l0_key.alloc(std::max<uint32_t>(g->num_hd, 1u));
   if (!g->l0_dict.p) {
     g->l0_dict.alloc(kDictSlots);
     g->l0_idmap.alloc(kDictSlots);
@@ -1522,7 +1589,6 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
     g->l0_table.zero();
     g->l0_flags.alloc(2);
   }
-  const unsigned sms = static_cast<unsigned>(num_sms());
   const uint32_t* feat = reinterpret_cast<const uint32_t*>(g->feat.p);
   {
     ProfScope ps("l0_keys");
@@ -1531,14 +1597,19 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
     if (g->num_hd)
       GROOT_LAUNCH(hd_key_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd, g->rp.p,
                    g->col.p, feat, g->l0_key.p, g->l0_dict.p, g->l0_flags.p);
-    GROOT_LAUNCH(l0_key_kernel, blocks_for(n, 256, sms * 8), 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold,
-                 g->l0_key.p, g->l0_dict.p, g->l0_flags.p);
+    GROOT_LAUNCH(l0_key_kernel, key_ctas, 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold, g->l0_slot.p,
+                 g->l0_ctab.p, g->l0_dict.p, g->l0_flags.p);
     GROOT_LAUNCH(dict_finalize_kernel, 1, 1024, 0, g->l0_dict.p, g->l0_flags.p, *reinterpret_cast<const Layer0W*>(m->l0w),
                  g->l0_table.p, g->l0_idmap.p);
-    GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, g->l0_key.p, g->l0_dict.p,
-                 g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
-    GROOT_LAUNCH(l0_halo_ids_kernel, blocks_for(ntiles * 32ull, 256, sms * 8), 256, 0, ntiles,
-                 reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_halo.p, g->tp_period, g->tp_period_rows,
+    GROOT_LAUNCH(l0_xlat_kernel, blocks_for(key_ctas * kDictLocal, 256), 256, 0, key_ctas, g->l0_ctab.p, g->l0_dict.p,
+                 g->l0_idmap.p, g->l0_flags.p, g->l0_xlat.p);
+    GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, key_ctas * 8u, g->l0_slot.p,
+                 g->l0_xlat.p, g->l0_flags.p, g->l0_id.p);
+    if (g->num_hd)
+      GROOT_LAUNCH(l0_hd_ids_kernel, blocks_for(g->num_hd, 256), 256, 0, g->num_hd, g->hd_rows.p, g->l0_key.p,
+                   g->l0_dict.p, g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
+    GROOT_LAUNCH(l0_halo_ids_kernel, blocks_for(ntiles * 32ull, 256, sms * 16), 256, 0,
+                 ntiles, reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_halo.p, g->tp_period, g->tp_period_rows,
                  g->l0_id.p, g->l0_flags.p, g->l0_hid.p);
   }
   if (g->l0_mode == 0) {
