@@ -8,6 +8,7 @@ shape, and for the fused layer the top SASS lines by warp-stall samples.
 """
 import json
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -17,16 +18,13 @@ UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def short_name(k):
-    if "sage_tile_kernel" in k:  # template modes: 0 layer, 1 last layer, 2 standalone SpMM
-        if "<1>" in k or "ILi1E" in k:
-            return "sage_layer_tc_last"
-        if "<2>" in k or "ILi2E" in k:
-            return "spmm_mean32"
-        return "sage_layer_tc"
+    m = re.search(r"sage_tile_kernel<(\d)(?:, (true|false))?>", k) or re.search(r"sage_tile_kernelILi(\d)E(?:Lb(\d)E)?", k)
+    if m:  # template modes: 0 layer, 1 last layer, 2 standalone SpMM; keyed (entry-table input) variants
+        mode, keyed = m.group(1), m.group(2) in ("true", "1")
+        base = {"0": "sage_layer_tc", "1": "sage_layer_tc_last", "2": "spmm_mean32"}[mode]
+        return base + ("_keyed" if keyed and mode == "0" else "")
     if "tile_plan_kernel" in k:
         return "tile_plan"
-    if "sage_layer_tc_kernel" in k:
-        return "sage_layer_tc_last" if ("(bool)1" in k or "<true>" in k or "<1>" in k) else "sage_layer_tc"
     for key in ("sage_layer0", "hd_mean_feat", "hd_mean32", "confusion", "spmm_mean32", "spmm_generic", "naive_layer"):
         if key in k:
             return key

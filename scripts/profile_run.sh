@@ -12,7 +12,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 \
    > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sage_tile|sage_layer0|hd_mean|confusion|tile_plan" -s 0 -c 10 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sage_tile|sage_layer0|hd_mean|confusion|tile_plan|l0_key|l0_halo" -s 0 -c 12 \
    -o gpurun_out/prof_$TAG -f python scripts/probe_perf.py 1024 16 > gpurun_out/ncu_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sage_tile|hd_mean32" -s 2 -c 2 \
    -o gpurun_out/prof_spmm_$TAG -f python scripts/probe_spmm.py 1024 16 > gpurun_out/ncu_spmm_$TAG.log 2>&1
