@@ -1343,25 +1343,62 @@ __global__ void head_kernel(uint32_t n, const float* __restrict__ h, const float
   }
 }
 
-// confusion[truth][pred] (finish_prediction, src/gnn.cpp:268-276): block
-// histogram with warp-aggregated shared atomics, one global add per bin.
+// confusion[truth][pred] (finish_prediction, src/gnn.cpp:268-276): 16 rows
+// per thread and iteration (128-bit loads of classes and labels). Per truth
+// class t a register holds five 6-bit counters (prediction p at bits 6p), so a
+// row costs a shift and five predicated adds; every 48 rows they are flushed
+// into 25 u32 totals, then warp-, block- and grid-reduced.
 __global__ void __launch_bounds__(256) confusion_kernel(uint32_t n, const uint8_t* __restrict__ cls,
                                                         const uint8_t* __restrict__ labels,
                                                         unsigned long long* __restrict__ conf) {
   __shared__ uint32_t h[25];
   if (threadIdx.x < 25) h[threadIdx.x] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
-    const uint32_t i = base + lane;
-    uint32_t key = 0xFFFFFFFFu;
-    if (i < n) {
-      const uint32_t p = cls[i], t = labels[i];
-      if (p < 5 && t < 5) key = t * 5 + p;
+  uint32_t tot[25], acc[5];
+#pragma unroll
+  for (int k = 0; k < 25; ++k) tot[k] = 0;
+#pragma unroll
+  for (int r = 0; r < 5; ++r) acc[r] = 0;
+  auto count = [&](uint32_t p, uint32_t t) {
+    const uint32_t inc = p < 5 ? 1u << (6 * p) : 0u;
+#pragma unroll
+    for (uint32_t r = 0; r < 5; ++r) acc[r] += t == r ? inc : 0u;
+  };
+  auto flush = [&]() {
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+#pragma unroll
+      for (int q = 0; q < 5; ++q) tot[5 * r + q] += (acc[r] >> (6 * q)) & 63u;
+      acc[r] = 0;
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    if (key != 0xFFFFFFFFu && (__ffs(peers) - 1) == lane) atomicAdd(&h[key], __popc(peers));
+  };
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(cls) | reinterpret_cast<uintptr_t>(labels)) & 15u) == 0;
+  const uint32_t vecs = aligned ? n / 16 : 0u;  // caller buffers may be unaligned: scalar path
+  uint32_t since = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < vecs; v += stride) {
+    const uint4 pc = __ldg(reinterpret_cast<const uint4*>(cls) + v);
+    const uint4 tl = __ldg(reinterpret_cast<const uint4*>(labels) + v);
+    const uint32_t pw[4] = {pc.x, pc.y, pc.z, pc.w}, tw[4] = {tl.x, tl.y, tl.z, tl.w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) count((pw[w] >> (8 * b)) & 0xFFu, (tw[w] >> (8 * b)) & 0xFFu);
+    if (++since == 3) {  // 48 rows < 64: no 6-bit counter overflows
+      flush();
+      since = 0;
+    }
+  }
+  flush();
+  for (uint32_t i = vecs * 16 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    count(cls[i], labels[i]);
+    flush();
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < 25; ++k) {
+    uint32_t c = tot[k];
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&h[k], c);
   }
   __syncthreads();
   if (threadIdx.x < 25 && h[threadIdx.x]) atomicAdd(&conf[threadIdx.x], static_cast<unsigned long long>(h[threadIdx.x]));
@@ -1719,7 +1756,7 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
                  cls, logits, 0, ~0u, true, keyed);
   if (confusion) {
     ProfScope ps("confusion");
-    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
+    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n / 16 + 1, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
                  g->labels.p, confusion);
   }
 }
@@ -1781,7 +1818,7 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   }
   if (confusion) {
     ProfScope ps("confusion");
-    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
+    GROOT_LAUNCH(confusion_kernel, blocks_for(g->n / 16 + 1, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
                  g->labels.p, confusion);
   }
 }
