@@ -1,4 +1,5 @@
-"""Small end-to-end pass over every device kernel family, for compute-sanitizer
+"""Small end-to-end pass over every device kernel family (keyed layer 0 by default;
+GROOT_L0_KEYED=0 for the materialized one), for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck):
 
     compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
@@ -24,5 +25,6 @@ for maker, w, b in ((api.gen_csa_multiplier, 16, 3), (api.gen_booth_multiplier, 
     api.predict(prm_model, g, parts)
     sub = api.materialize(g, parts, 1)
     api.forward(prm_model, sub)
+    api.classify_aig(prm_model, c.aig, c.labels, 3)  # tile-aligned batch, periodic plan, split last layer
     print(maker.__name__, w, b, "n", g.n, "acc", round(pred.accuracy, 4), "finite", bool(np.isfinite(lg).all()))
 print("sanitize smoke done")
