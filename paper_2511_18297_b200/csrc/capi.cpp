@@ -971,8 +971,10 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
       if (g != g1) delete g;
       throw;
     }
+    const auto t5 = now();
     if (g != g1) delete g;
     delete g1;
+    if (host_timing) std::fprintf(stderr, "[classify_aig] total %.2f ms, release %.2f ms\n", ms(t0, now()), ms(t5, now()));
   });
 }
 

@@ -1763,9 +1763,9 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
 
 // Forward + classify of a tile-aligned batch (batch_padded: copy k at rows
 // k*P .. k*P + n1) with the class read-back overlapped: the last layer runs
-// as two launches over the two halves of the tiles, and the classes of the
-// copies the first half completes go to the host on a side stream while the
-// second half computes. labels_out is in the reference's numbering (k*n1 + v).
+// as kReadbackParts launches over consecutive tile ranges, and the classes of
+// the copies each range completes go to the host on a side stream while the
+// next range computes. labels_out is in the reference's numbering (k*n1 + v).
 void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls, unsigned long long* confusion,
                               uint32_t copies, uint32_t n1, uint32_t P, uint8_t* labels_out) {
   require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
@@ -1791,24 +1791,32 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
     GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return e;
   }();
+  // the last layer in kReadbackParts tile ranges: the classes of the copies a
+  // range completes go to the host on the side stream while the next computes
+  constexpr uint32_t kReadbackParts = 4;
   uint32_t k1 = 0;
   if (D == 1) {
     layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true, false);
   } else {
     const float* hin = g->act[(D - 2) & 1].p;
-    const uint32_t ntiles = (g->n + kTileM - 1) / kTileM, half = ntiles / 2;
-    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, 0, half, true, keyed);
-    const uint64_t rows_done = static_cast<uint64_t>(half) * kTileM;
-    while (k1 < copies && static_cast<uint64_t>(k1) * P + n1 <= rows_done) ++k1;
-    if (labels_out && k1) {
-      GROOT_CUDA(cudaEventRecord(ev_half, stream()));
-      GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
-      for (uint32_t k = 0; k < k1; ++k)
-        GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
-                                   cudaMemcpyDeviceToHost, side));
-      GROOT_CUDA(cudaEventRecord(ev_side, side));
+    const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
+    for (uint32_t part = 0; part < kReadbackParts; ++part) {
+      const uint32_t tb = static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * part / kReadbackParts);
+      const uint32_t te = part + 1 == kReadbackParts ? ~0u : static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * (part + 1) / kReadbackParts);
+      layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, tb, te, part == 0, keyed);
+      if (part + 1 == kReadbackParts || !labels_out) continue;
+      const uint64_t rows_done = static_cast<uint64_t>(te) * kTileM;
+      const uint32_t k0 = k1;
+      while (k1 < copies && static_cast<uint64_t>(k1) * P + n1 <= rows_done) ++k1;
+      if (k1 > k0) {
+        GROOT_CUDA(cudaEventRecord(ev_half, stream()));
+        GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
+        for (uint32_t k = k0; k < k1; ++k)
+          GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
+                                     cudaMemcpyDeviceToHost, side));
+      }
     }
-    layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, half, ~0u, false, keyed);
+    if (k1) GROOT_CUDA(cudaEventRecord(ev_side, side));
   }
   if (labels_out) {
     for (uint32_t k = k1; k < copies; ++k)

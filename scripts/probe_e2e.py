@@ -21,8 +21,11 @@ lab = torch.from_numpy(np.ascontiguousarray(c.labels)).pin_memory()
 pred = torch.empty(16 * (c.labels.shape[0]), dtype=torch.uint8).pin_memory()
 conf = (C.c_uint64 * 25)()
 acc = C.c_double()
+import time
 for _ in range(reps):
+    t0 = time.perf_counter()
     check(lib().groot_classify_aig(model.handle, c.aig.num_inputs, c.aig.num_ands, C.c_void_p(ands.data_ptr()),
                                    int(outs.numel()), C.c_void_p(outs.data_ptr()), C.c_void_p(lab.data_ptr()), 16,
                                    C.c_void_p(pred.data_ptr()), conf, C.byref(acc)))
+    print(f"call {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
 print("accuracy", acc.value)
