@@ -176,7 +176,7 @@ constexpr bool kTraceOn = true;
 constexpr bool kTraceOn = false;
 #endif
 __device__ __forceinline__ void tstamp(unsigned long long* tr, uint32_t it, int k) {
-  if (kTraceOn && tr && blockIdx.x == 0 && it < 64) tr[it * 16 + k] = clock64();
+  if (kTraceOn && tr && blockIdx.x == 0 && it < 60) tr[it * 16 + k] = clock64();
 }
 
 // ---------------------------------------------------------------------------
@@ -193,9 +193,7 @@ __device__ __forceinline__ void tstamp(unsigned long long* tr, uint32_t it, int 
 // are. Their accumulators are swapped back once per row.
 // ---------------------------------------------------------------------------
 enum TileMode { kModeLayer = 0, kModeLast = 1, kModeSpmm = 2 };
-constexpr int kTkRowStages = 4;
 constexpr int kTkMetaStages = 8;
-constexpr int kTkMetaLead = kTkMetaStages - kTkRowStages;
 constexpr uint32_t kCopiersMma = 2;   // warps 14, 15
 constexpr uint32_t kCopiersSpmm = 2;  // warps 14, 15 (7 copiers measured no faster)
 constexpr uint32_t kTkRowBytes = (kTpRows + kTpHaloCap) * 128u;
@@ -211,15 +209,29 @@ constexpr uint32_t kTkMetaBytes = ((kTkHidOff + kTpHaloCap + 127u) / 128u) * 128
 constexpr uint32_t kTileRing = 32;     // tile ids of the CTA's iterations (dynamic scheduler)
 constexpr uint32_t kEndTile = 0xFFFFFFFFu;
 constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8)
-constexpr uint32_t kTkSmemBytes = kTkRowStages * kTkRowBytes + kTkMetaStages * kTkMetaBytes + kTkTableRows * 128 + kBBytes +
-                                  (256 + 32 + kTileRing) * 4 +
-                                  16 * kTkMetaStages + 8 * (2 * kStages + 4 + 2 * kTkRowStages + 2 * kTkMetaStages) +
-                                  16 + 1024;
+#ifndef GROOT_ROW_STAGES
+#define GROOT_ROW_STAGES 4
+#endif
+// Shared-memory plan per variant: staged-row kernels spend it on the row ring,
+// keyed kernels stage no rows (their ring only sequences the copiers' slot
+// rewrite) and hold the entry table. (5 row stages fit only with the plan lead
+// cut to 3 tiles: measured 2 % slower.)
+template <bool kKeyed>
+struct TkCfg {
+  static constexpr int kRowStages = kKeyed ? 4 : GROOT_ROW_STAGES;
+  static constexpr int kMetaLead = kTkMetaStages - kRowStages;
+  static constexpr uint32_t kRowMem = kKeyed ? 0u : kRowStages * kTkRowBytes;
+  static constexpr uint32_t kTableMem = kKeyed ? kTkTableRows * 128u : 0u;
+  static constexpr uint32_t kSmem = kRowMem + kTkMetaStages * kTkMetaBytes + kTableMem + kBBytes +
+                                    (256 + 32 + kTileRing) * 4 + 16 * kTkMetaStages +
+                                    8 * (2 * kStages + 4 + 2 * kRowStages + 2 * kTkMetaStages) + 16 + 1024;
+  static_assert(kSmem <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
+  static_assert(kMetaLead >= 2, "plan records lead the rows");
+};
 static_assert(kTkRowBytes % 1024 == 0, "row stages keep 1024-B alignment");
 static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0 && kTkKidOff % 16 == 0 && kTkHidOff % 16 == 0 &&
                   kTpHaloCap % 16 == 0,
               "bulk-copy destinations and keyed halo-id sources must be 16-B aligned");
-static_assert(kTkSmemBytes <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
 
 __device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const float4& x1) {
   m[0] = ptx::fadd2(m[0], make_float2(x0.x, x0.y));
@@ -243,10 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   constexpr bool kMma = kMode != kModeSpmm;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows
-  uint8_t* sPlan = sRows + kTkRowStages * kTkRowBytes;   // [kTkMetaStages] lrp | lcol | halo list
+  using Cfg = TkCfg<kKeyed>;
+  constexpr int kTkRowStages = Cfg::kRowStages;
+  constexpr int kTkMetaLead = Cfg::kMetaLead;
+  uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows (none when keyed)
+  uint8_t* sPlan = sRows + Cfg::kRowMem;                 // [kTkMetaStages] lrp | lcol | halo list
   uint8_t* sTable = sPlan + kTkMetaStages * kTkMetaBytes;  // keyed layer 1: entry rows
-  uint8_t* sB = sTable + kTkTableRows * 128;
+  uint8_t* sB = sTable + Cfg::kTableMem;
   float* sInv = reinterpret_cast<float*>(sB + kBBytes);  // 1/d, d < 256
   float* sBias = sInv + 256;                              // layer bias by output feature
   uint32_t* sTile = reinterpret_cast<uint32_t*>(sBias + 32);  // [kTileRing] tile of iteration i (kEndTile: done)
@@ -511,12 +526,15 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     const uint32_t li = lbase + (lane >> 2);  // tile rows li and li + 8
     const uint32_t thr = a.hd.threshold;
     const float* hin_j = a.hin + 8 * j;
+    unsigned long long wt0 = 0, wt1 = 0, wt2 = 0, wt3 = 0;
+    unsigned long long acc_rows = 0, acc_gather = 0, acc_wait = 0, acc_store = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
       unsigned long long* tr = (warp == kEpiWarps && lane == 0) ? a.trace : nullptr;
       unsigned long long* tr7 = (warp == kEpiWarps + 3 && lane == 0) ? a.trace : nullptr;
       tstamp(tr, it, 3);
       tstamp(tr7, it, 13);
+      if (kTraceOn) wt0 = clock64();
       ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
       const uint32_t t = sTile[it % kTileRing];
       if (t == kEndTile) {  // hand the MMA an empty stage so it sees the end too
@@ -525,11 +543,19 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           ptx::mbar_arrive(&full[s]);
         }
+        if (kTraceOn && a.trace && blockIdx.x == 0 && lane == 0) {  // per-warp totals: trace rows 60..61
+          unsigned long long* tw = a.trace + 60 * 16 + (warp - kEpiWarps) * 4;
+          tw[0] = acc_rows;
+          tw[1] = acc_gather;
+          tw[2] = acc_wait;
+          tw[3] = acc_store;
+        }
         break;
       }
       const uint32_t row0 = t * kTileM;
       ptx::mbar_wait(&r_full[rs], (it / kTkRowStages) & 1);
       tstamp(tr, it, 4);
+      if (kTraceOn) wt1 = clock64();
       const uint8_t* st = sRows + rs * kTkRowBytes;
       const uint8_t* sp = sPlan + ms * kTkMetaBytes;
       // neighbour rows: staged rows, or (keyed) entry rows: the copiers have
@@ -610,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       }
       tstamp(tr, it, 5);
       tstamp(tr7, it, 14);
+      if (kTraceOn) wt2 = clock64();
       ptx::mbar_arrive(&r_empty[rs]);
       ptx::mbar_arrive(&m_empty[ms]);
 #pragma unroll
@@ -639,6 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const uint32_t s = it % kStages, ph = (it / kStages) & 1;
         ptx::mbar_wait(&empty[s], ph ^ 1);
         tstamp(tr, it, 6);
+        if (kTraceOn) wt3 = clock64();
         ptx::tc_fence_after();
         const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
         tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
@@ -647,6 +675,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         ptx::tc_fence_before();
         ptx::mbar_arrive(&full[s]);
         tstamp(tr, it, 7);
+        if (kTraceOn) {
+          const unsigned long long wt4 = clock64();
+          acc_rows += wt1 - wt0;
+          acc_gather += wt2 - wt1;
+          acc_wait += wt3 - wt2;
+          acc_store += wt4 - wt3;
+        }
         tstamp(tr7, it, 15);
       }
     }
@@ -1569,11 +1604,12 @@ static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) 
 static void set_tc_smem() {
   static bool done = false;
   if (done) return;
-  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
-  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTkSmemBytes));
+  constexpr uint32_t kS0 = TkCfg<false>::kSmem, kS1 = TkCfg<true>::kSmem;
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
   done = true;
 }
 
@@ -1715,15 +1751,15 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   if (l + 1 == m->depth) {
     ProfScope ps("sage_layer_tc_last");
     if (keyed_in)
-      GROOT_LAUNCH((sage_tile_kernel<kModeLast, true>), grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+      GROOT_LAUNCH((sage_tile_kernel<kModeLast, true>), grid, kThreads, TkCfg<true>::kSmem, a, hw, tmap_in);
     else
-      GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+      GROOT_LAUNCH(sage_tile_kernel<kModeLast>, grid, kThreads, TkCfg<false>::kSmem, a, hw, tmap_in);
   } else {
     ProfScope ps(keyed_in ? "sage_layer_tc_keyed" : "sage_layer_tc");
     if (keyed_in)
-      GROOT_LAUNCH((sage_tile_kernel<kModeLayer, true>), grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+      GROOT_LAUNCH((sage_tile_kernel<kModeLayer, true>), grid, kThreads, TkCfg<true>::kSmem, a, hw, tmap_in);
     else
-      GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, kTkSmemBytes, a, hw, tmap_in);
+      GROOT_LAUNCH(sage_tile_kernel<kModeLayer>, grid, kThreads, TkCfg<false>::kSmem, a, hw, tmap_in);
   }
   if (a.trace) {
     std::vector<unsigned long long> h(64 * 16);
@@ -1874,7 +1910,7 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
     const CUtensorMap tmap_in = make_rows32_tmap(const_cast<float*>(dense), g->n, kTileM);
     const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
     HeadW hw{};
-    GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, kTkSmemBytes, a, hw, tmap_in);
+    GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, TkCfg<false>::kSmem, a, hw, tmap_in);
   } else {
     GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
                  nullptr, dense, f, out);

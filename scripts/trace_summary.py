@@ -15,8 +15,20 @@ import sys
 import numpy as np
 
 
+def warp_totals(t):
+    # rows 60..61: per producer warp (4..11) totals over CTA 0's tiles: wait rows, gather, wait A, split+store
+    w = t[60:62].reshape(-1)[:32].reshape(8, 4)
+    if w.sum() <= 0:
+        return
+    print("per-warp totals (Mcycles): warp  wait-rows  gather  wait-A  split+store")
+    for i in range(8):
+        print(f"  {i + 4:2d}  " + "  ".join(f"{x / 1e6:8.3f}" for x in w[i]))
+
+
 def main(path):
     t = np.loadtxt(path, dtype=np.float64)
+    warp_totals(t)
+    t = t[:60]
     t = t[(t[:, 3] > 0) & (t[:, 7] > 0)]
     if len(t) < 6:
         print("trace: too few tiles")
