@@ -216,15 +216,23 @@ constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8
 // keyed kernels stage no rows (their ring only sequences the copiers' slot
 // rewrite) and hold the entry table. (5 row stages fit only with the plan lead
 // cut to 3 tiles: measured 2 % slower.)
+#ifndef GROOT_KEYED_META
+#define GROOT_KEYED_META 8
+#endif
+#ifndef GROOT_KEYED_ROWS
+#define GROOT_KEYED_ROWS 4
+#endif
 template <bool kKeyed>
 struct TkCfg {
-  static constexpr int kRowStages = kKeyed ? 4 : GROOT_ROW_STAGES;
-  static constexpr int kMetaLead = kTkMetaStages - kRowStages;
+  static constexpr int kRowStages = kKeyed ? GROOT_KEYED_ROWS : GROOT_ROW_STAGES;
+  static constexpr int kMetaStages = kKeyed ? GROOT_KEYED_META : kTkMetaStages;  // keyed: deeper plan ring
+  static constexpr int kMetaLead = kMetaStages - kRowStages;
   static constexpr uint32_t kRowMem = kKeyed ? 0u : kRowStages * kTkRowBytes;
   static constexpr uint32_t kTableMem = kKeyed ? kTkTableRows * 128u : 0u;
-  static constexpr uint32_t kSmem = kRowMem + kTkMetaStages * kTkMetaBytes + kTableMem + kBBytes +
-                                    (256 + 32 + kTileRing) * 4 + 16 * kTkMetaStages +
-                                    8 * (2 * kStages + 4 + 2 * kRowStages + 2 * kTkMetaStages) + 16 + 1024;
+  static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes +
+                                    (256 + 32 + kTileRing) * 4 + 16 * kMetaStages +
+                                    8 * (2 * kStages + 4 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
+  static_assert(kMetaLead + kRowStages + kStages + 4 < static_cast<int>(kTileRing), "tile ring covers every role's lag");
   static_assert(kSmem <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
   static_assert(kMetaLead >= 2, "plan records lead the rows");
 };
@@ -256,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
   using Cfg = TkCfg<kKeyed>;
+  constexpr int kTkMetaStages = Cfg::kMetaStages;
   constexpr int kTkRowStages = Cfg::kRowStages;
   constexpr int kTkMetaLead = Cfg::kMetaLead;
   uint8_t* sRows = smem;                                 // [kTkRowStages] tile + halo rows (none when keyed)
