@@ -163,6 +163,7 @@ struct LayerArgs {
   uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
+  const float* ktable_self;   // kModeXform: Ts (entry rows . W_self)
   const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused; tiles x 128), see l0_key_kernel
   const uint8_t* hids;        //                entry ids of the halo rows (tiles x kTpHaloCap, as the halo list)
   const float* ktable;        //                kTkTableRows x 32 rows of the entries
@@ -192,7 +193,12 @@ __device__ __forceinline__ void tstamp(unsigned long long* tr, uint32_t it, int 
 // always touch disjoint banks (even vs odd 16-B chunks) whatever the rows
 // are. Their accumulators are swapped back once per row.
 // ---------------------------------------------------------------------------
-enum TileMode { kModeLayer = 0, kModeLast = 1, kModeSpmm = 2 };
+// kModeXform (keyed layer 1 of a model with more layers): transform first.
+// mean(H1[N(v)]) . Wn = mean over u of (table[id_u] . Wn), so with the entry
+// table transformed once (Tn = table . Wn, Ts = table . Ws; <= 255 rows) the
+// layer is a gather-sum of 32-wide rows: relu(Ts[id_v] + mean Tn[id_u] + b),
+// stored by the producers as in SpMM mode -- no tensor-core pass.
+enum TileMode { kModeLayer = 0, kModeLast = 1, kModeSpmm = 2, kModeXform = 3 };
 constexpr int kTkMetaStages = 8;
 constexpr uint32_t kCopiersMma = 2;   // warps 14, 15
 constexpr uint32_t kCopiersSpmm = 2;  // warps 14, 15 (7 copiers measured no faster)
@@ -228,7 +234,7 @@ struct TkCfg {
   static constexpr int kMetaStages = kKeyed ? GROOT_KEYED_META : kTkMetaStages;  // keyed: deeper plan ring
   static constexpr int kMetaLead = kMetaStages - kRowStages;
   static constexpr uint32_t kRowMem = kKeyed ? 0u : kRowStages * kTkRowBytes;
-  static constexpr uint32_t kTableMem = kKeyed ? kTkTableRows * 128u : 0u;
+  static constexpr uint32_t kTableMem = kKeyed ? 2u * kTkTableRows * 128u : 0u;  // entry rows (Tn) | Ts
   static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes +
                                     (256 + 32 + kTileRing) * 4 + 16 * kMetaStages +
                                     8 * (2 * kStages + 4 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
@@ -260,7 +266,9 @@ __device__ __forceinline__ void swap_halves(float2 (&m)[4], bool sw) {
 template <int kMode, bool kKeyed = false>
 __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
                                                                 const __grid_constant__ CUtensorMap tmap_in) {
-  constexpr bool kMma = kMode != kModeSpmm;
+  constexpr bool kMma = kMode == kModeLayer || kMode == kModeLast;
+  constexpr bool kXform = kMode == kModeXform;
+  static_assert(!kXform || kKeyed, "transform-first mode reads the entry tables");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_addr(smem_raw) & 1023u)) & 1023u);
   using Cfg = TkCfg<kKeyed>;
@@ -298,8 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   if (kKeyed)
     for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
       reinterpret_cast<uint4*>(sTable)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
+  if (kXform)
+    for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
+      reinterpret_cast<uint4*>(sTable + kTkTableRows * 128)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable_self) + i);
   for (uint32_t d = threadIdx.x; d < 256; d += kThreads) sInv[d] = d ? 1.0f / static_cast<float>(d) : 0.0f;
-  if (kMma) {
+  if (kMma || kXform) {
     for (uint32_t i = threadIdx.x; i < 32; i += kThreads) sBias[i] = hw.bias[i];
   }
   if (threadIdx.x == 0) {
@@ -633,10 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           }
       }
       float4 hs[2][2], mm[2][2];
-      if (kMma) {
+      if (kMma || kXform) {
+        const uint8_t* sself = kXform ? sTable + kTkTableRows * 128 : sTable;  // Ts, or the entry rows
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint8_t* rowp = kKeyed ? sTable + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
+          const uint8_t* rowp = kKeyed ? sself + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
           const float4 f0 = *reinterpret_cast<const float4*>(rowp + off0);
           const float4 f1 = *reinterpret_cast<const float4*>(rowp + off1);
           hs[h][0] = gp ? f1 : f0;
@@ -652,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       for (int h = 0; h < 2; ++h) {
         const uint32_t r = row0 + li + 8 * h;
         if (hd[h]) {
-          if (kMma) {
+          if (kMma || kXform) {
             const float* src = a.hd.mean + static_cast<size_t>(hd_slot(a.hd, r)) * kF + 8 * j;
             mm[h][0] = ptx::ldg_f4(src);
             mm[h][1] = ptx::ldg_f4(src + 4);
@@ -667,6 +679,15 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         }
         if (kMode == kModeSpmm) {
           if (r < n && !hd[h]) ptx::stg_f8(a.spmm_out + static_cast<size_t>(r) * kF + 8 * j, mm[h][0], mm[h][1]);
+        } else if (kXform) {
+          if (r < n) {
+            const float* bj = sBias + 8 * j;
+            const float4 o0 = make_float4(fmaxf((hs[h][0].x + mm[h][0].x) + bj[0], 0.f), fmaxf((hs[h][0].y + mm[h][0].y) + bj[1], 0.f),
+                                          fmaxf((hs[h][0].z + mm[h][0].z) + bj[2], 0.f), fmaxf((hs[h][0].w + mm[h][0].w) + bj[3], 0.f));
+            const float4 o1 = make_float4(fmaxf((hs[h][1].x + mm[h][1].x) + bj[4], 0.f), fmaxf((hs[h][1].y + mm[h][1].y) + bj[5], 0.f),
+                                          fmaxf((hs[h][1].z + mm[h][1].z) + bj[6], 0.f), fmaxf((hs[h][1].w + mm[h][1].w) + bj[7], 0.f));
+            ptx::stg_f8(a.hout + static_cast<size_t>(r) * kF + 8 * j, o0, o1);
+          }
         } else if (r >= n) {
           hs[h][0] = hs[h][1] = mm[h][0] = mm[h][1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -1314,6 +1335,19 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
   }
 }
 
+// kModeXform tables: Tn[k] = table[k] . W_neigh, Ts[k] = table[k] . W_self
+// (fp64 accumulation, rounded once), CTA per entry, thread per output.
+__global__ void __launch_bounds__(64) l1_xform_kernel(const float* __restrict__ table, const float* __restrict__ ws,
+                                                      const float* __restrict__ wn, const uint32_t* __restrict__ flags,
+                                                      float* __restrict__ tn, float* __restrict__ ts) {
+  const uint32_t k = blockIdx.x, o = threadIdx.x & 31;
+  if (flags[0] || k >= flags[1]) return;
+  const float* W = threadIdx.x < 32 ? wn : ws;
+  double acc = 0.0;
+  for (uint32_t i = 0; i < kF; ++i) acc = fma(static_cast<double>(table[k * kF + i]), static_cast<double>(W[i * kF + o]), acc);
+  (threadIdx.x < 32 ? tn : ts)[k * kF + o] = static_cast<float>(acc);
+}
+
 // General CSR SpMM (spmm::execute over CsrMatrix<float>): 8 lanes per row,
 // columns strided by 8, nonzeros accumulated in order. vals == nullptr -> 1/deg.
 __global__ void __launch_bounds__(256) spmm_generic_kernel(uint32_t rows, const uint32_t* __restrict__ rp,
@@ -1619,6 +1653,7 @@ static void set_tc_smem() {
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeSpmm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
+  GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeXform, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
   done = true;
 }
 
@@ -1729,15 +1764,28 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
     return;
   }
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
+  // keyed layer 1 with layers after it: transform first (kModeXform)
+  const char* xe = std::getenv("GROOT_L1_XFORM");
+  const bool xform = keyed_in && l + 1 < m->depth && !(xe && std::atoi(xe) == 0);
+  if (xform) {
+    if (!g->l0_xtab.p) g->l0_xtab.alloc(2ull * kTkTableRows * kF);
+    g->l0_xtab.zero();
+    const float* w1 = m->naive_w.p + (2 * m->in_dim * kF + kF);  // layer 1: W_self, W_neigh, b
+    ProfScope ps("l1_xform");
+    GROOT_LAUNCH(l1_xform_kernel, kTkTableRows, 64, 0, g->l0_table.p, w1, w1 + kF * kF, g->l0_flags.p, g->l0_xtab.p,
+                 g->l0_xtab.p + kTkTableRows * kF);
+  }
+  const float* hd_src = xform ? g->l0_xtab.p : hin;  // (xform: HD means of Tn rows)
   if (g->num_hd && hd_means) {
     ProfScope ps("hd_mean32");
-    hd_means32(g, hin, g->hd_mean.p, 0, keyed_in ? g->l0_id.p : nullptr);
+    hd_means32(g, hd_src, g->hd_mean.p, 0, keyed_in ? g->l0_id.p : nullptr);
   }
   LayerArgs a = plan_args(g, hin, hd);
   if (keyed_in) {
     a.keys = g->l0_id.p;
     a.hids = g->l0_hid.p;
-    a.ktable = g->l0_table.p;
+    a.ktable = xform ? g->l0_xtab.p : g->l0_table.p;
+    a.ktable_self = g->l0_xtab.p + kTkTableRows * kF;
   }
   a.tile_begin = std::min(tile_begin, ntiles);
   a.tile_end = std::min(tile_end, ntiles);
@@ -1757,7 +1805,10 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
     trace.zero();
     a.trace = trace.p;
   }
-  if (l + 1 == m->depth) {
+  if (xform) {
+    ProfScope ps("sage_layer1_xform");
+    GROOT_LAUNCH((sage_tile_kernel<kModeXform, true>), grid, kThreads, TkCfg<true>::kSmem, a, hw, tmap_in);
+  } else if (l + 1 == m->depth) {
     ProfScope ps("sage_layer_tc_last");
     if (keyed_in)
       GROOT_LAUNCH((sage_tile_kernel<kModeLast, true>), grid, kThreads, TkCfg<true>::kSmem, a, hw, tmap_in);
