@@ -22,7 +22,7 @@ def main(path, cmd):
     all_ms = sum(tot.values()) or 1.0
     print(f"# {cmd}")
     print("# per-kernel totals over the captured launches (cold-cache, serialised: compare SHARES, not absolutes)")
-    print("# forward step (keyed default) = l0 keys (hd_key, l0_key, dict_finalize, l0_xlat, l0_ids, l0_halo_ids) + 3x(hd_chunk + hd_reduce + sage_tile_kernel) [<0,1> keyed layer 1, <0,0> layer 2, <1,0> last] + confusion; sage_layer0 launches come from the materialized-layer-0 comparison run")
+    print("# forward step (keyed default) = l0 keys (hd_key, l0_key, dict_finalize, l0_xlat, l0_ids, l0_halo_ids) + l1_xform + 3x(hd_chunk + hd_reduce + sage_tile_kernel) [<3,1> keyed transform-first layer 1, <0,0> layer 2, <1,0> last] + confusion; sage_layer0 launches come from the materialized-layer-0 comparison run")
     for name, ms in tot.most_common():
         print(f"{name[:70]:70s} launches={cnt[name]:4d} total_ms={ms:9.3f} avg_ms={ms / cnt[name]:8.3f} "
               f"share={100 * ms / all_ms:5.1f}%")

@@ -21,7 +21,7 @@ def short_name(k):
     m = re.search(r"sage_tile_kernel<(\d)(?:, (true|false|0|1))?>", k) or re.search(r"sage_tile_kernelILi(\d)E(?:Lb(\d)E)?", k)
     if m:  # template modes: 0 layer, 1 last layer, 2 standalone SpMM; keyed (entry-table input) variants
         mode, keyed = m.group(1), m.group(2) in ("true", "1")
-        base = {"0": "sage_layer_tc", "1": "sage_layer_tc_last", "2": "spmm_mean32"}[mode]
+        base = {"0": "sage_layer_tc", "1": "sage_layer_tc_last", "2": "spmm_mean32", "3": "sage_layer1_xform"}[mode]
         return base + ("_keyed" if keyed and mode == "0" else "")
     if "tile_plan_kernel" in k:
         return "tile_plan"
