@@ -18,8 +18,12 @@
 //                 the last layer, the 32 -> classes head + first-max argmax)
 // The same kernel without the MMA is the standalone LD SpMM. High-degree rows
 // (the row classifier's HD band; the PIs of a multiplier) are aggregated first
-// by a CTA-per-row kernel with a fixed-order reduction. Layer 0 (4 -> 32,
-// inputs in {0,1}^4) is a gather + FFMA kernel.
+// in L2-ordered chunks with a fixed-order reduction (hd_chunk_kernel).
+// Layer 0 (4 -> 32, inputs in {0,1}^4) is keyed by default: per row an exact
+// integer record, a dictionary of the distinct records, their 4 -> 32 rows and
+// a u8 entry id per row (l0_key_kernel ...); layer 1 then reads entry ids
+// instead of layer-0 rows and, when more layers follow, runs transform-first
+// (kModeXform). Graphs that are not keyable use sage_layer0_kernel.
 #include <cub/cub.cuh>
 #include <cuda.h>
 
