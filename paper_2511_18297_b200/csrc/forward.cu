@@ -251,6 +251,17 @@ static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0 && kTkKidOff % 16 == 
                   kTpHaloCap % 16 == 0,
               "bulk-copy destinations and keyed halo-id sources must be 16-B aligned");
 
+#ifndef GROOT_XFORM_PAIR
+#define GROOT_XFORM_PAIR 1
+#endif
+#ifndef GROOT_MMA_PAIR
+#define GROOT_MMA_PAIR 1
+#endif
+#ifndef GROOT_PAIR_BATCH
+#define GROOT_PAIR_BATCH 4
+#endif
+constexpr uint32_t kPairBatch = GROOT_PAIR_BATCH;  // kModeXform: neighbours per row per batch, both rows together
+
 __device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const float4& x1) {
   m[0] = ptx::fadd2(m[0], make_float2(x0.x, x0.y));
   m[1] = ptx::fadd2(m[1], make_float2(x0.z, x0.w));
@@ -604,6 +615,34 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           hd[h] = (w0 & kTpHdBit) != 0;
           d[h] = hd[h] ? 0u : (w1 & 0x7FFFu) - lo[h];  // HD rows: mean from the HD kernel
         }
+        if ((kXform && GROOT_XFORM_PAIR) || (kMma && GROOT_MMA_PAIR)) {
+          // both rows' neighbour batches in flight at once (kXform holds no TMEM
+          // operands, so it affords kPairBatch = 4 neighbours per row)
+          constexpr uint32_t kPB = kXform ? kPairBatch : 2u;
+          const uint32_t dmax = d[0] > d[1] ? d[0] : d[1];
+          for (uint32_t k0 = 0; k0 < dmax; k0 += kPB) {
+            uint32_t loc[2][kPB];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (uint32_t u = 0; u < kPB; ++u) loc[h][u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
+            float4 x[2][kPB][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (uint32_t u = 0; u < kPB; ++u)
+                if (k0 + u < d[h]) {
+                  const uint8_t* rowp = rbase + loc[h][u] * 128u;
+                  x[h][u][0] = *reinterpret_cast<const float4*>(rowp + off0);
+                  x[h][u][1] = *reinterpret_cast<const float4*>(rowp + off1);
+                }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (uint32_t u = 0; u < kPB; ++u)
+                if (k0 + u < d[h]) acc_row(m[h], x[h][u][0], x[h][u][1]);
+          }
+        } else
         // rows one after the other (4 neighbour rows in flight per row keeps
         // the producers inside 128 registers)
 #pragma unroll
