@@ -333,6 +333,12 @@ def run_ours(args):
     mid = ld + 128 * n + 128 * n + 128 * num_hd
     last = ld + 128 * n + n + 128 * num_hd
     full_bytes = l0 + l1 + mid * (depth - 3) + last + 2 * n
+    k_x = kernels.get("sage_layer1_xform")
+    l1_roof = None
+    if k_x:  # keyed transform-first layer 1 (a gather-sum: no input rows, table in shared memory)
+        ach = l1 / (k_x["ms_per_launch"] * 1e-3) / 1e9
+        l1_roof = {"kernel": "sage_tile_kernel<kModeXform, true> (keyed transform-first layer 1)", "bound": "hbm",
+                   "algorithmic_bytes_per_launch": l1, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
 
     # standalone SpMM (mean aggregation, f=32): the metric's "SpMM HBM GB/s"
     dense = torch.randn(n, 32, device="cuda")
@@ -414,6 +420,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (whole batch copies per GPU)" if world > 1 else "single GPU",
                        "l2": "inputs (>40 GB resident) far exceed L2; no flush"},
             "roofline": roof,
+            "layer1_roofline": l1_roof,
             "materialized_layer0": {"ms_per_step": ms_mat, "value": E * world / (ms_mat * 1e-3), "unit": UNIT,
                                     "note": "same forward with GROOT_L0_KEYED=0 (layer-0 rows materialized)"},
             "forward_roofline": ({"algorithmic_bytes": full_bytes, "achieved_gbs": full_bytes / ms / 1e6,
