@@ -1843,7 +1843,8 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   std::memcpy(hw.bias, m->bias_h.data() + static_cast<size_t>(l - 1) * kF, sizeof(hw.bias));
   static const char* trace_path = std::getenv("GROOT_TRACE");
   DevBuf<unsigned long long> trace;
-  if (trace_path && l == 1) {
+  static const uint32_t trace_layer = env_u32("GROOT_TRACE_LAYER", 1);
+  if (trace_path && l == trace_layer) {
     trace.alloc(64 * 16);
     trace.zero();
     a.trace = trace.p;
