@@ -1730,6 +1730,9 @@ static void prepare_graph(const groot_model* m, groot_graph* g) {
 static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   const char* e = std::getenv("GROOT_L0_KEYED");
   if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2) return false;
+  // small graphs: the key passes' fixed launch cost exceeds the layer-0 rows they save
+  const char* mr = std::getenv("GROOT_L0_KEYED_MIN_ROWS");
+  if (g->n < (mr ? std::strtoull(mr, nullptr, 10) : (1ull << 20))) return false;
   const uint32_t n = g->n;
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   const unsigned sms = static_cast<unsigned>(num_sms());

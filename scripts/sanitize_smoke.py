@@ -12,6 +12,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_18297_b200 import api  # noqa: E402
 
+os.environ.setdefault("GROOT_L0_KEYED_MIN_ROWS", "0")  # key these small graphs too
+
 prm_model = api.init_model(7)
 for maker, w, b in ((api.gen_csa_multiplier, 16, 3), (api.gen_booth_multiplier, 12, 2), (api.gen_csa_multiplier, 160, 1)):
     c = maker(w)

@@ -31,6 +31,18 @@ def api():
     return A
 
 
+@pytest.fixture(autouse=True)
+def keyed_on_small_graphs():
+    """The library keys only graphs of >= 2^20 rows by default; these tests use small ones."""
+    old = os.environ.get("GROOT_L0_KEYED_MIN_ROWS")
+    os.environ["GROOT_L0_KEYED_MIN_ROWS"] = "0"
+    yield
+    if old is None:
+        del os.environ["GROOT_L0_KEYED_MIN_ROWS"]
+    else:
+        os.environ["GROOT_L0_KEYED_MIN_ROWS"] = old
+
+
 def profiled_names(fn):
     """Run fn with the library's per-kernel profiler on; return the scope names."""
     from paper_2511_18297_b200 import _lib
