@@ -257,6 +257,9 @@ static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0 && kTkKidOff % 16 == 
 #ifndef GROOT_MMA_PAIR
 #define GROOT_MMA_PAIR 1
 #endif
+#ifndef GROOT_MMA_PB
+#define GROOT_MMA_PB 2u
+#endif
 #ifndef GROOT_PAIR_BATCH
 #define GROOT_PAIR_BATCH 4
 #endif
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if ((kXform && GROOT_XFORM_PAIR) || (kMma && GROOT_MMA_PAIR)) {
           // both rows' neighbour batches in flight at once (kXform holds no TMEM
           // operands, so it affords kPairBatch = 4 neighbours per row)
-          constexpr uint32_t kPB = kXform ? kPairBatch : 2u;
+          constexpr uint32_t kPB = kXform ? kPairBatch : GROOT_MMA_PB;
           const uint32_t dmax = d[0] > d[1] ? d[0] : d[1];
           for (uint32_t k0 = 0; k0 < dmax; k0 += kPB) {
             uint32_t loc[2][kPB];
