@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         uint8_t* sp = sPlan + ms * kTkMetaBytes;
         sMeta[ms] = m;
         const bool slow = (m.w & kTpSlow) != 0;
-        const uint32_t hpad = slow ? 0u : (m.w + 3u) & ~3u;
+        const uint32_t hpad = (slow || kKeyed) ? 0u : (m.w + 3u) & ~3u;  // keyed: halo ids instead of rows
         const uint32_t kpad = kKeyed ? (slow ? 0u : (m.w + 15u) & ~15u) : 0u;
         ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u + (kKeyed ? kTpRows + kpad : 0u));
         if (kKeyed) {
