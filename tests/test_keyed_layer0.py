@@ -152,3 +152,52 @@ def test_keyed_fallback(api, case):
         plain = with_env("GROOT_L0_KEYED", "0", lambda: api.forward(model, g))
         np.testing.assert_array_equal(with_env("GROOT_L1_XFORM", "0", lambda: api.forward(model, g)), plain)
         assert rel_err(lg, plain.astype(np.float64)) <= 5e-6
+
+
+@pytest.mark.parametrize("cap", ["0", "64"])
+def test_keyed_slow_tiles(cap):
+    """Keyed + transform-first layers with the tile plan's fallback forced
+    (GROOT_TP_HALO_CAP): slow tiles gather entry rows from global memory."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+from paper_2511_18297_b200 import api
+from oracle import pyoracle as O
+c = api.gen_csa_multiplier(64); g = api.batch(api.encode(c.aig, c.labels), 2)
+h = O.batch(O.encode(O.gen_csa(64)), 2)
+for depth in (2, 4):
+    prm = O.init_model(3, depth=depth)
+    lg = api.forward(api.Model.from_params(prm, depth=depth), g)
+    ref = O.forward(h, prm, depth=depth)
+    err = (np.abs(lg - ref).max(1) / np.maximum(np.abs(ref).max(1), 1e-6)).max()
+    assert err <= 1e-5, (depth, err)
+print("ok")
+"""
+    env = dict(os.environ, GROOT_TP_HALO_CAP=cap, GROOT_L0_KEYED_MIN_ROWS="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("circuit,width,copies,depth", [("booth", 64, 2, 4), ("csa", 160, 1, 6)])
+def test_keyed_more_shapes(api, circuit, width, copies, depth):
+    """Booth (more record kinds) and a deep model (transform-first layer 1 then four tensor-core layers),
+    HD rows included (CSA 160: PI degree 160)."""
+    c = api.gen_csa_multiplier(width) if circuit == "csa" else api.gen_booth_multiplier(width)
+    g = api.encode(c.aig, c.labels)
+    if copies > 1:
+        g = api.batch(g, copies)
+    prm = O.init_model(13, depth=depth)
+    model = api.Model.from_params(prm, depth=depth)
+    lg, names = profiled_names(lambda: api.forward(model, g))
+    h = O.encode(O.Aig(c.aig.num_inputs, c.aig.and_lits, c.aig.out_lits, c.labels))
+    if copies > 1:
+        h = O.batch(h, copies)
+    ref = O.forward(h, prm, depth=depth)
+    assert rel_err(lg, ref) <= 1e-5
+    if "l0_keys" in names and "sage_layer0" not in names:
+        assert "sage_layer1_xform" in names
+    r1 = api.classify_aig(model, c.aig, c.labels, 3)
+    r0 = with_env("GROOT_L0_KEYED", "0", lambda: api.classify_aig(model, c.aig, c.labels, 3))
+    assert (r1.labels != r0.labels).sum() <= 3
