@@ -201,3 +201,17 @@ def test_keyed_more_shapes(api, circuit, width, copies, depth):
     r1 = api.classify_aig(model, c.aig, c.labels, 3)
     r0 = with_env("GROOT_L0_KEYED", "0", lambda: api.classify_aig(model, c.aig, c.labels, 3))
     assert (r1.labels != r0.labels).sum() <= 3
+
+
+def test_small_graphs_stay_materialized(api):
+    """Below GROOT_L0_KEYED_MIN_ROWS (default 2^20 rows) the key passes' launch cost
+    exceeds what they save: layer 0 is materialized."""
+    c = api.gen_csa_multiplier(16)
+    g = api.encode(c.aig, c.labels)
+    model = api.Model.from_params(O.init_model(2))
+    del os.environ["GROOT_L0_KEYED_MIN_ROWS"]  # the library default (restored by the fixture)
+    try:
+        _, names = profiled_names(lambda: api.forward(model, g))
+    finally:
+        os.environ["GROOT_L0_KEYED_MIN_ROWS"] = "0"
+    assert "sage_layer0" in names and "l0_keys" not in names, names
