@@ -147,6 +147,14 @@ int groot_footprint_proxy(const groot_parts* p, uint32_t feature_cols, uint32_t 
 /* materialize (src/partition.cpp:488-506): standalone EdaGraph of one part (K7). */
 int groot_materialize(const groot_graph* g, const groot_parts* p, uint32_t part,
                       groot_graph** out);
+/* The caller's vector<AugmentedPartition> (e.g. the predict(model, g, parts)
+ * argument, src/gnn.cpp:280-291) uploaded as it is: per part p the core
+ * nodes core_nodes[core_off[p] .. core_off[p+1]), the boundary nodes and the
+ * local edge pairs likewise (offsets: k+1 entries each, starting at 0).
+ * Validated: global ids < n, local endpoints < the part's size. */
+int groot_parts_from_host(uint32_t n, uint32_t k, const uint64_t* core_off, const uint32_t* core_nodes,
+                          const uint64_t* bnd_off, const uint32_t* boundary_nodes, const uint64_t* edge_off,
+                          const uint32_t* edges, groot_parts** out);
 void groot_parts_free(groot_parts* p);
 
 /* ---- model (src/gnn.cpp:113-138, 330-372) ------------------------------------
@@ -166,6 +174,15 @@ int groot_model_info(const groot_model* m, uint32_t* depth, uint32_t* in_dim, ui
                      uint32_t* classes);
 int groot_model_params(const groot_model* m, double* params);
 void groot_model_free(groot_model* m);
+
+/* ---- SageContext: make_context (src/gnn.cpp:140-170) --------------------------
+ * Everything the forward derives from the graph alone -- the row classifier
+ * (HD band of the degree-polarised split), the per-tile gather plan, the HD
+ * chunk plan and the activation buffers -- built on the device and cached on
+ * the graph handle (every forward entry point builds what is missing on first
+ * use; prepare builds it eagerly). release frees it; the next forward rebuilds. */
+int groot_graph_prepare(const groot_graph* g);
+int groot_graph_release_context(const groot_graph* g);
 
 /* ---- layer forward + classify ------------------------------------------------
  * forward (src/gnn.cpp:172-178): logits n x classes, fp32 on device (written to
@@ -223,9 +240,25 @@ int groot_build_plan(const groot_graph* g, uint32_t hd_threshold, uint32_t ld_th
 /* out = D^-1 A * dense (mean aggregation, spmm::execute with a_mean values),
  * dense/out f32 row-major on host, f in {4, 32} or any f <= 256. */
 int groot_spmm_mean(const groot_graph* g, const float* dense, uint32_t f, float* out);
-/* General CSR SpMM (spmm::execute over CsrMatrix<float>): host arrays. */
+/* spmm::execute over a host CsrMatrix<float> / CsrMatrix<double>
+ * (inc/spmm.hpp:106-181) on the device: nonzeros accumulated in order with
+ * separately rounded multiply and add; rows of degree >= hd_threshold summed
+ * as 32 chunk partials added in ascending order, as the HD band of a plan
+ * built with that threshold -- so the result is bitwise the reference's
+ * execute. hd_threshold 0: the plain row loop (reference_spmm,
+ * inc/spmm.hpp:183-195). values NULL -> 1/deg (a_mean). */
 int groot_spmm_csr(uint32_t rows, uint32_t cols, const uint64_t* row_ptr, const uint32_t* col_idx,
-                   const float* values, const float* dense, uint32_t f, float* out);
+                   const float* values, const float* dense, uint32_t f, uint32_t hd_threshold, float* out);
+int groot_spmm_csr_f64(uint32_t rows, uint32_t cols, const uint64_t* row_ptr, const uint32_t* col_idx,
+                       const double* values, const double* dense, uint32_t f, uint32_t hd_threshold, double* out);
+/* build_plan over a host row_ptr (build_plan(rows, span row_ptr, ...),
+ * src/spmm.cpp:37-127), same outputs as groot_build_plan. */
+int groot_build_plan_rows(uint32_t rows, const uint64_t* row_ptr, uint32_t hd_threshold, uint32_t ld_threshold,
+                          uint32_t nz_budget, uint64_t* counts, uint32_t* perm, uint32_t* hd_rows,
+                          uint32_t* mid_rows, uint32_t* ld_groups, uint64_t* units);
+/* degree_sort (src/spmm.cpp:9-35): stable ascending-by-degree permutation
+ * (perm[sorted] = original row) and the row pointers in that order (rows+1). */
+int groot_degree_sort(uint32_t rows, const uint64_t* row_ptr, uint32_t* perm, uint64_t* sorted_row_ptr);
 /* Device variant of the mean SpMM (bench / roofline): pointers on device. */
 int groot_spmm_mean_dev(const groot_graph* g, const float* dense_dev, uint32_t f, float* out_dev);
 

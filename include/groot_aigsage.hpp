@@ -17,15 +17,24 @@
 // Link: -I include -L paper_2511_18297_b200 -lgroot_b200
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <fstream>
+#include <functional>
 #include <iterator>
 #include <map>
 #include <memory>
+#include <random>
+#include <span>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -384,6 +393,28 @@ inline std::vector<AugmentedPartition> parts_from_device(const groot_parts* p) {
   return out;
 }
 
+// The caller's parts, uploaded as they are (groot_parts_from_host).
+inline gpu::DeviceParts parts_to_device(std::uint32_t n, const std::vector<AugmentedPartition>& parts) {
+  const std::uint32_t k = static_cast<std::uint32_t>(parts.size());
+  std::vector<std::uint64_t> co(k + 1, 0), bo(k + 1, 0), eo(k + 1, 0);
+  std::vector<std::uint32_t> core, bnd, edges;
+  for (std::uint32_t p = 0; p < k; ++p) {
+    const AugmentedPartition& a = parts[p];
+    core.insert(core.end(), a.core_nodes.begin(), a.core_nodes.end());
+    bnd.insert(bnd.end(), a.boundary_nodes.begin(), a.boundary_nodes.end());
+    for (const auto& [u, v] : a.edges) {
+      edges.push_back(u);
+      edges.push_back(v);
+    }
+    co[p + 1] = core.size();
+    bo[p + 1] = bnd.size();
+    eo[p + 1] = edges.size() / 2;
+  }
+  groot_parts* out = nullptr;
+  detail::check(groot_parts_from_host(n, k, co.data(), core.data(), bo.data(), bnd.data(), eo.data(), edges.data(), &out));
+  return gpu::DeviceParts(out);
+}
+
 inline PartitionAssignment partition_topo_chunks(const EdaGraph& g, std::uint32_t k) {  // src/partition.cpp:301
   auto d = g.to_device();
   groot_assignment* a = nullptr;
@@ -423,15 +454,18 @@ inline std::vector<AugmentedPartition> core_subgraphs(const EdaGraph& g, const P
   auto a = pa.to_device();
   return parts_from_device(gpu::regrow(d.get(), a.get(), false).get());
 }
-inline double crossing_fraction(const EdaGraph& g, const PartitionAssignment& pa) {
-  if (g.fwd_edges.empty()) return 0.0;
-  std::uint64_t c = 0;
-  for (const auto& [u, v] : g.fwd_edges) c += pa.part_of[u] != pa.part_of[v];
-  return static_cast<double>(c) / static_cast<double>(g.fwd_edges.size());
+inline double crossing_fraction(const EdaGraph& g, const PartitionAssignment& pa) {  // src/partition.cpp:468-474
+  auto d = g.to_device();
+  auto a = pa.to_device();
+  double f = 0.0;
+  detail::check(groot_crossing_fraction(d.get(), a.get(), &f));
+  return f;
 }
-inline std::uint64_t edge_cut(const EdaGraph& g, const PartitionAssignment& pa) {
+inline std::uint64_t edge_cut(const EdaGraph& g, const PartitionAssignment& pa) {  // src/partition.cpp:508-513
+  auto d = g.to_device();
+  auto a = pa.to_device();
   std::uint64_t c = 0;
-  for (const auto& [u, v] : g.fwd_edges) c += pa.part_of[u] != pa.part_of[v];
+  detail::check(groot_edge_cut(d.get(), a.get(), &c));
   return c;
 }
 inline std::uint64_t footprint_proxy(const std::vector<AugmentedPartition>& parts, std::uint32_t feature_cols = 4,
@@ -599,20 +633,12 @@ inline Prediction predict_full(const Model& model, const EdaGraph& g) {  // src/
   return detail::finish(std::move(labels), conf, acc);
 }
 
+// predict (src/gnn.cpp:280-291): every part forwarded as given, each node scored
+// from the part that holds it as a core node.
 inline Prediction predict(const Model& model, const EdaGraph& g, const std::vector<AugmentedPartition>& parts) {
-  // src/gnn.cpp:280-291: the parts are re-derived on the device from their core sets.
-  PartitionAssignment pa;
-  pa.part_of.assign(g.n, 0);
-  pa.k = static_cast<std::uint32_t>(parts.size());
-  bool regrown = false;
-  for (std::uint32_t p = 0; p < parts.size(); ++p) {
-    for (std::uint32_t v : parts[p].core_nodes) pa.part_of[v] = p;
-    regrown = regrown || !parts[p].boundary_nodes.empty();
-  }
   auto m = model.to_device();
   auto d = g.to_device();
-  auto a = pa.to_device();
-  auto dp = gpu::regrow(d.get(), a.get(), regrown);
+  auto dp = parts_to_device(g.n, parts);
   std::vector<std::uint8_t> labels(g.n);
   std::uint64_t conf[25];
   double acc = 0;
@@ -620,7 +646,50 @@ inline Prediction predict(const Model& model, const EdaGraph& g, const std::vect
   return detail::finish(std::move(labels), conf, acc);
 }
 
-// ---- inc/spmm.hpp (API parity) -----------------------------------------------------------
+// ---- inc/worker_pool.hpp -----------------------------------------------------------
+// Host thread pool with the reference's surface (inc/worker_pool.hpp:18-56). The
+// device path does not use it (the GPU is the parallelism); it is here so caller
+// code that builds or passes pools compiles and runs unchanged.
+class WorkerPool {
+ public:
+  explicit WorkerPool(unsigned workers = 0) : workers_(workers ? workers : default_workers()) {}
+  WorkerPool(const WorkerPool&) = delete;
+  WorkerPool& operator=(const WorkerPool&) = delete;
+  unsigned workers() const { return workers_; }
+  void for_each(std::size_t count, const std::function<void(std::size_t)>& fn) {
+    if (workers_ <= 1 || count <= 1 || busy_.exchange(true)) {  // nested / concurrent: inline
+      for (std::size_t i = 0; i < count; ++i) fn(i);
+      return;
+    }
+    std::atomic<std::size_t> next{0};
+    auto run = [&] {
+      for (std::size_t i = next++; i < count; i = next++) fn(i);
+    };
+    std::vector<std::thread> ts;
+    for (unsigned t = 1; t < workers_; ++t) ts.emplace_back(run);
+    run();
+    for (auto& t : ts) t.join();
+    busy_ = false;
+  }
+  static unsigned default_workers() {
+    if (const char* e = std::getenv("AIGSAGE_WORKERS")) {
+      const long v = std::strtol(e, nullptr, 10);
+      if (v > 0) return static_cast<unsigned>(v);
+    }
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? h : 1u;
+  }
+
+ private:
+  unsigned workers_ = 1;
+  std::atomic<bool> busy_{false};
+};
+inline WorkerPool& default_pool() {
+  static WorkerPool pool;
+  return pool;
+}
+
+// ---- inc/spmm.hpp ---------------------------------------------------------------------
 namespace spmm {
 template <class T>
 struct CsrMatrix {
@@ -630,17 +699,268 @@ struct CsrMatrix {
   std::vector<T> values;
   std::uint64_t nnz() const { return row_ptr.empty() ? 0 : row_ptr.back(); }
   std::uint32_t degree(std::uint32_t r) const { return static_cast<std::uint32_t>(row_ptr[r + 1] - row_ptr[r]); }
+  void validate() const {  // inc/spmm.hpp:25-36, same messages
+    if (row_ptr.size() != static_cast<std::size_t>(rows) + 1) throw std::invalid_argument("CsrMatrix: row_ptr size");
+    for (std::uint32_t r = 0; r < rows; ++r)
+      if (row_ptr[r] > row_ptr[r + 1]) throw std::invalid_argument("CsrMatrix: row_ptr not monotone");
+    if (col_idx.size() != nnz() || values.size() != nnz()) throw std::invalid_argument("CsrMatrix: nnz mismatch");
+    for (std::uint32_t c : col_idx)
+      if (c >= cols) throw std::invalid_argument("CsrMatrix: column index out of range");
+  }
 };
 
-// out = m * dense (spmm::execute, inc/spmm.hpp:106-181) on the device, fp32.
+struct DegreeSort {
+  std::vector<std::uint32_t> perm;            // sorted position -> original row
+  std::vector<std::uint64_t> sorted_row_ptr;  // row pointers in the new order
+};
+
+// degree_sort (src/spmm.cpp:9-35): stable ascending by degree, on the device.
+inline DegreeSort degree_sort(std::uint32_t rows, std::span<const std::uint64_t> row_ptr) {
+  if (row_ptr.size() != static_cast<std::size_t>(rows) + 1) throw std::invalid_argument("degree_sort: row_ptr size");
+  DegreeSort d;
+  d.perm.resize(rows);
+  d.sorted_row_ptr.resize(rows + 1ull);
+  detail::check(groot_degree_sort(rows, row_ptr.data(), d.perm.data(), d.sorted_row_ptr.data()));
+  return d;
+}
+template <class T>
+DegreeSort degree_sort(const CsrMatrix<T>& m) {
+  return degree_sort(m.rows, m.row_ptr);
+}
+
+enum class WorkKind : std::uint8_t { HdChunk, LdBatch, MidRow };
+struct WorkUnit {
+  WorkKind kind;
+  std::uint32_t sorted_row = 0;
+  std::uint32_t row_count = 1;
+  std::uint64_t nz_begin = 0;
+  std::uint64_t nz_end = 0;
+  std::uint32_t partial_slot = 0;
+};
+struct LdGroup {
+  std::uint32_t degree;
+  std::uint32_t row_begin;
+  std::uint32_t row_end;
+};
+struct SpmmPlan {  // inc/spmm.hpp:72-90
+  std::uint32_t rows = 0;
+  std::uint64_t nnz = 0;
+  std::vector<std::uint32_t> perm;
+  std::vector<std::uint32_t> inv_perm;
+  std::vector<std::uint64_t> sorted_row_ptr;
+  std::vector<std::uint32_t> hd_rows;
+  std::vector<LdGroup> ld_groups;
+  std::vector<std::uint32_t> mid_rows;
+  std::vector<WorkUnit> work_units;
+  std::uint32_t hd_threshold = 512;
+  std::uint32_t ld_threshold = 12;
+  std::uint32_t nz_budget = 96;
+  std::uint32_t ld_row_begin = 0;
+  std::uint32_t ld_row_end = 0;
+  unsigned workers = 0;
+};
+inline constexpr std::uint32_t kHdChunksPerRow = 32;
+
+// build_plan (src/spmm.cpp:37-127): the row classifier; the degree sort runs on
+// the device, the unit list is the reference's exactly.
+inline SpmmPlan build_plan(std::uint32_t rows, std::span<const std::uint64_t> row_ptr, unsigned workers,
+                           std::uint32_t hd_threshold = 512, std::uint32_t ld_threshold = 12,
+                           std::uint32_t nz_budget = 96) {
+  if (row_ptr.size() != static_cast<std::size_t>(rows) + 1) throw std::invalid_argument("build_plan: row_ptr size");
+  std::uint64_t counts[6];
+  detail::check(groot_build_plan_rows(rows, row_ptr.data(), hd_threshold, ld_threshold, nz_budget, counts, nullptr,
+                                      nullptr, nullptr, nullptr, nullptr));
+  SpmmPlan p;
+  p.rows = rows;
+  p.nnz = row_ptr[rows];
+  p.hd_threshold = hd_threshold;
+  p.ld_threshold = ld_threshold;
+  p.nz_budget = nz_budget;
+  p.workers = workers;
+  p.perm.resize(rows);
+  p.hd_rows.resize(counts[0]);
+  p.mid_rows.resize(counts[1]);
+  std::vector<std::uint32_t> ldg(3 * counts[2]);
+  std::vector<std::uint64_t> units(6 * counts[3]);
+  detail::check(groot_build_plan_rows(rows, row_ptr.data(), hd_threshold, ld_threshold, nz_budget, counts,
+                                      p.perm.data(), p.hd_rows.data(), p.mid_rows.data(), ldg.data(), units.data()));
+  p.ld_row_begin = static_cast<std::uint32_t>(counts[4]);
+  p.ld_row_end = static_cast<std::uint32_t>(counts[5]);
+  p.inv_perm.resize(rows);
+  for (std::uint32_t s = 0; s < rows; ++s) p.inv_perm[p.perm[s]] = s;
+  p.sorted_row_ptr.assign(rows + 1ull, 0);
+  for (std::uint32_t s = 0; s < rows; ++s)
+    p.sorted_row_ptr[s + 1] = p.sorted_row_ptr[s] + (row_ptr[p.perm[s] + 1] - row_ptr[p.perm[s]]);
+  for (std::uint64_t i = 0; i < counts[2]; ++i) p.ld_groups.push_back({ldg[3 * i], ldg[3 * i + 1], ldg[3 * i + 2]});
+  for (std::uint64_t i = 0; i < counts[3]; ++i) {
+    const std::uint64_t* u = &units[6 * i];
+    const WorkKind kind = u[0] == 0 ? WorkKind::HdChunk : (u[0] == 1 ? WorkKind::LdBatch : WorkKind::MidRow);
+    p.work_units.push_back({kind, static_cast<std::uint32_t>(u[1]), static_cast<std::uint32_t>(u[2]), u[3], u[4],
+                            static_cast<std::uint32_t>(u[5])});
+  }
+  return p;
+}
+template <class T>
+SpmmPlan build_plan(const CsrMatrix<T>& m, unsigned workers, std::uint32_t hd_threshold = 512,
+                    std::uint32_t ld_threshold = 12, std::uint32_t nz_budget = 96) {
+  return build_plan(m.rows, m.row_ptr, workers, hd_threshold, ld_threshold, nz_budget);
+}
+
+namespace detail {
+// out = m * dense on the device, rows of degree >= hd_threshold as 32 ordered chunk
+// partials (0: plain row loop). Bitwise the reference's arithmetic for T = float, double.
+template <class T>
+void device_spmm(const CsrMatrix<T>& m, const T* dense, std::uint32_t f, T* out, std::uint32_t hd_threshold) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "spmm: float or double values");
+  if constexpr (std::is_same_v<T, double>)
+    aigsage::detail::check(groot_spmm_csr_f64(m.rows, m.cols, m.row_ptr.data(), m.col_idx.data(),
+                                              m.values.empty() ? nullptr : m.values.data(), dense, f, hd_threshold, out));
+  else
+    aigsage::detail::check(groot_spmm_csr(m.rows, m.cols, m.row_ptr.data(), m.col_idx.data(),
+                                          m.values.empty() ? nullptr : m.values.data(), dense, f, hd_threshold, out));
+}
+}  // namespace detail
+
+// execute (inc/spmm.hpp:106-170): out = m * dense on the device; bitwise the
+// reference's result for this plan (same per-row order, HD rows as 32 ordered
+// chunk partials). The pool argument is accepted and unused.
+template <class T>
+void execute(const SpmmPlan& plan, const CsrMatrix<T>& m, const T* dense, std::uint32_t f, T* out,
+             WorkerPool* pool = nullptr) {
+  (void)pool;
+  if (m.rows != plan.rows || m.nnz() != plan.nnz)
+    throw std::invalid_argument("spmm::execute: plan does not match matrix");
+  detail::device_spmm(m, dense, f, out, plan.hd_rows.empty() ? 0u : plan.hd_threshold);
+}
+template <class T>
+std::vector<T> execute(const SpmmPlan& plan, const CsrMatrix<T>& m, const std::vector<T>& dense, std::uint32_t f,
+                       WorkerPool* pool = nullptr) {
+  if (dense.size() != static_cast<std::size_t>(m.cols) * f) throw std::invalid_argument("spmm::execute: dense shape mismatch");
+  std::vector<T> out(static_cast<std::size_t>(m.rows) * f);
+  execute(plan, m, dense.data(), f, out.data(), pool);
+  return out;
+}
+// Convenience (no plan argument): the plan the reference would build by default.
 template <class T>
 std::vector<T> execute(const CsrMatrix<T>& m, const std::vector<T>& dense, std::uint32_t f) {
-  if (dense.size() != static_cast<size_t>(m.cols) * f) throw std::invalid_argument("spmm::execute: dense shape mismatch");
-  std::vector<float> v(m.values.begin(), m.values.end()), d(dense.begin(), dense.end()),
-      o(static_cast<size_t>(m.rows) * f);
-  detail::check(groot_spmm_csr(m.rows, m.cols, m.row_ptr.data(), m.col_idx.data(), v.data(), d.data(), f, o.data()));
-  return std::vector<T>(o.begin(), o.end());
+  return execute(build_plan(m, 0), m, dense, f);
+}
+
+// reference_spmm (inc/spmm.hpp:183-204): plain row loop, on the device.
+template <class T>
+void reference_spmm(const CsrMatrix<T>& m, const T* dense, std::uint32_t f, T* out) {
+  detail::device_spmm(m, dense, f, out, 0u);
+}
+template <class T>
+std::vector<T> reference_spmm(const CsrMatrix<T>& m, const std::vector<T>& dense, std::uint32_t f) {
+  if (dense.size() != static_cast<std::size_t>(m.cols) * f)
+    throw std::invalid_argument("spmm::reference_spmm: dense shape mismatch");
+  std::vector<T> out(static_cast<std::size_t>(m.rows) * f);
+  reference_spmm(m, dense.data(), f, out.data());
+  return out;
+}
+// row_parallel_reference (inc/spmm.hpp:206-225): same result as reference_spmm.
+template <class T>
+void row_parallel_reference(const CsrMatrix<T>& m, const T* dense, std::uint32_t f, T* out, WorkerPool& pool) {
+  (void)pool;
+  reference_spmm(m, dense, f, out);
+}
+
+struct BenchReport {
+  double plan_ms = 0;
+  double exec_ms = 0;
+  double baseline_ms = 0;
+  double speedup = 0;  // baseline_ms / exec_ms
+  unsigned workers = 0;
+  int reps = 0;
+};
+// bench (src/spmm.cpp:129-175): median-of-reps wall time of build_plan + execute
+// against the row loop, f columns of U(-1,1) from mt19937_64(0xb00b1e5), through
+// the host entry points (copies included).
+inline BenchReport bench(const CsrMatrix<float>& m, std::uint32_t f, int reps, WorkerPool* pool = nullptr) {
+  m.validate();
+  std::mt19937_64 rng(0xb00b1e5);
+  std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+  std::vector<float> dense(static_cast<std::size_t>(m.cols) * f), out(static_cast<std::size_t>(m.rows) * f);
+  for (float& x : dense) x = dist(rng);
+  auto ms_of = [](auto fn) {
+    const auto t0 = std::chrono::steady_clock::now();
+    fn();
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  auto median = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v.empty() ? 0.0 : v[v.size() / 2];
+  };
+  BenchReport r;
+  r.reps = reps < 1 ? 1 : reps;
+  r.workers = pool ? pool->workers() : 0;
+  SpmmPlan plan;
+  r.plan_ms = ms_of([&] { plan = build_plan(m, r.workers); });
+  std::vector<double> ex, base;
+  for (int i = 0; i < r.reps; ++i) {
+    ex.push_back(ms_of([&] { execute(plan, m, dense.data(), f, out.data(), pool); }));
+    base.push_back(ms_of([&] { reference_spmm(m, dense.data(), f, out.data()); }));
+  }
+  r.exec_ms = median(ex);
+  r.baseline_ms = median(base);
+  r.speedup = r.exec_ms > 0 ? r.baseline_ms / r.exec_ms : 0.0;
+  return r;
 }
 }  // namespace spmm
+
+// ---- inc/gnn.hpp: SageContext (src/gnn.cpp:140-178) ------------------------------------
+// The reference's host fields (a_mean = D^-1 A, a_mean_t = A D^-1 with 1/deg values,
+// their plans, features as an n x 4 matrix, labels) plus the graph resident in
+// HBM with the device's per-graph state built (groot_graph_prepare: row
+// classifier, tile plan, HD chunk plan, activations). forward(model, ctx) runs
+// on that resident graph without re-uploading or re-planning it.
+struct SageContext {
+  spmm::CsrMatrix<double> a_mean;
+  spmm::CsrMatrix<double> a_mean_t;
+  spmm::SpmmPlan plan;
+  spmm::SpmmPlan plan_t;
+  RowMat features;
+  std::vector<std::uint8_t> labels;
+  std::shared_ptr<groot_graph> device;
+};
+
+inline SageContext make_context(const EdaGraph& g) {
+  SageContext c;
+  c.a_mean.rows = c.a_mean.cols = g.n;
+  c.a_mean.row_ptr = g.row_ptr;
+  c.a_mean.col_idx = g.col_idx;
+  c.a_mean.values.resize(g.col_idx.size());
+  c.a_mean_t = c.a_mean;
+  for (std::uint32_t v = 0; v < g.n; ++v) {
+    const double inv = g.degree[v] ? 1.0 / g.degree[v] : 0.0;
+    for (std::uint64_t q = g.row_ptr[v]; q < g.row_ptr[v + 1]; ++q) {
+      c.a_mean.values[q] = inv;
+      const std::uint32_t u = g.col_idx[q];
+      c.a_mean_t.values[q] = g.degree[u] ? 1.0 / g.degree[u] : 0.0;
+    }
+  }
+  c.plan = spmm::build_plan(c.a_mean, 0);
+  c.plan_t = spmm::build_plan(c.a_mean_t, 0);
+  c.features = RowMat(g.n, 4);
+  for (std::size_t i = 0; i < g.features.size(); ++i) c.features.data()[i] = g.features[i];
+  c.labels = g.labels;
+  auto d = g.to_device();
+  detail::check(groot_graph_prepare(d.get()));
+  c.device = std::shared_ptr<groot_graph>(d.release(), gpu::GraphDeleter{});
+  return c;
+}
+
+inline RowMat forward(const Model& model, const SageContext& ctx) {  // src/gnn.cpp:172-178
+  auto m = model.to_device();
+  std::uint32_t n;
+  std::uint64_t nnz, ne;
+  detail::check(groot_graph_sizes(ctx.device.get(), &n, &nnz, &ne));
+  std::vector<float> lg(static_cast<size_t>(n) * model.num_classes());
+  detail::check(groot_forward(m.get(), ctx.device.get(), lg.data()));
+  RowMat out(n, model.num_classes());
+  for (size_t i = 0; i < lg.size(); ++i) out.data()[i] = lg[i];
+  return out;
+}
 
 }  // namespace aigsage

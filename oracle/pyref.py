@@ -76,7 +76,7 @@ def _declare(L):
         "ref_plan_execute": (i32, [P, u32, P, P, P, P, u32, P, C.c_uint]),
         "ref_plan_free": (None, [P]),
         "ref_predict_full": (i32, [P, u32, u32, u32, u32, P, P, P, P, P]),
-        "ref_predict_parts": (i32, [P, P, u32, u32, u32, u32, u32, u32, P, P]),
+        "ref_predict_parts": (i32, [P, P, u32, u32, u32, u32, u32, u32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -109,6 +109,19 @@ class RefGraph:
         n, nnz, ne = u32(), u64(), u64()
         lib().ref_graph_sizes(self.h, C.byref(n), C.byref(nnz), C.byref(ne))
         return n.value, nnz.value, ne.value
+
+    def field(self, name: str) -> np.ndarray:
+        """One EdaGraph array (row_ptr, col_idx, features, labels, degree, fwd_edges),
+        copied alone so BASELINE-size graphs are compared one array at a time."""
+        n, nnz, ne = self.sizes()
+        shapes = {"row_ptr": (n + 1, np.uint64), "col_idx": (nnz, np.uint32), "features": ((n, 4), np.uint8),
+                  "labels": (n, np.uint8), "degree": (n, np.uint32), "fwd_edges": ((ne, 2), np.uint32)}
+        shape, dt = shapes[name]
+        out = np.empty(shape, dt)
+        args = [None] * 6
+        args[list(shapes).index(name)] = out
+        lib().ref_graph_copy(self.h, *[ptr(a) for a in args])
+        return out
 
     def to_host(self) -> HostGraph:
         n, nnz, ne = self.sizes()
@@ -263,10 +276,11 @@ def predict_full(g: RefGraph, params, depth=4, in_dim=4, hidden=32, classes=5, w
 
 
 def predict_parts(parts: RefParts, first: int, count: int, params, pred=None, depth=4, in_dim=4, hidden=32,
-                  classes=5):
-    """predict (src/gnn.cpp:280-291) over parts [first, first+count), parts in parallel."""
+                  classes=5, logits=None):
+    """predict (src/gnn.cpp:280-291) over parts [first, first+count), parts in parallel.
+    pred (u8[n]) / logits (f64[n, classes]) receive the core rows of those parts."""
     st = lib().ref_predict_parts(parts.g.h, parts.h, first, count, depth, in_dim, hidden, classes,
-                                 ptr(np.ascontiguousarray(params, np.float64)), ptr(pred))
+                                 ptr(np.ascontiguousarray(params, np.float64)), ptr(pred), ptr(logits))
     if st != 0:
         raise ValueError(_err())
 

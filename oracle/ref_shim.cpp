@@ -11,6 +11,7 @@
 // run_forward (src/gnn.cpp:37-52) around the reference's compiled
 // spmm::build_plan / spmm::execute / default_pool — the only part that is
 // not the reference's own object code is the dense h*W product.
+#include <algorithm>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
@@ -54,6 +55,49 @@ struct ref_aig {
   Aig aig;
   GroundTruth gt;
 };
+
+// Restated dense step of run_forward (src/gnn.cpp:46-49: z = h*W_self + m*W_neigh,
+// + bias, ReLU) for rows [r0, r1). Per output j the two products are summed
+// over k ascending and combined as (s1 + s2) + b -- the same operation order
+// as a naive triple loop, but with j innermost so the compiler vectorises it
+// (no FMA contraction: -ffp-contract=off in oracle/Makefile).
+static void dense_rows(const double* h, const double* m, uint32_t in, const double* ws, const double* wn,
+                       const double* b, uint32_t hidden, size_t r0, size_t r1, double* hn) {
+  std::vector<double> s1(hidden), s2(hidden);
+  for (size_t r = r0; r < r1; ++r) {
+    std::fill(s1.begin(), s1.end(), 0.0);
+    std::fill(s2.begin(), s2.end(), 0.0);
+    const double* hr = h + r * in;
+    const double* mr = m + r * in;
+    for (uint32_t k = 0; k < in; ++k) {
+      const double hk = hr[k], mk = mr[k];
+      const double* wsk = ws + static_cast<size_t>(k) * hidden;
+      const double* wnk = wn + static_cast<size_t>(k) * hidden;
+      for (uint32_t j = 0; j < hidden; ++j) {
+        s1[j] += hk * wsk[j];
+        s2[j] += mk * wnk[j];
+      }
+    }
+    double* o = hn + r * hidden;
+    for (uint32_t j = 0; j < hidden; ++j) {
+      const double z = (s1[j] + s2[j]) + b[j];
+      o[j] = z > 0.0 ? z : 0.0;
+    }
+  }
+}
+
+// the dense step over all n rows, split into row blocks on `pool` (null: inline)
+static void dense_layer(const double* h, const double* m, uint32_t in, const double* ws, const double* wn,
+                        const double* b, uint32_t hidden, size_t n, double* hn, WorkerPool* pool) {
+  constexpr size_t kBlock = 4096;
+  const size_t blocks = (n + kBlock - 1) / kBlock;
+  auto run = [&](std::size_t i) {
+    const size_t r0 = i * kBlock, r1 = std::min(n, r0 + kBlock);
+    dense_rows(h, m, in, ws, wn, b, hidden, r0, r1, hn);
+  };
+  if (pool && blocks > 1) pool->for_each(blocks, run);
+  else for (size_t i = 0; i < blocks; ++i) run(i);
+}
 
 extern "C" {
 
@@ -299,14 +343,7 @@ int ref_predict_full(const ref_graph* g, uint32_t depth, uint32_t in_dim, uint32
       WorkerPool* pool = a.nnz() * in >= (1u << 16) ? &default_pool() : nullptr;
       spmm::execute(plan, a, h.data(), in, m.data(), pool);
       std::vector<double> hn(static_cast<size_t>(n) * hidden);
-      for (uint32_t r = 0; r < n; ++r)
-        for (uint32_t j = 0; j < hidden; ++j) {
-          double s1 = 0.0, s2 = 0.0;
-          for (uint32_t k = 0; k < in; ++k) s1 += h[static_cast<size_t>(r) * in + k] * ws[k * hidden + j];
-          for (uint32_t k = 0; k < in; ++k) s2 += m[static_cast<size_t>(r) * in + k] * wn[k * hidden + j];
-          const double z = (s1 + s2) + b[j];
-          hn[static_cast<size_t>(r) * hidden + j] = z > 0.0 ? z : 0.0;
-        }
+      dense_layer(h.data(), m.data(), in, ws, wn, b, hidden, n, hn.data(), &default_pool());
       h.swap(hn);
       in = hidden;
     }
@@ -336,10 +373,11 @@ int ref_predict_full(const ref_graph* g, uint32_t depth, uint32_t in_dim, uint32
 // predict (src/gnn.cpp:280-291) over parts [first, first+count): default_pool()
 // runs one part per item (the nested SpMM then runs inline, src/worker_pool.cpp:55-60),
 // each part = forward(materialize(g, part)) with the restated dense product,
-// scored on core rows. pred (global, n entries) receives the core labels.
+// scored on core rows. pred (global, n entries) receives the core labels and
+// logits (global, n x classes, may be NULL) the core rows' logits.
 int ref_predict_parts(const ref_graph* g, const ref_parts* h, uint32_t first, uint32_t count,
                       uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
-                      const double* prm, uint8_t* pred) {
+                      const double* prm, uint8_t* pred, double* logits) {
   return guarded([&] {
     if (first + count > h->parts.size()) throw std::invalid_argument("ref_predict_parts: range");
     default_pool().for_each(count, [&](std::size_t i) {
@@ -368,14 +406,7 @@ int ref_predict_parts(const ref_graph* g, const ref_parts* h, uint32_t first, ui
         std::vector<double> m(static_cast<size_t>(n) * in);
         spmm::execute(plan, a, x.data(), in, m.data(), &default_pool());  // nested: runs inline
         std::vector<double> hn(static_cast<size_t>(n) * hidden);
-        for (uint32_t r = 0; r < n; ++r)
-          for (uint32_t j = 0; j < hidden; ++j) {
-            double s1 = 0.0, s2 = 0.0;
-            for (uint32_t k = 0; k < in; ++k) s1 += x[static_cast<size_t>(r) * in + k] * ws[k * hidden + j];
-            for (uint32_t k = 0; k < in; ++k) s2 += m[static_cast<size_t>(r) * in + k] * wn[k * hidden + j];
-            const double z = (s1 + s2) + b[j];
-            hn[static_cast<size_t>(r) * hidden + j] = z > 0.0 ? z : 0.0;
-          }
+        dense_layer(x.data(), m.data(), in, ws, wn, b, hidden, n, hn.data(), nullptr);  // part-parallel already
         x.swap(hn);
         in = hidden;
       }
@@ -388,6 +419,7 @@ int ref_predict_parts(const ref_graph* g, const ref_parts* h, uint32_t first, ui
           double s = 0.0;
           for (uint32_t k = 0; k < in; ++k) s += x[static_cast<size_t>(r) * in + k] * wo[k * classes + c];
           s += bo[c];
+          if (logits) logits[static_cast<size_t>(part.core_nodes[r]) * classes + c] = s;
           if (c == 0 || s > best) { best = s; arg = c; }
         }
         if (pred) pred[part.core_nodes[r]] = static_cast<uint8_t>(arg);

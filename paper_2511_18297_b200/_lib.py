@@ -68,7 +68,10 @@ _SIG = {
     "groot_parts_copy_out": (i32, [P, u32, P, P, P]),
     "groot_footprint_proxy": (i32, [P, u32, u32, P]),
     "groot_materialize": (i32, [P, P, u32, P]),
+    "groot_parts_from_host": (i32, [u32, u32, P, P, P, P, P, P, P]),
     "groot_parts_free": (None, [P]),
+    "groot_graph_prepare": (i32, [P]),
+    "groot_graph_release_context": (i32, [P]),
     "groot_param_count": (u64, [u32, u32, u32, u32]),
     "groot_init_params": (i32, [u64, u32, u32, u32, u32, P]),
     "groot_model_create": (i32, [u32, u32, u32, u32, P, P]),
@@ -88,7 +91,10 @@ _SIG = {
     "groot_build_plan": (i32, [P, u32, u32, u32, P, P, P, P, P, P]),
     "groot_spmm_mean": (i32, [P, P, u32, P]),
     "groot_spmm_mean_dev": (i32, [P, P, u32, P]),
-    "groot_spmm_csr": (i32, [u32, u32, P, P, P, P, u32, P]),
+    "groot_spmm_csr": (i32, [u32, u32, P, P, P, P, u32, u32, P]),
+    "groot_spmm_csr_f64": (i32, [u32, u32, P, P, P, P, u32, u32, P]),
+    "groot_build_plan_rows": (i32, [u32, P, u32, u32, u32, P, P, P, P, P, P]),
+    "groot_degree_sort": (i32, [u32, P, P, P]),
 }
 
 # Every symbol include/groot.h declares (checked by tests/test_capi.py).

@@ -368,6 +368,23 @@ class AugmentedPartitions:
     def __iter__(self):
         return (self[p] for p in range(len(self)))
 
+    @staticmethod
+    def from_host(n: int, parts) -> "AugmentedPartitions":
+        """Upload a list of AugmentedPartition as given (groot_parts_from_host)."""
+        parts = list(parts)
+        k = len(parts)
+        cores = [np.ascontiguousarray(p.core_nodes, np.uint32) for p in parts]
+        bnds = [np.ascontiguousarray(p.boundary_nodes, np.uint32) for p in parts]
+        edges = [np.ascontiguousarray(p.edges, np.uint32).reshape(-1, 2) for p in parts]
+        off = lambda arrs: np.concatenate([[0], np.cumsum([a.shape[0] for a in arrs])]).astype(np.uint64)
+        cat = lambda arrs: np.ascontiguousarray(np.concatenate(arrs) if arrs else np.zeros(0, np.uint32), np.uint32)
+        # (keep every array referenced until the call returns: ptr() holds no reference)
+        co, ca, bo, ba = off(cores), cat(cores), off(bnds), cat(bnds)
+        eo, ea = off(edges), cat([e.ravel() for e in edges])
+        h = C.c_void_p()
+        check(lib().groot_parts_from_host(n, k, ptr(co), ptr(ca), ptr(bo), ptr(ba), ptr(eo), ptr(ea), C.byref(h)))
+        return AugmentedPartitions(h.value)
+
 
 def regrow(g: EdaGraph, pa: PartitionAssignment) -> AugmentedPartitions:
     """Algorithm 1 boundary re-growth (src/partition.cpp:460-462; K5, K6)."""
@@ -475,12 +492,36 @@ class Prediction:
     accuracy: float
 
 
-def forward(model: Model, g: EdaGraph) -> np.ndarray:
-    """src/gnn.cpp:172-178: n x classes logits (fp32 on device)."""
+def forward(model: Model, g) -> np.ndarray:
+    """src/gnn.cpp:172-178: n x classes logits (fp32 on device). g: EdaGraph or SageContext."""
+    if isinstance(g, SageContext):
+        g = g.graph
     c = model.info()["classes"]
     out = np.empty((g.n, c), np.float32)
     check(lib().groot_forward(model.handle, g.handle, ptr(out)))
     return out
+
+
+class SageContext:
+    """make_context (src/gnn.cpp:140-170): the per-graph state the forward derives
+    from the graph alone (row classifier, tile plan, HD plan, activation buffers),
+    built on the device and cached on the resident graph. forward(model, ctx)
+    reuses it; release() frees it."""
+
+    def __init__(self, g: EdaGraph):
+        self.graph = g
+        check(lib().groot_graph_prepare(g.handle))
+
+    @property
+    def labels(self):
+        return self.graph.labels
+
+    def release(self):
+        check(lib().groot_graph_release_context(self.graph.handle))
+
+
+def make_context(g: EdaGraph) -> SageContext:
+    return SageContext(g)
 
 
 def layer_dev(model: Model, g: EdaGraph, layer: int, hin=None, hout=None, labels=None, logits=None):
@@ -502,8 +543,10 @@ def forward_naive(model: Model, g: EdaGraph):
     return lg, lab
 
 
-def predict_full(model: Model, g: EdaGraph) -> Prediction:
-    """src/gnn.cpp:293-300."""
+def predict_full(model: Model, g) -> Prediction:
+    """src/gnn.cpp:293-300. g: EdaGraph or SageContext."""
+    if isinstance(g, SageContext):
+        g = g.graph
     n = g.n
     labels = np.empty(n, np.uint8)
     conf = np.zeros((5, 5), np.uint64)
@@ -512,9 +555,12 @@ def predict_full(model: Model, g: EdaGraph) -> Prediction:
     return Prediction(labels, conf, acc.value)
 
 
-def predict(model: Model, g: EdaGraph, parts: AugmentedPartitions) -> Prediction:
-    """src/gnn.cpp:280-291: every node scored from its core partition."""
+def predict(model: Model, g: EdaGraph, parts) -> Prediction:
+    """src/gnn.cpp:280-291: every node scored from its core partition. `parts` is a
+    device AugmentedPartitions (regrow's result) or a list of AugmentedPartition."""
     n = g.n
+    if not isinstance(parts, AugmentedPartitions):
+        parts = AugmentedPartitions.from_host(n, parts)
     labels = np.empty(n, np.uint8)
     conf = np.zeros((5, 5), np.uint64)
     acc = C.c_double()
@@ -565,6 +611,51 @@ def build_plan(g: EdaGraph, hd_threshold=512, ld_threshold=12, nz_budget=96) -> 
             "ld_row_begin": int(counts[4]), "ld_row_end": int(counts[5])}
 
 
+def build_plan_rows(row_ptr, hd_threshold=512, ld_threshold=12, nz_budget=96) -> dict:
+    """build_plan(rows, span row_ptr, ...) (src/spmm.cpp:37-127) from a host row_ptr."""
+    rp = np.ascontiguousarray(row_ptr, np.uint64)
+    rows = rp.shape[0] - 1
+    counts = np.zeros(6, np.uint64)
+    check(lib().groot_build_plan_rows(rows, ptr(rp), hd_threshold, ld_threshold, nz_budget, ptr(counts),
+                                      None, None, None, None, None))
+    perm = np.empty(rows, np.uint32)
+    hd = np.empty(int(counts[0]), np.uint32)
+    mid = np.empty(int(counts[1]), np.uint32)
+    ldg = np.empty((int(counts[2]), 3), np.uint32)
+    units = np.empty((int(counts[3]), 6), np.uint64)
+    check(lib().groot_build_plan_rows(rows, ptr(rp), hd_threshold, ld_threshold, nz_budget, ptr(counts), ptr(perm),
+                                      ptr(hd), ptr(mid), ptr(ldg), ptr(units)))
+    return {"perm": perm, "hd_rows": hd, "mid_rows": mid, "ld_groups": ldg, "units": units,
+            "ld_row_begin": int(counts[4]), "ld_row_end": int(counts[5]), "rows": rows, "nnz": int(rp[-1])}
+
+
+def degree_sort(row_ptr):
+    """src/spmm.cpp:9-35: (perm, sorted_row_ptr)."""
+    rp = np.ascontiguousarray(row_ptr, np.uint64)
+    rows = rp.shape[0] - 1
+    perm = np.empty(rows, np.uint32)
+    srp = np.empty(rows + 1, np.uint64)
+    check(lib().groot_degree_sort(rows, ptr(rp), ptr(perm), ptr(srp)))
+    return perm, srp
+
+
+def spmm_csr_f64(row_ptr, col_idx, values, dense, cols=None, hd_threshold=512) -> np.ndarray:
+    """spmm::execute over CsrMatrix<double> on the device, bitwise the reference's
+    execute with a plan of this hd_threshold (0: reference_spmm's row loop)."""
+    rp = np.ascontiguousarray(row_ptr, np.uint64)
+    ci = np.ascontiguousarray(col_idx, np.uint32)
+    vals = None if values is None else np.ascontiguousarray(values, np.float64)
+    d = np.ascontiguousarray(dense, np.float64)
+    rows = rp.shape[0] - 1
+    cols = d.shape[0] if cols is None else cols
+    if d.shape[0] != cols:
+        raise GrootInvalidArgument(1, "spmm::execute: dense shape mismatch")
+    out = np.empty((rows, d.shape[1]), np.float64)
+    check(lib().groot_spmm_csr_f64(rows, cols, ptr(rp), ptr(ci), ptr(vals), ptr(d), d.shape[1], hd_threshold,
+                                   ptr(out)))
+    return out
+
+
 def spmm_mean(g: EdaGraph, dense: np.ndarray) -> np.ndarray:
     """out = D^-1 A dense (spmm::execute over make_context's a_mean), fp32."""
     d = np.ascontiguousarray(dense, np.float32)
@@ -575,8 +666,8 @@ def spmm_mean(g: EdaGraph, dense: np.ndarray) -> np.ndarray:
     return out
 
 
-def spmm_csr(row_ptr, col_idx, values, dense, cols=None) -> np.ndarray:
-    """spmm::execute over a general CsrMatrix<float> (inc/spmm.hpp:106-181)."""
+def spmm_csr(row_ptr, col_idx, values, dense, cols=None, hd_threshold=512) -> np.ndarray:
+    """spmm::execute over a general CsrMatrix<float> (inc/spmm.hpp:106-181); see spmm_csr_f64."""
     rp = np.ascontiguousarray(row_ptr, np.uint64)
     ci = np.ascontiguousarray(col_idx, np.uint32)
     vals = None if values is None else np.ascontiguousarray(values, np.float32)
@@ -586,7 +677,7 @@ def spmm_csr(row_ptr, col_idx, values, dense, cols=None) -> np.ndarray:
     if d.shape[0] != cols:
         raise GrootInvalidArgument(1, "spmm::execute: dense shape mismatch")
     out = np.empty((rows, d.shape[1]), np.float32)
-    check(lib().groot_spmm_csr(rows, cols, ptr(rp), ptr(ci), ptr(vals), ptr(d), d.shape[1], ptr(out)))
+    check(lib().groot_spmm_csr(rows, cols, ptr(rp), ptr(ci), ptr(vals), ptr(d), d.shape[1], hd_threshold, ptr(out)))
     return out
 
 

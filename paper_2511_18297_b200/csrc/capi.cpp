@@ -23,17 +23,29 @@
 namespace groot {
 
 std::atomic<uint64_t> g_launches{0};
-static cudaStream_t g_stream = nullptr;
 static thread_local std::string g_error;
 
-cudaStream_t stream() { return g_stream; }
+// One session per device: every device has its own library
+// stream and cached attributes; the calling thread's current device selects
+// them, and the handle-taking entry points make the handle's device current.
+static std::atomic<cudaStream_t> g_stream[kMaxDevices];
+static std::atomic<int> g_sms[kMaxDevices];
+
+int current_device() {
+  int dev = 0;
+  GROOT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) fail(GROOT_ECUDA, "device ordinal beyond the library's session table");
+  return dev;
+}
+
+cudaStream_t stream() { return g_stream[current_device()].load(std::memory_order_relaxed); }
 
 int num_sms() {
-  static int sms = 0;
+  const int dev = current_device();
+  int sms = g_sms[dev].load(std::memory_order_relaxed);
   if (!sms) {
-    int dev = 0;
-    GROOT_CUDA(cudaGetDevice(&dev));
     GROOT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    g_sms[dev].store(sms, std::memory_order_relaxed);
   }
   return sms;
 }
@@ -51,6 +63,8 @@ groot_assignment* load_assignment(const char*, uint32_t);
 uint64_t edge_cut(const groot_graph*, const groot_assignment*);
 groot_parts* regrow(const groot_graph*, const groot_assignment*, int);
 groot_graph* materialize(const groot_graph*, const groot_parts*, uint32_t);
+groot_parts* parts_from_host(uint32_t, uint32_t, const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*,
+                             const uint64_t*, const uint32_t*);
 groot_graph* union_of_parts(const groot_graph*, const groot_parts*, std::vector<uint64_t>&,
                             const std::vector<uint32_t>*);
 void scatter_core_labels(const groot_parts*, const std::vector<uint64_t>&, const uint8_t*, uint8_t*);
@@ -64,10 +78,15 @@ groot_graph* batch_padded(const groot_graph*, uint32_t, uint32_t);
 bool replicate_forward_plan(groot_graph*, groot_graph*, uint32_t, uint32_t);
 void forward_naive_device(const groot_model*, groot_graph*, uint8_t*, float*, unsigned long long*);
 void spmm_mean_device(groot_graph*, const float*, uint32_t, float*);
-void spmm_csr_device(uint32_t, const uint32_t*, const uint32_t*, const float*, const float*, uint32_t, float*);
+void spmm_csr_device(uint32_t, const uint32_t*, const uint32_t*, const float*, const float*, uint32_t, float*, uint32_t);
 void model_upload(groot_model*);
 void classify_rows(groot_graph*, uint32_t);
 uint32_t hd_threshold();
+void confusion_device(uint32_t, const uint8_t*, const uint8_t*, unsigned long long*);
+void spmm_csr_device_f64(uint32_t, const uint32_t*, const uint32_t*, const double*, const double*, uint32_t, double*,
+                         uint32_t);
+void graph_prepare(groot_graph*);
+void graph_release_context(groot_graph*);
 
 // ---------------------------------------------------------------------------
 // CSA multiplier generator (src/circuitgen.cpp:13-133). Nodes are created in
@@ -414,6 +433,7 @@ groot_model* model_create(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint
   if (in_dim != 4 || hidden != 32) fail(GROOT_EINVAL, "model: the device path supports in_dim 4 and hidden 32");
   if (classes < 1 || classes > 8) fail(GROOT_EINVAL, "model: classes must be in 1..8");
   auto* m = new groot_model;
+  m->device = current_device();
   m->depth = depth;
   m->in_dim = in_dim;
   m->hidden = hidden;
@@ -436,6 +456,35 @@ static void need(const void* p, const char* what) {
   if (!p) fail(GROOT_EINVAL, std::string(what) + ": null argument");
 }
 
+// spmm::execute over a host CsrMatrix<T> (validate() checks, inc/spmm.hpp:25-36)
+template <class T, class Dev>
+static void spmm_csr_host(uint32_t rows, uint32_t cols, const uint64_t* rp, const uint32_t* col, const T* vals,
+                          const T* dense, uint32_t f, uint32_t hd_threshold, T* out, Dev device_fn) {
+  need(rp, "groot_spmm_csr");
+  const uint64_t nnz = rp[rows];
+  if (nnz >= 0xFFFFFFFFull) fail(GROOT_EINVAL, "spmm: nnz must be < 2^32");
+  std::vector<uint32_t> rp32(rows + 1ull);
+  for (uint32_t r = 0; r <= rows; ++r) {
+    if (r && rp[r] < rp[r - 1]) fail(GROOT_EINVAL, "CsrMatrix: row_ptr not monotone");
+    rp32[r] = static_cast<uint32_t>(rp[r]);
+  }
+  for (uint64_t q = 0; q < nnz; ++q)
+    if (col[q] >= cols) fail(GROOT_EINVAL, "CsrMatrix: column index out of range");
+  DevBuf<uint32_t> drp(rows + 1ull), dcol(nnz);
+  DevBuf<T> dval(nnz), dd(static_cast<size_t>(cols) * f), dout(static_cast<size_t>(rows) * f);
+  drp.upload(rp32.data(), rows + 1ull);
+  dcol.upload(col, nnz);
+  if (vals) dval.upload(vals, nnz);
+  dd.upload(dense, static_cast<size_t>(cols) * f);
+  device_fn(rows, drp.p, dcol.p, vals ? dval.p : nullptr, dd.p, f, dout.p, hd_threshold);
+  dout.download(out, static_cast<size_t>(rows) * f);
+  stream_sync();
+}
+
+static void same_device(const groot_model* m, const groot_graph* g) {
+  if (m->device != g->device) fail(GROOT_EINVAL, "model and graph live on different devices");
+}
+
 }  // namespace groot
 
 using namespace groot;
@@ -446,12 +495,15 @@ const char* groot_last_error(void) { return g_error.c_str(); }
 int groot_version(void) { return 1; }
 
 int groot_set_stream(void* s) {
-  g_stream = static_cast<cudaStream_t>(s);
-  return GROOT_OK;
+  return guarded([&] { g_stream[current_device()].store(static_cast<cudaStream_t>(s)); });
 }
-void* groot_get_stream(void) { return g_stream; }
+void* groot_get_stream(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  return g_stream[dev].load();
+}
 int groot_device_synchronize(void) {
-  return guarded([] { GROOT_CUDA(cudaStreamSynchronize(g_stream)); });
+  return guarded([] { GROOT_CUDA(cudaStreamSynchronize(stream())); });
 }
 uint64_t groot_kernel_launches(void) { return g_launches.load(); }
 void groot_reset_kernel_launches(void) { g_launches.store(0); }
@@ -534,6 +586,7 @@ int groot_encode(uint32_t ni, uint32_t na, const uint32_t* ands, uint32_t no, co
 int groot_batch(const groot_graph* g, uint32_t copies, groot_graph** out) {
   return guarded([&] {
     need(g, "groot_batch");
+    DeviceScope ds_g(g->device);
     *out = batch(g, copies);
   });
 }
@@ -559,6 +612,7 @@ int groot_graph_from_edges(uint32_t n, const uint8_t* feat, const uint8_t* lab, 
 int groot_graph_sizes(const groot_graph* g, uint32_t* n, uint64_t* nnz, uint64_t* ne) {
   return guarded([&] {
     need(g, "groot_graph_sizes");
+    DeviceScope ds_g(g->device);
     if (n) *n = g->n;
     if (nnz) *nnz = g->nnz;
     if (ne) *ne = g->ne;
@@ -569,6 +623,7 @@ int groot_graph_copy_out(const groot_graph* g, uint64_t* rp, uint32_t* col, uint
                          uint32_t* deg, uint32_t* edges) {
   return guarded([&] {
     need(g, "groot_graph_copy_out");
+    DeviceScope ds_g(g->device);
     graph_copy_out(g, rp, col, feat, lab, deg, edges);
   });
 }
@@ -577,6 +632,7 @@ int groot_graph_device_ptrs(const groot_graph* g, const uint32_t** rp, const uin
                             const uint8_t** lab, const uint32_t** edges) {
   return guarded([&] {
     need(g, "groot_graph_device_ptrs");
+    DeviceScope ds_g(g->device);
     if (rp) *rp = g->rp.p;
     if (col) *col = g->col.p;
     if (feat) *feat = g->feat.p;
@@ -591,6 +647,7 @@ void groot_graph_free(groot_graph* g) { delete g; }
 int groot_partition_topo_chunks(const groot_graph* g, uint32_t k, groot_assignment** out) {
   return guarded([&] {
     need(g, "groot_partition_topo_chunks");
+    DeviceScope ds_g(g->device);
     *out = topo_chunks(g, k);
   });
 }
@@ -612,6 +669,7 @@ int groot_assignment_from_host(uint32_t n, const uint32_t* part_of, groot_assign
 int groot_assignment_info(const groot_assignment* a, uint32_t* n, uint32_t* k) {
   return guarded([&] {
     need(a, "groot_assignment_info");
+    DeviceScope ds_a(a->device);
     if (n) *n = a->n;
     if (k) *k = a->k;
   });
@@ -620,6 +678,7 @@ int groot_assignment_info(const groot_assignment* a, uint32_t* n, uint32_t* k) {
 int groot_assignment_copy_out(const groot_assignment* a, uint32_t* part_of) {
   return guarded([&] {
     need(a, "groot_assignment_copy_out");
+    DeviceScope ds_a(a->device);
     a->part_of.download(part_of, a->n);
     stream_sync();
   });
@@ -630,14 +689,17 @@ void groot_assignment_free(groot_assignment* a) { delete a; }
 int groot_crossing_fraction(const groot_graph* g, const groot_assignment* a, double* fraction) {
   return guarded([&] {
     need(g, "groot_crossing_fraction");
+    DeviceScope ds_g(g->device);
     need(a, "groot_crossing_fraction");
-    *fraction = g->ne ? static_cast<double>(edge_cut(g, a)) / static_cast<double>(g->ne) : 0.0;
+    const uint64_t cut = edge_cut(g, a);
+    *fraction = g->ne ? static_cast<double>(cut) / static_cast<double>(g->ne) : 0.0;
   });
 }
 
 int groot_edge_cut(const groot_graph* g, const groot_assignment* a, uint64_t* cut) {
   return guarded([&] {
     need(g, "groot_edge_cut");
+    DeviceScope ds_g(g->device);
     need(a, "groot_edge_cut");
     *cut = edge_cut(g, a);
   });
@@ -647,6 +709,7 @@ int groot_edge_cut(const groot_graph* g, const groot_assignment* a, uint64_t* cu
 int groot_regrow(const groot_graph* g, const groot_assignment* a, int with_b, groot_parts** out) {
   return guarded([&] {
     need(g, "groot_regrow");
+    DeviceScope ds_g(g->device);
     need(a, "groot_regrow");
     *out = regrow(g, a, with_b);
   });
@@ -655,6 +718,7 @@ int groot_regrow(const groot_graph* g, const groot_assignment* a, int with_b, gr
 int groot_parts_count(const groot_parts* p, uint32_t* k) {
   return guarded([&] {
     need(p, "groot_parts_count");
+    DeviceScope ds_p(p->device);
     *k = p->k;
   });
 }
@@ -662,6 +726,7 @@ int groot_parts_count(const groot_parts* p, uint32_t* k) {
 int groot_parts_sizes(const groot_parts* p, uint32_t part, uint32_t* nc, uint32_t* nb, uint64_t* ne) {
   return guarded([&] {
     need(p, "groot_parts_sizes");
+    DeviceScope ds_p(p->device);
     if (part >= p->k) fail(GROOT_EINVAL, "parts: index out of range");
     if (nc) *nc = static_cast<uint32_t>(p->core_off[part + 1] - p->core_off[part]);
     if (nb) *nb = static_cast<uint32_t>(p->bnd_off[part + 1] - p->bnd_off[part]);
@@ -672,6 +737,7 @@ int groot_parts_sizes(const groot_parts* p, uint32_t part, uint32_t* nc, uint32_
 int groot_parts_copy_out(const groot_parts* p, uint32_t part, uint32_t* core, uint32_t* bnd, uint32_t* edges) {
   return guarded([&] {
     need(p, "groot_parts_copy_out");
+    DeviceScope ds_p(p->device);
     if (part >= p->k) fail(GROOT_EINVAL, "parts: index out of range");
     const uint64_t c0 = p->core_off[part], c1 = p->core_off[part + 1];
     const uint64_t b0 = p->bnd_off[part], b1 = p->bnd_off[part + 1];
@@ -689,6 +755,7 @@ int groot_parts_copy_out(const groot_parts* p, uint32_t part, uint32_t* core, ui
 int groot_footprint_proxy(const groot_parts* p, uint32_t feature_cols, uint32_t hidden_dim, uint64_t* bytes) {
   return guarded([&] {
     need(p, "groot_footprint_proxy");
+    DeviceScope ds_p(p->device);
     uint64_t best = 0;
     for (uint32_t q = 0; q < p->k; ++q) {
       const uint64_t size = (p->core_off[q + 1] - p->core_off[q]) + (p->bnd_off[q + 1] - p->bnd_off[q]);
@@ -702,8 +769,18 @@ int groot_footprint_proxy(const groot_parts* p, uint32_t feature_cols, uint32_t 
 int groot_materialize(const groot_graph* g, const groot_parts* p, uint32_t part, groot_graph** out) {
   return guarded([&] {
     need(g, "groot_materialize");
+    DeviceScope ds_g(g->device);
     need(p, "groot_materialize");
     *out = materialize(g, p, part);
+  });
+}
+
+int groot_parts_from_host(uint32_t n, uint32_t k, const uint64_t* core_off, const uint32_t* core_nodes,
+                          const uint64_t* bnd_off, const uint32_t* boundary_nodes, const uint64_t* edge_off,
+                          const uint32_t* edges, groot_parts** out) {
+  return guarded([&] {
+    need(out, "groot_parts_from_host");
+    *out = parts_from_host(n, k, core_off, core_nodes, bnd_off, boundary_nodes, edge_off, edges);
   });
 }
 
@@ -793,6 +870,8 @@ int groot_forward(const groot_model* m, const groot_graph* g, float* logits_host
   return guarded([&] {
     need(m, "groot_forward");
     need(g, "groot_forward");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     auto* gg = const_cast<groot_graph*>(g);
     DevBuf<uint8_t> cls(g->n);
     DevBuf<float> lg(static_cast<size_t>(g->n) * m->classes);
@@ -807,6 +886,8 @@ int groot_debug_forward_naive(const groot_model* m, const groot_graph* g, float*
   return guarded([&] {
     need(m, "groot_debug_forward_naive");
     need(g, "groot_debug_forward_naive");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     auto* gg = const_cast<groot_graph*>(g);
     DevBuf<uint8_t> cls(g->n);
     DevBuf<float> lg(static_cast<size_t>(g->n) * m->classes);
@@ -822,6 +903,8 @@ int groot_predict_full(const groot_model* m, const groot_graph* g, uint8_t* labe
   return guarded([&] {
     need(m, "groot_predict_full");
     need(g, "groot_predict_full");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     auto* gg = const_cast<groot_graph*>(g);
     DevBuf<uint8_t> cls(g->n);
     DevBuf<unsigned long long> conf(25);
@@ -840,6 +923,8 @@ int groot_predict_full_dev(const groot_model* m, const groot_graph* g, uint8_t* 
   return guarded([&] {
     need(m, "groot_predict_full_dev");
     need(g, "groot_predict_full_dev");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     need(labels_dev, "groot_predict_full_dev");
     forward_device(m, const_cast<groot_graph*>(g), labels_dev, logits_dev,
                    reinterpret_cast<unsigned long long*>(confusion_dev));
@@ -851,6 +936,8 @@ int groot_layer_dev(const groot_model* m, const groot_graph* g, uint32_t layer, 
   return guarded([&] {
     need(m, "groot_layer_dev");
     need(g, "groot_layer_dev");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     if (layer >= m->depth) fail(GROOT_EINVAL, "layer: index out of range");
     const bool last = layer + 1 == m->depth;
     if (layer > 0 && !hin_dev) fail(GROOT_EINVAL, "layer: input activations required for layer >= 1");
@@ -867,22 +954,23 @@ int groot_predict(const groot_model* m, const groot_graph* g, const groot_parts*
   return guarded([&] {
     need(m, "groot_predict");
     need(g, "groot_predict");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     need(p, "groot_predict");
     std::vector<uint64_t> node_off;
     groot_graph* u = union_of_parts(g, p, node_off, nullptr);
     try {
       DevBuf<uint8_t> cls(u->n), out(g->n);
+      DevBuf<unsigned long long> dconf(25);
       out.zero();
-      forward_device(m, u, cls.p, nullptr, nullptr);
+      dconf.zero();
+      if (u->n) forward_device(m, u, cls.p, nullptr, nullptr);
       scatter_core_labels(p, node_off, cls.p, out.p);
-      std::vector<uint8_t> pred(g->n), truth(g->n);
-      out.download(pred.data(), g->n);
-      g->labels.download(truth.data(), g->n);
+      confusion_device(g->n, out.p, g->labels.p, dconf.p);  // over all n nodes (src/gnn.cpp:265-276)
+      uint64_t conf[25];
+      dconf.download(reinterpret_cast<unsigned long long*>(conf), 25);
+      if (labels_host) out.download(labels_host, g->n);
       stream_sync();
-      uint64_t conf[25] = {0};
-      for (uint32_t v = 0; v < g->n; ++v)
-        if (truth[v] < 5 && pred[v] < 5) ++conf[truth[v] * 5 + pred[v]];
-      if (labels_host) std::copy(pred.begin(), pred.end(), labels_host);
       finish_confusion(conf, g->n, confusion, accuracy);
     } catch (...) {
       delete u;
@@ -897,6 +985,8 @@ int groot_predict_parts(const groot_model* m, const groot_graph* g, const groot_
   return guarded([&] {
     need(m, "groot_predict_parts");
     need(g, "groot_predict_parts");
+    DeviceScope ds_g(g->device);
+    same_device(m, g);
     need(p, "groot_predict_parts");
     need(labels_host, "groot_predict_parts");
     std::vector<uint32_t> ids(part_ids, part_ids + count);
@@ -982,6 +1072,7 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
 int groot_spmm_mean(const groot_graph* g, const float* dense, uint32_t f, float* out) {
   return guarded([&] {
     need(g, "groot_spmm_mean");
+    DeviceScope ds_g(g->device);
     need(dense, "groot_spmm_mean");
     need(out, "groot_spmm_mean");
     if (f == 0) fail(GROOT_EINVAL, "spmm: f must be >= 1");
@@ -996,34 +1087,36 @@ int groot_spmm_mean(const groot_graph* g, const float* dense, uint32_t f, float*
 int groot_spmm_mean_dev(const groot_graph* g, const float* dense_dev, uint32_t f, float* out_dev) {
   return guarded([&] {
     need(g, "groot_spmm_mean_dev");
+    DeviceScope ds_g(g->device);
     if (f == 0) fail(GROOT_EINVAL, "spmm: f must be >= 1");
     spmm_mean_device(const_cast<groot_graph*>(g), dense_dev, f, out_dev);
   });
 }
 
-int groot_spmm_csr(uint32_t rows, uint32_t cols, const uint64_t* rp, const uint32_t* col, const float* vals,
-                   const float* dense, uint32_t f, float* out) {
+int groot_graph_prepare(const groot_graph* g) {
   return guarded([&] {
-    need(rp, "groot_spmm_csr");
-    const uint64_t nnz = rp[rows];
-    if (nnz >= 0xFFFFFFFFull) fail(GROOT_EINVAL, "spmm: nnz must be < 2^32");
-    std::vector<uint32_t> rp32(rows + 1ull);
-    for (uint32_t r = 0; r <= rows; ++r) {
-      if (r && rp[r] < rp[r - 1]) fail(GROOT_EINVAL, "CsrMatrix: row_ptr not monotone");
-      rp32[r] = static_cast<uint32_t>(rp[r]);
-    }
-    for (uint64_t q = 0; q < nnz; ++q)
-      if (col[q] >= cols) fail(GROOT_EINVAL, "CsrMatrix: column index out of range");
-    DevBuf<uint32_t> drp(rows + 1ull), dcol(nnz);
-    DevBuf<float> dval(nnz), dd(static_cast<size_t>(cols) * f), dout(static_cast<size_t>(rows) * f);
-    drp.upload(rp32.data(), rows + 1ull);
-    dcol.upload(col, nnz);
-    if (vals) dval.upload(vals, nnz);
-    dd.upload(dense, static_cast<size_t>(cols) * f);
-    spmm_csr_device(rows, drp.p, dcol.p, vals ? dval.p : nullptr, dd.p, f, dout.p);
-    dout.download(out, static_cast<size_t>(rows) * f);
-    stream_sync();
+    need(g, "groot_graph_prepare");
+    DeviceScope ds(g->device);
+    graph_prepare(const_cast<groot_graph*>(g));
   });
+}
+
+int groot_graph_release_context(const groot_graph* g) {
+  return guarded([&] {
+    need(g, "groot_graph_release_context");
+    DeviceScope ds(g->device);
+    graph_release_context(const_cast<groot_graph*>(g));
+  });
+}
+
+int groot_spmm_csr(uint32_t rows, uint32_t cols, const uint64_t* rp, const uint32_t* col, const float* vals,
+                   const float* dense, uint32_t f, uint32_t hd_threshold, float* out) {
+  return guarded([&] { spmm_csr_host(rows, cols, rp, col, vals, dense, f, hd_threshold, out, spmm_csr_device); });
+}
+
+int groot_spmm_csr_f64(uint32_t rows, uint32_t cols, const uint64_t* rp, const uint32_t* col, const double* vals,
+                       const double* dense, uint32_t f, uint32_t hd_threshold, double* out) {
+  return guarded([&] { spmm_csr_host(rows, cols, rp, col, vals, dense, f, hd_threshold, out, spmm_csr_device_f64); });
 }
 
 }  // extern "C"

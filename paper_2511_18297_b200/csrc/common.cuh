@@ -35,7 +35,25 @@ inline void require(bool ok, const char* msg) {
   } while (0)
 
 extern std::atomic<uint64_t> g_launches;
+constexpr int kMaxDevices = 64;
+int current_device();
+// The library stream of the calling thread's current device (groot_set_stream).
 cudaStream_t stream();
+
+// Makes `dev` the current device for a scope (restored on exit): entry points
+// taking a handle run on the device that owns it.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
 
 // Launch helper: counts launches (bench evidence) and checks the launch.
 #define GROOT_LAUNCH(kernel, grid, block, smem, ...)                                           \
@@ -148,6 +166,9 @@ struct groot_graph {
   groot::DevBuf<uint8_t> feat;     // 4n, byte j of node v = feature j (== u32 per node)
   groot::DevBuf<uint8_t> labels;   // n
   groot::DevBuf<uint32_t> edges;   // 2*ne (fwd_edges pairs)
+  // every feature byte is 0 or 1 (encode's features always are; host uploads are
+  // scanned): packed byte counters in the layer-0 gathers are exact
+  bool binary_feat = true;
   // Forward-path cache: row classifier output and activation buffers.
   uint32_t hd_threshold = 0;
   uint32_t num_hd = 0;
@@ -179,11 +200,13 @@ struct groot_graph {
 };
 
 struct groot_assignment {
+  int device = 0;
   uint32_t n = 0, k = 0;
   groot::DevBuf<uint32_t> part_of;
 };
 
 struct groot_parts {
+  int device = 0;
   uint32_t k = 0;
   int with_boundary = 1;
   std::vector<uint64_t> core_off, bnd_off, edge_off;  // host copies, k+1 each
@@ -193,6 +216,7 @@ struct groot_parts {
 };
 
 struct groot_model {
+  int device = 0;                   // weights live on this device
   uint32_t depth = 0, in_dim = 0, hidden = 0, classes = 0;
   std::vector<double> params;       // fp64, ASG1 order (host copy)
   groot::DevBuf<float> l0;          // layer 0: Ws[4x32], Wn[4x32], b[32]

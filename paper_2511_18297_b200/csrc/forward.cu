@@ -27,8 +27,10 @@
 #include <cub/cub.cuh>
 #include <cuda.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 
@@ -861,6 +863,7 @@ struct Layer0Args {
   const uint32_t* feat;
   HdInfo hd;  // mean width 4
   float* hout;
+  uint32_t binary;  // every feature byte is 0/1: neighbour words summed as packed byte counters
 };
 
 constexpr int kL0Threads = 256;
@@ -880,7 +883,10 @@ __global__ void __launch_bounds__(kL0Threads) sage_layer0_kernel(const Layer0Arg
     }
     const bool is_hd = d >= a.hd.threshold;
     const uint32_t dl = is_hd ? 0u : d;
-    uint32_t packed = 0;
+    // per-feature neighbour sums: binary features as packed byte counters
+    // (exact: an LD row has < 256 neighbours), any other u8 values in four
+    // separate u32 counters (the reference sums arbitrary u8 features)
+    uint32_t cnt[4] = {0u, 0u, 0u, 0u};
     {
       uint32_t c[8];
 #pragma unroll
@@ -888,9 +894,24 @@ __global__ void __launch_bounds__(kL0Threads) sage_layer0_kernel(const Layer0Arg
       uint32_t f[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) f[k] = (static_cast<uint32_t>(k) < dl) ? __ldg(a.feat + c[k]) : 0u;
+      if (a.binary) {
+        uint32_t packed = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) packed += f[k];
-      for (uint32_t k = 8; k < dl; ++k) packed += __ldg(a.feat + __ldg(a.col + b + k));
+        for (int k = 0; k < 8; ++k) packed += f[k];
+        for (uint32_t k = 8; k < dl; ++k) packed += __ldg(a.feat + __ldg(a.col + b + k));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cnt[q] = (packed >> (8 * q)) & 0xFFu;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cnt[q] += (f[k] >> (8 * q)) & 0xFFu;
+        for (uint32_t k = 8; k < dl; ++k) {
+          const uint32_t x = __ldg(a.feat + __ldg(a.col + b + k));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cnt[q] += (x >> (8 * q)) & 0xFFu;
+        }
+      }
     }
     float m[4];
     if (is_hd) {
@@ -899,7 +920,7 @@ __global__ void __launch_bounds__(kL0Threads) sage_layer0_kernel(const Layer0Arg
     } else {
       const float inv = d > 0 ? 1.0f / static_cast<float>(d) : 0.0f;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) m[k] = static_cast<float>((packed >> (8 * k)) & 0xFFu) * inv;
+      for (int k = 0; k < 4; ++k) m[k] = static_cast<float>(cnt[k]) * inv;
     }
     const uint32_t x = row < a.n ? __ldg(a.feat + row) : 0u;
     float xk[4];
@@ -1394,23 +1415,54 @@ __global__ void __launch_bounds__(64) l1_xform_kernel(const float* __restrict__ 
   (threadIdx.x < 32 ? tn : ts)[k * kF + o] = static_cast<float>(acc);
 }
 
-// General CSR SpMM (spmm::execute over CsrMatrix<float>): 8 lanes per row,
-// columns strided by 8, nonzeros accumulated in order. vals == nullptr -> 1/deg.
+// General CSR SpMM (spmm::execute over CsrMatrix<T>, T = float or double): 8
+// lanes per row, columns strided by 8, nonzeros accumulated in order with
+// separately rounded multiply and add (no FMA contraction), i.e. the
+// reference's dst[c] += v * src[c] (inc/spmm.hpp:117-124) bit for bit.
+// vals == nullptr -> 1/deg.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// hd_threshold > 0: rows of degree >= hd_threshold are summed as execute's HD
+// band does (src/spmm.cpp:73-96, inc/spmm.hpp:141-157): 32 chunks, the
+// remainder on the trailing chunks, each chunk summed from zero, the chunk
+// partials added in ascending order -- bitwise the reference's execute for a
+// plan with that threshold. hd_threshold == 0: the plain row loop
+// (reference_spmm, inc/spmm.hpp:183-195).
+template <class T>
 __global__ void __launch_bounds__(256) spmm_generic_kernel(uint32_t rows, const uint32_t* __restrict__ rp,
                                                            const uint32_t* __restrict__ col,
-                                                           const float* __restrict__ vals,
-                                                           const float* __restrict__ dense, uint32_t f,
-                                                           float* __restrict__ out) {
+                                                           const T* __restrict__ vals,
+                                                           const T* __restrict__ dense, uint32_t f,
+                                                           T* __restrict__ out, uint32_t hd_threshold) {
   const int j = threadIdx.x & 7;
   const uint32_t groups = gridDim.x * (blockDim.x >> 3);
   for (uint32_t r = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); r < rows; r += groups) {
-    const uint32_t b = rp[r], e = rp[r + 1];
-    const float inv = e > b ? 1.0f / static_cast<float>(e - b) : 0.0f;
+    const uint32_t b = rp[r], e = rp[r + 1], d = e - b;
+    const T inv = e > b ? T(1) / static_cast<T>(d) : T(0);
+    auto sum = [&](uint32_t q0, uint32_t q1, uint32_t c) {
+      T acc = T(0);
+      for (uint32_t q = q0; q < q1; ++q) {
+        const T v = vals ? vals[q] : inv;
+        acc = add_rn(acc, mul_rn(v, dense[static_cast<size_t>(col[q]) * f + c]));
+      }
+      return acc;
+    };
+    const bool hd = hd_threshold && d >= hd_threshold;
     for (uint32_t c = j; c < f; c += 8) {
-      float acc = 0.f;
-      for (uint32_t q = b; q < e; ++q) {
-        const float v = vals ? vals[q] : inv;
-        acc += v * dense[static_cast<size_t>(col[q]) * f + c];
+      T acc = T(0);
+      if (hd) {
+        const uint32_t qd = d / 32, rem = d % 32;
+        uint32_t nz = b;
+        for (uint32_t k = 0; k < 32; ++k) {
+          const uint32_t len = qd + (k >= 32 - rem ? 1u : 0u);
+          acc = add_rn(acc, sum(nz, nz + len, c));
+          nz += len;
+        }
+      } else {
+        acc = sum(b, e, c);
       }
       out[static_cast<size_t>(r) * f + c] = acc;
     }
@@ -1690,9 +1742,10 @@ static CUtensorMap make_rows32_tmap(float* base, uint32_t n, uint32_t box_rows) 
   return m;
 }
 
-static void set_tc_smem() {
-  static bool done = false;
-  if (done) return;
+static void set_tc_smem() {  // a per-device function attribute: once per device
+  static std::atomic<bool> done[kMaxDevices];
+  const int dev = current_device();
+  if (done[dev].load()) return;
   constexpr uint32_t kS0 = TkCfg<false>::kSmem, kS1 = TkCfg<true>::kSmem;
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS0));
@@ -1700,7 +1753,7 @@ static void set_tc_smem() {
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLayer, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeLast, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
   GROOT_CUDA(cudaFuncSetAttribute(sage_tile_kernel<kModeXform, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kS1));
-  done = true;
+  done[dev].store(true);
 }
 
 // Per-graph preparation shared by the whole forward and the layer API:
@@ -1732,7 +1785,7 @@ static void prepare_graph(const groot_model* m, groot_graph* g) {
 // keyable; the first forward on a graph finds that out (one host sync).
 static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   const char* e = std::getenv("GROOT_L0_KEYED");
-  if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2) return false;
+  if ((e && std::atoi(e) == 0) || m->depth < 2 || g->n == 0 || g->l0_mode == 2 || !g->binary_feat) return false;
   // small graphs: the key passes' fixed launch cost exceeds the layer-0 rows they save
   const char* mr = std::getenv("GROOT_L0_KEYED_MIN_ROWS");
   if (g->n < (mr ? std::strtoull(mr, nullptr, 10) : (1ull << 20))) return false;
@@ -1801,7 +1854,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
       GROOT_LAUNCH(hd_mean_feat_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd,
                    g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), g->hd_mean.p);
     }
-    Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), hd, hout};
+    Layer0Args l0{n, g->rp.p, g->col.p, reinterpret_cast<const uint32_t*>(g->feat.p), hd, hout, g->binary_feat ? 1u : 0u};
     {
       ProfScope ps("sage_layer0");
       GROOT_LAUNCH(sage_layer0_kernel, blocks_for(n, kL0Threads, sms * 8), kL0Threads, 0, l0,
@@ -1922,21 +1975,23 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   const bool keyed = layer0_keyed(m, g);
   for (uint32_t l = keyed ? 1 : 0; l + 1 < D; ++l)
     layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, g->act[l & 1].p, cls, nullptr, 0, ~0u, true, keyed);
-  static cudaStream_t side = [] {
-    cudaStream_t st;
-    GROOT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    return st;
-  }();
-  static cudaEvent_t ev_half = [] {
-    cudaEvent_t e;
-    GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return e;
-  }();
-  static cudaEvent_t ev_side = [] {
-    cudaEvent_t e;
-    GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return e;
-  }();
+  // read-back stream: one per device (created once); events per call, so
+  // concurrent calls on different devices or threads share nothing
+  static std::mutex side_mu;
+  static cudaStream_t side_of[kMaxDevices] = {};
+  cudaStream_t side;
+  {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(side_mu);
+    if (!side_of[dev]) GROOT_CUDA(cudaStreamCreateWithFlags(&side_of[dev], cudaStreamNonBlocking));
+    side = side_of[dev];
+  }
+  struct Ev {
+    cudaEvent_t e = nullptr;
+    Ev() { GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    ~Ev() { if (e) cudaEventDestroy(e); }
+  } evh, evs;
+  cudaEvent_t ev_half = evh.e, ev_side = evs.e;
   // the last layer in kReadbackParts tile ranges: the classes of the copies a
   // range completes go to the host on the side stream while the next computes
   constexpr uint32_t kReadbackParts = 4;
@@ -1975,6 +2030,14 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
     GROOT_LAUNCH(confusion_kernel, blocks_for(g->n / 16 + 1, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
                  g->labels.p, confusion);
   }
+}
+
+// confusion[truth][pred] += over rows (device counts; labels >= 5 are skipped)
+void confusion_device(uint32_t n, const uint8_t* cls, const uint8_t* labels, unsigned long long* conf) {
+  if (n == 0) return;
+  ProfScope ps("confusion");
+  GROOT_LAUNCH(confusion_kernel, blocks_for(n / 16 + 1, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, n, cls,
+               labels, conf);
 }
 
 // Naive path (tests): same math, thread per row, plain loads.
@@ -2022,15 +2085,61 @@ void spmm_mean_device(groot_graph* g, const float* dense, uint32_t f, float* out
     HeadW hw{};
     GROOT_LAUNCH(sage_tile_kernel<kModeSpmm>, std::min<uint32_t>(ntiles, sms), kThreads, TkCfg<false>::kSmem, a, hw, tmap_in);
   } else {
-    GROOT_LAUNCH(spmm_generic_kernel, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
-                 nullptr, dense, f, out);
+    GROOT_LAUNCH(spmm_generic_kernel<float>, blocks_for(g->n, 32, num_sms() * 16), 256, 0, g->n, g->rp.p, g->col.p,
+                 nullptr, dense, f, out, 0u);
   }
 }
 
 void spmm_csr_device(uint32_t rows, const uint32_t* rp, const uint32_t* col, const float* vals, const float* dense,
-                     uint32_t f, float* out) {
+                     uint32_t f, float* out, uint32_t hd_threshold) {
   if (rows == 0) return;
-  GROOT_LAUNCH(spmm_generic_kernel, blocks_for(rows, 32, num_sms() * 16), 256, 0, rows, rp, col, vals, dense, f, out);
+  GROOT_LAUNCH(spmm_generic_kernel<float>, blocks_for(rows, 32, num_sms() * 16), 256, 0, rows, rp, col, vals, dense, f, out,
+               hd_threshold);
+}
+
+void spmm_csr_device_f64(uint32_t rows, const uint32_t* rp, const uint32_t* col, const double* vals,
+                         const double* dense, uint32_t f, double* out, uint32_t hd_threshold) {
+  if (rows == 0) return;
+  GROOT_LAUNCH(spmm_generic_kernel<double>, blocks_for(rows, 32, num_sms() * 16), 256, 0, rows, rp, col, vals, dense, f,
+               out, hd_threshold);
+}
+
+// make_context (src/gnn.cpp:140-170) on the device: everything the forward
+// derives from the graph alone -- the row classifier (HD band), the tile plan,
+// the HD chunk plan and the activation buffers -- built once and cached on the
+// handle until graph_release_context.
+void graph_prepare(groot_graph* g) {
+  set_tc_smem();
+  classify_rows(g, hd_threshold());
+  if (g->n) {
+    build_tile_plan(g, g->hd_threshold);
+    build_hd_plan(g);
+  }
+  ensure_activations(g);
+  stream_sync();
+}
+
+void graph_release_context(groot_graph* g) {
+  stream_sync();
+  g->hd_threshold = 0;
+  g->num_hd = 0;
+  g->hd_rows.release();
+  g->hd_mean.release();
+  for (auto& b : g->act) b.release();
+  g->tp_threshold = g->tp_halo_cap = g->tp_slow = 0;
+  g->tp_period = g->tp_period_rows = 0;
+  g->tp_meta.release();
+  g->tp_lrp.release();
+  g->tp_lcol.release();
+  g->tp_halo.release();
+  g->hdp_valid = false;
+  g->hdp_nunits = 0;
+  g->hdp_base.release();
+  g->hdp_slot.release();
+  g->hdp_k.release();
+  g->hdp_units.release();
+  g->hdp_partial.release();
+  g->l0_mode = 0;
 }
 
 // Host-side TF32 split (round-to-nearest, ties away — same as cvt.rna.tf32.f32).

@@ -508,6 +508,7 @@ groot_graph* batch(const groot_graph* g, uint32_t copies) {
   const uint64_t n64 = static_cast<uint64_t>(g->n) * copies;
   require(n64 < 0xFFFFFFFFull, "batch: node count exceeds 2^32-1");
   groot_graph* o = graph_alloc(static_cast<uint32_t>(n64), g->ne * copies);
+  o->binary_feat = g->binary_feat;
   try {
     const uint32_t n = g->n;
     GROOT_LAUNCH(batch_rp_kernel, blocks_for(n64, 256), 256, 0, n, copies,
@@ -561,6 +562,7 @@ groot_graph* batch_padded(const groot_graph* g, uint32_t copies, uint32_t P) {
   auto* o = new groot_graph;
   try {
     GROOT_CUDA(cudaGetDevice(&o->device));
+    o->binary_feat = g->binary_feat;
     o->n = static_cast<uint32_t>(n64);
     o->nnz = g->nnz * copies;
     o->ne = 0;
@@ -579,6 +581,13 @@ groot_graph* batch_padded(const groot_graph* g, uint32_t copies, uint32_t P) {
     throw;
   }
   return o;
+}
+
+static bool host_features_binary(const uint8_t* feat, uint64_t bytes) {
+  if (!feat) return true;
+  for (uint64_t i = 0; i < bytes; ++i)
+    if (feat[i] > 1) return false;
+  return true;
 }
 
 groot_graph* graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col,
@@ -605,6 +614,7 @@ groot_graph* graph_from_host(uint32_t n, const uint64_t* rp, const uint32_t* col
     g->col.upload(col, nnz);
     g->feat.alloc(4ull * n);
     if (feat) g->feat.upload(feat, 4ull * n); else g->feat.zero();
+    g->binary_feat = host_features_binary(feat, 4ull * n);
     g->labels.alloc(n);
     if (lab) g->labels.upload(lab, n); else g->labels.zero();
     g->edges.alloc(2 * g->ne);
@@ -622,6 +632,7 @@ groot_graph* graph_from_edges(uint32_t n, const uint8_t* feat, const uint8_t* la
   groot_graph* g = graph_alloc(n, ne);
   try {
     if (feat) g->feat.upload(feat, 4ull * n); else g->feat.zero();
+    g->binary_feat = host_features_binary(feat, 4ull * n);
     if (lab) g->labels.upload(lab, n); else g->labels.zero();
     g->edges.upload(edges, 2 * ne);
     DevBuf<uint32_t> bad(1);
@@ -663,6 +674,7 @@ groot_assignment* topo_chunks(const groot_graph* g, uint32_t k) {
   if (k < 1) fail(GROOT_EINVAL, "partition: k must be >= 1");
   if (k > g->n) fail(GROOT_EINVAL, "partition: k exceeds node count");
   auto* a = new groot_assignment;
+  GROOT_CUDA(cudaGetDevice(&a->device));
   a->n = g->n;
   a->k = k;
   a->part_of.alloc(g->n);
@@ -672,15 +684,21 @@ groot_assignment* topo_chunks(const groot_graph* g, uint32_t k) {
 }
 
 groot_assignment* assignment_from_host(uint32_t n, const uint32_t* part_of) {
-  uint32_t k = 0;
-  for (uint32_t v = 0; v < n; ++v) k = std::max(k, part_of[v] + 1);
-  std::vector<uint8_t> nonempty(k, 0);
-  for (uint32_t v = 0; v < n; ++v) nonempty[part_of[v]] = 1;
-  for (uint32_t p = 0; p < k; ++p)
+  // k = max id + 1 and no part may be empty (src/partition.cpp:384-389). An id
+  // >= n leaves some part in [0, n] empty, so only ids < n are tallied (the
+  // table stays n + 1 entries whatever the ids) and the first empty part is
+  // the one the reference reports.
+  uint64_t k = 0;
+  for (uint32_t v = 0; v < n; ++v) k = std::max<uint64_t>(k, static_cast<uint64_t>(part_of[v]) + 1);
+  std::vector<uint8_t> nonempty(std::min<uint64_t>(k, static_cast<uint64_t>(n) + 1), 0);
+  for (uint32_t v = 0; v < n; ++v)
+    if (part_of[v] < nonempty.size()) nonempty[part_of[v]] = 1;
+  for (uint64_t p = 0; p < nonempty.size(); ++p)
     if (!nonempty[p]) fail(GROOT_ERUNTIME, "assignment: empty partition " + std::to_string(p));
   auto* a = new groot_assignment;
+  GROOT_CUDA(cudaGetDevice(&a->device));
   a->n = n;
-  a->k = k;
+  a->k = static_cast<uint32_t>(k);
   a->part_of.alloc(n);
   a->part_of.upload(part_of, n);
   stream_sync();
@@ -705,8 +723,14 @@ groot_assignment* load_assignment(const char* path, uint32_t n) {
   return assignment_from_host(n, part.data());
 }
 
+// regrow / crossing_fraction / edge_cut walk fwd_edges; a CSR-only upload has none
+void require_fwd_edges(const groot_graph* g) {
+  require(g->nnz == 0 || g->ne > 0, "graph: fwd_edges required (this graph was uploaded as CSR only)");
+}
+
 uint64_t edge_cut(const groot_graph* g, const groot_assignment* a) {
   require(a->n == g->n, "regrow: assignment size mismatch");
+  require_fwd_edges(g);
   DevBuf<unsigned long long> cut(1);
   cut.zero();
   if (g->ne)
@@ -728,8 +752,10 @@ static void sort_pairs_by_part(uint32_t k, const uint32_t* kin, uint32_t* kout, 
 
 groot_parts* regrow(const groot_graph* g, const groot_assignment* a, int with_b) {
   if (a->n != g->n) fail(GROOT_EINVAL, "regrow: assignment size mismatch");
+  require_fwd_edges(g);
   const uint32_t n = g->n, k = a->k;
   auto* P = new groot_parts;
+  GROOT_CUDA(cudaGetDevice(&P->device));
   try {
     P->k = k;
     P->with_boundary = with_b;
@@ -822,6 +848,49 @@ groot_parts* regrow(const groot_graph* g, const groot_assignment* a, int with_b)
   return P;
 }
 
+// vector<AugmentedPartition> given by the caller (host arrays, concatenated
+// per part with k+1 offsets) -> device parts, validated like materialize's
+// inputs: global ids < n, local edge endpoints < the part's size.
+groot_parts* parts_from_host(uint32_t n, uint32_t k, const uint64_t* core_off, const uint32_t* core,
+                             const uint64_t* bnd_off, const uint32_t* bnd, const uint64_t* edge_off,
+                             const uint32_t* edges) {
+  require(k >= 1, "parts: at least one partition required");
+  require(core_off && bnd_off && edge_off, "parts: null offsets");
+  for (uint32_t p = 0; p < k; ++p)
+    require(core_off[p] <= core_off[p + 1] && bnd_off[p] <= bnd_off[p + 1] && edge_off[p] <= edge_off[p + 1],
+            "parts: offsets not monotone");
+  require(core_off[0] == 0 && bnd_off[0] == 0 && edge_off[0] == 0, "parts: offsets must start at 0");
+  for (uint64_t i = 0; i < core_off[k]; ++i) require(core[i] < n, "parts: core node id out of range");
+  for (uint64_t i = 0; i < bnd_off[k]; ++i) require(bnd[i] < n, "parts: boundary node id out of range");
+  bool any_bnd = false;
+  for (uint32_t p = 0; p < k; ++p) {
+    const uint64_t size = (core_off[p + 1] - core_off[p]) + (bnd_off[p + 1] - bnd_off[p]);
+    any_bnd = any_bnd || bnd_off[p + 1] > bnd_off[p];
+    for (uint64_t e = edge_off[p]; e < edge_off[p + 1]; ++e)
+      require(edges[2 * e] < size && edges[2 * e + 1] < size, "parts: local edge endpoint out of range");
+  }
+  auto* P = new groot_parts;
+  try {
+    GROOT_CUDA(cudaGetDevice(&P->device));
+    P->k = k;
+    P->with_boundary = any_bnd ? 1 : 0;
+    P->core_off.assign(core_off, core_off + k + 1);
+    P->bnd_off.assign(bnd_off, bnd_off + k + 1);
+    P->edge_off.assign(edge_off, edge_off + k + 1);
+    P->core.alloc(core_off[k]);
+    P->core.upload(core, core_off[k]);
+    P->bnd.alloc(bnd_off[k]);
+    P->bnd.upload(bnd, bnd_off[k]);
+    P->edges.alloc(2 * edge_off[k]);
+    P->edges.upload(edges, 2 * edge_off[k]);
+    stream_sync();
+  } catch (...) {
+    delete P;
+    throw;
+  }
+  return P;
+}
+
 // Nodes of part p in local order (cores then boundary) -> device l2g.
 static void part_l2g(const groot_parts* P, uint32_t p, uint32_t* d_l2g) {
   const uint64_t nc = P->core_off[p + 1] - P->core_off[p];
@@ -839,6 +908,7 @@ groot_graph* materialize(const groot_graph* g, const groot_parts* P, uint32_t p)
   const uint64_t ne = P->edge_off[p + 1] - P->edge_off[p];
   const uint32_t n = static_cast<uint32_t>(nc + nb);
   groot_graph* o = graph_alloc(n, ne);
+  o->binary_feat = g->binary_feat;
   try {
     DevBuf<uint32_t> l2g(n);
     part_l2g(P, p, l2g.p);
@@ -877,6 +947,7 @@ groot_graph* union_of_parts(const groot_graph* g, const groot_parts* P, std::vec
   for (uint32_t p = 0; p < k; ++p) eoff[p + 1] = eoff[p] + (use[p] ? P->edge_off[p + 1] - P->edge_off[p] : 0);
   const uint64_t ne = eoff[k];
   groot_graph* o = graph_alloc(n, ne);
+  o->binary_feat = g->binary_feat;
   try {
     DevBuf<uint32_t> l2g(n);
     for (uint32_t p = 0; p < k; ++p)

@@ -14,40 +14,45 @@
 namespace groot {
 
 // ---------------------------------------------------------------------------
-// Caching allocator. All library work is ordered on one stream, so a block
-// freed by the host can be handed to the next allocation immediately: any
-// kernel still reading it precedes, in stream order, every kernel that will
-// write it.
+// Caching allocator, one pool per device. All library work on a device is
+// ordered on that device's library stream, so a block freed by the host can
+// be handed to the next allocation immediately: any kernel still reading it
+// precedes, in stream order, every kernel that will write it.
 // ---------------------------------------------------------------------------
 namespace {
 std::mutex g_mem_mu;
-std::multimap<size_t, void*> g_free;             // size -> block
-std::unordered_map<void*, size_t> g_live;         // block -> size
-size_t g_cached_bytes = 0;
+// Per device: cached blocks by size, and the size of every live block.
+struct DevPool {
+  std::multimap<size_t, void*> free_blocks;
+  std::unordered_map<void*, size_t> live;
+  size_t cached_bytes = 0;
+};
+DevPool g_pools[kMaxDevices];
 
 size_t round_size(size_t b) {
   if (b <= (1u << 20)) return (b + 511) & ~size_t(511);
   return (b + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
 }
 
-void release_all_free() {
-  for (auto& kv : g_free) cudaFree(kv.second);
-  g_free.clear();
-  g_cached_bytes = 0;
+void release_all_free(DevPool& pool) {  // the pool's device is current
+  for (auto& kv : pool.free_blocks) cudaFree(kv.second);
+  pool.free_blocks.clear();
+  pool.cached_bytes = 0;
 }
 }  // namespace
 
 void* dev_alloc(size_t bytes) {
   const size_t sz = round_size(bytes);
+  DevPool& pool = g_pools[current_device()];
   std::lock_guard<std::mutex> lk(g_mem_mu);
   // best fit among cached blocks no more than 25% (+2 MB) larger than needed
-  auto it = g_free.lower_bound(sz);
-  if (it != g_free.end() && it->first <= sz + sz / 4 + (2u << 20)) {
+  auto it = pool.free_blocks.lower_bound(sz);
+  if (it != pool.free_blocks.end() && it->first <= sz + sz / 4 + (2u << 20)) {
     void* p = it->second;
     const size_t have = it->first;
-    g_free.erase(it);
-    g_cached_bytes -= have;
-    g_live[p] = have;
+    pool.free_blocks.erase(it);
+    pool.cached_bytes -= have;
+    pool.live[p] = have;
     return p;
   }
   void* p = nullptr;
@@ -55,31 +60,41 @@ void* dev_alloc(size_t bytes) {
   if (e != cudaSuccess) {
     cudaGetLastError();
     cudaDeviceSynchronize();
-    release_all_free();
+    release_all_free(pool);
     e = cudaMalloc(&p, sz);
     if (e != cudaSuccess) {
       cudaGetLastError();
       fail(GROOT_ECUDA, "device allocation of " + std::to_string(sz) + " bytes failed: " + cudaGetErrorString(e));
     }
   }
-  g_live[p] = sz;
+  pool.live[p] = sz;
   return p;
 }
 
 void dev_free(void* p) {
   if (!p) return;
   std::lock_guard<std::mutex> lk(g_mem_mu);
-  auto it = g_live.find(p);
-  if (it == g_live.end()) return;
-  g_free.emplace(it->second, p);
-  g_cached_bytes += it->second;
-  g_live.erase(it);
+  for (DevPool& pool : g_pools) {  // the block's owner (free may run with another device current)
+    auto it = pool.live.find(p);
+    if (it == pool.live.end()) continue;
+    pool.free_blocks.emplace(it->second, p);
+    pool.cached_bytes += it->second;
+    pool.live.erase(it);
+    return;
+  }
 }
 
 void dev_empty_cache() {
   std::lock_guard<std::mutex> lk(g_mem_mu);
-  cudaDeviceSynchronize();
-  release_all_free();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < kMaxDevices; ++d) {
+    if (g_pools[d].free_blocks.empty()) continue;
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();
+    release_all_free(g_pools[d]);
+  }
+  cudaSetDevice(cur);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,6 +1,7 @@
 // Exercises the C++ drop-in mirror (include/groot_aigsage.hpp) the way a
 // reference (aigsage) user would call it. Host-only checks always run; the
 // device pipeline runs when a CUDA device is present (argv[1] == "gpu").
+#include <algorithm>
 #include <cassert>
 #include <cmath>
 #include <cstdio>
@@ -50,6 +51,12 @@ int main(int argc, char** argv) {
   CHECK(m.layers.size() == 4 && m.in_dim() == 4 && m.num_classes() == 5 && m.layers[1].w_self.rows() == 32);
   const double lim = std::sqrt(6.0 / 36.0);
   CHECK(std::fabs(m.layers[0].w_self(0, 0)) <= lim);
+  // worker pool surface (inc/worker_pool.hpp)
+  WorkerPool pool(4);
+  std::vector<int> hit(100, 0);
+  pool.for_each(hit.size(), [&](std::size_t i) { hit[i] += 1; });
+  CHECK(pool.workers() == 4 && std::count(hit.begin(), hit.end(), 1) == 100);
+  CHECK(default_pool().workers() >= 1);
   if (!gpu) {
     std::printf("host checks ok\n");
     return 0;
@@ -87,6 +94,59 @@ int main(int argc, char** argv) {
   eye.values = {1, 1, 1};
   auto y = spmm::execute(eye, std::vector<double>{1, 2, 3, 4, 5, 6}, 2);
   CHECK(y == (std::vector<double>{1, 2, 3, 4, 5, 6}));
+  // SageContext (src/gnn.cpp:140-178): host fields as the reference builds them,
+  // and forward(model, ctx) on the prepared resident graph
+  SageContext ctx = make_context(gb);
+  CHECK(ctx.a_mean.rows == gb.n && ctx.a_mean.nnz() == gb.col_idx.size() && ctx.plan.rows == gb.n);
+  CHECK(ctx.a_mean.values[gb.row_ptr[10]] == 1.0 / gb.degree[10]);
+  CHECK(ctx.a_mean_t.values[gb.row_ptr[10]] == 1.0 / gb.degree[gb.col_idx[gb.row_ptr[10]]]);
+  CHECK(ctx.features.rows() == gb.n && ctx.features.cols() == 4 && ctx.labels == gb.labels);
+  RowMat lc = forward(m, ctx);
+  for (std::int64_t i = 0; i < lg.size(); ++i) CHECK(lc.data()[i] == lg.data()[i]);
+  // spmm surface: degree_sort, build_plan, execute (bitwise the plain loop here: no HD rows at 8 bits)
+  std::vector<std::uint64_t> rp3 = {0, 3, 4, 6};
+  spmm::DegreeSort ds = spmm::degree_sort(3, rp3);
+  CHECK((ds.perm == std::vector<std::uint32_t>{1, 2, 0}) && ds.sorted_row_ptr.back() == 6);
+  ctx.a_mean.validate();
+  CHECK(ctx.plan.hd_rows.empty() && !ctx.plan.work_units.empty() && ctx.plan.nnz == ctx.a_mean.nnz());
+  std::vector<double> x(static_cast<std::size_t>(gb.n) * 4);
+  for (std::size_t i = 0; i < x.size(); ++i) x[i] = std::sin(0.37 * static_cast<double>(i));
+  std::vector<double> y1 = spmm::execute(ctx.plan, ctx.a_mean, x, 4, &default_pool());
+  std::vector<double> y0(x.size(), 0.0);
+  for (std::uint32_t r = 0; r < gb.n; ++r)
+    for (std::uint64_t q = gb.row_ptr[r]; q < gb.row_ptr[r + 1]; ++q)
+      for (int c = 0; c < 4; ++c) y0[4 * r + c] += ctx.a_mean.values[q] * x[4ull * gb.col_idx[q] + c];
+  CHECK(y1 == y0);
+  CHECK(spmm::reference_spmm(ctx.a_mean, x, 4) == y0);
+  bool mismatch = false;
+  try {
+    spmm::execute(ctx.plan, eye, std::vector<double>{1, 2, 3}, 1);
+  } catch (const std::invalid_argument& e) {
+    mismatch = std::string(e.what()) == "spmm::execute: plan does not match matrix";
+  }
+  CHECK(mismatch);
+  spmm::CsrMatrix<float> af;
+  af.rows = af.cols = gb.n;
+  af.row_ptr = gb.row_ptr;
+  af.col_idx = gb.col_idx;
+  af.values.assign(gb.col_idx.size(), 0.5f);
+  spmm::BenchReport br = spmm::bench(af, 32, 3);
+  CHECK(br.exec_ms > 0 && br.baseline_ms > 0 && br.reps == 3);
+  // predict consumes the parts it is given: core_subgraphs' parts == regrow's parts with boundaries cut off
+  auto cut = regrow(gb, pa);
+  for (auto& p : cut) {
+    const std::uint32_t nc = p.num_core();
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> keep;
+    for (auto& e : p.edges)
+      if (e.first < nc && e.second < nc) keep.push_back(e);
+    p.edges = keep;
+    p.boundary_nodes.clear();
+    p.local_to_global.resize(nc);
+  }
+  CHECK(predict(m, gb, cut).labels == predict(m, gb, core).labels);
+  std::uint64_t cross = 0;
+  for (const auto& [u, v] : gb.fwd_edges) cross += pa.part_of[u] != pa.part_of[v];
+  CHECK(edge_cut(gb, pa) == cross && crossing_fraction(gb, pa) == static_cast<double>(cross) / gb.fwd_edges.size());
   std::printf("device checks ok (accuracy %.4f)\n", full.accuracy);
   return 0;
 }

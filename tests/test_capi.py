@@ -117,3 +117,24 @@ def test_compute_without_device_fails_loudly():
     c = api.gen_csa_multiplier(2)
     with pytest.raises(GrootError):
         api.encode(c.aig, c.labels)
+
+
+def test_assignment_ids_beyond_n_are_rejected_before_sizing():
+    """a part id >= n (e.g. -1 cast to u32) must not size the empty-part
+    table by the id; the reference reports the first empty partition."""
+    from paper_2511_18297_b200 import api
+    for bad, first_empty in ((0xFFFFFFFF, 2), (7, 2), (3, 2)):
+        part = np.array([0, 1, bad, 1], np.uint32)
+        with pytest.raises(RuntimeError, match=f"assignment: empty partition {first_empty}$"):
+            api.PartitionAssignment.from_host(part)
+
+
+def test_parts_from_host_validation():
+    from paper_2511_18297_b200 import api
+    P = api.AugmentedPartition
+    bad_core = [P(np.array([0, 9], np.uint32), np.zeros(0, np.uint32), np.zeros((0, 2), np.uint32))]
+    with pytest.raises(ValueError, match="core node id out of range"):
+        api.AugmentedPartitions.from_host(5, bad_core)
+    bad_edge = [P(np.array([0, 1], np.uint32), np.array([2], np.uint32), np.array([[0, 3]], np.uint32))]
+    with pytest.raises(ValueError, match="local edge endpoint out of range"):
+        api.AugmentedPartitions.from_host(5, bad_edge)

@@ -155,3 +155,95 @@ def test_regrow_laws_random_graphs():
         total = sum(P.edges.shape[0] for P in parts)
         cross = int((part[edges[:, 0]] != part[edges[:, 1]]).sum()) if E else 0
         assert total == E + cross
+
+
+# ---------------------------------------------------------------------------
+# (2) the restatement against the reference library itself (oracle/_ref)
+# ---------------------------------------------------------------------------
+def _ref():
+    from oracle import pyref as R
+    if not R.available():
+        pytest.skip("oracle/_ref (the compiled reference) is not built")
+    return R
+
+
+@pytest.mark.parametrize("width,copies", [(3, 2), (16, 1), (33, 3), (64, 4), (128, 2)])
+def test_restatement_vs_reference_graph_stages(width, copies):
+    """gen_csa/encode/batch/topo/regrow/core_subgraphs/materialize/crossing, bit-exact."""
+    R = _ref()
+    raig, rg = R.gen_csa(width)
+    a = O.gen_csa(width)
+    np.testing.assert_array_equal(a.and_lits, raig.and_lits)
+    np.testing.assert_array_equal(a.out_lits, raig.out_lits)
+    np.testing.assert_array_equal(a.labels, raig.labels)
+    g = O.batch(O.encode(a), copies) if copies > 1 else O.encode(a)
+    rb = R.batch(rg, copies) if copies > 1 else rg
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(g, f), rb.field(f), err_msg=f)
+    for k in (1, 2, 5, 16):
+        part = O.topo_chunks(g.n, k)
+        np.testing.assert_array_equal(part, R.topo_chunks(rb, k))
+        assert O.crossing_fraction(g, part) == R.crossing_fraction(rb, part, k)
+        for wb in (True, False):
+            parts = O.regrow(g, part, k, wb)
+            rparts = R.RefParts(rb, part, k, wb)
+            assert O.footprint_proxy(parts) == rparts.footprint_proxy()
+            for p in range(k):
+                rp_ = rparts.part(p)
+                np.testing.assert_array_equal(parts[p].core_nodes, rp_.core_nodes)
+                np.testing.assert_array_equal(parts[p].boundary_nodes, rp_.boundary_nodes)
+                np.testing.assert_array_equal(parts[p].edges, rp_.edges)
+            m = O.materialize(g, parts[k - 1])
+            rm = rparts.materialize(k - 1)
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(m, f), rm.field(f), err_msg=f"materialize {f}")
+
+
+def test_restatement_vs_reference_random_assignments():
+    """regrow on random multigraphs with arbitrary (file-style) assignments."""
+    R = _ref()
+    rng = np.random.default_rng(17)
+    for t in range(8):
+        ni = int(rng.integers(2, 12))
+        na = int(rng.integers(1, 400))
+        ands = np.empty((na, 2), np.uint32)
+        for q in range(na):
+            v = 1 + ni + q
+            ands[q] = 2 * rng.integers(0, v, 2) + rng.integers(0, 2, 2)
+        outs = (2 * rng.integers(0, 1 + ni + na, 5) + rng.integers(0, 2, 5)).astype(np.uint32)
+        raig, rg = R.aig_from_lits(ni, ands, outs)
+        g = O.encode(O.Aig(ni, ands, outs, raig.labels))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(g, f), rg.field(f), err_msg=f)
+        k = int(rng.integers(1, 9))
+        part = rng.integers(0, k, g.n).astype(np.uint32)
+        part[:k] = np.arange(k)
+        parts = O.regrow(g, part, k, True)
+        rparts = R.RefParts(rg, part, k, True)
+        for p in range(k):
+            np.testing.assert_array_equal(parts[p].edges, rparts.part(p).edges)
+            np.testing.assert_array_equal(parts[p].boundary_nodes, rparts.part(p).boundary_nodes)
+
+
+@pytest.mark.parametrize("width,copies,seed", [(8, 1, 7), (32, 2, 3), (64, 1, 11)])
+def test_restatement_vs_reference_plan_and_forward(width, copies, seed):
+    """build_plan arrays bit-exact; fp64 logits of the restated forward (restated
+    spmm::execute) vs the shim's forward over the compiled spmm::execute."""
+    R = _ref()
+    _, rg = R.gen_csa(width)
+    rb = R.batch(rg, copies) if copies > 1 else rg
+    g = O.batch(O.encode(O.gen_csa(width)), copies) if copies > 1 else O.encode(O.gen_csa(width))
+    for thr in ((512, 12, 96), (16, 3, 24)):
+        op = O.build_plan(g.row_ptr, *thr)
+        rp_ = R.build_plan(g.row_ptr, *thr)
+        for key in ("hd_rows", "mid_rows", "ld_groups", "units", "perm"):
+            np.testing.assert_array_equal(op[key], rp_[key], err_msg=key)
+        O.free_plan(op)
+        R.free_plan(rp_)
+    prm = O.init_model(seed)
+    pred, conf, acc, lg = O.predict_full(g, prm)
+    rpred, rconf, racc, rlg = R.predict_full(rb, prm, want_logits=True)
+    np.testing.assert_array_equal(lg, rlg)  # same accumulation order end to end
+    np.testing.assert_array_equal(pred, rpred)
+    np.testing.assert_array_equal(conf, rconf)
+    assert acc == racc
