@@ -375,10 +375,17 @@ def test_empty_and_edge_cases(api):
 def test_large_batch_copy_consistency(api, golden_dir):
     """Size-independent property at a BASELINE size: every batch copy of the
     512-bit b16 graph gets exactly the classes of the single copy, and the
-    single copy matches the oracle."""
-    model = api.Model.from_params(trained_params(golden_dir))
+    single copy's classes match the compiled reference's predict_full on every
+    node outside fp64 near-ties."""
+    from oracle import pyref as R
+    prm = trained_params(golden_dir)
+    model = api.Model.from_params(prm)
     g1 = dev_graph(api, 512)
     p1 = api.predict_full(model, g1).labels
+    _, rg = R.gen_csa(512)
+    rpred, _, _, rlog = R.predict_full(rg, prm, want_logits=True)
+    check_classes(p1, rlog, "csa512 b1")
+    assert ((p1 != rpred) & (p1 != np.argmax(rlog, 1))).sum() == 0
     gb = dev_graph(api, 512, 16)
     assert gb.n == 16 * g1.n
     pb = api.predict_full(model, gb).labels.reshape(16, -1)
