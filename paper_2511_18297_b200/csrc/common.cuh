@@ -225,6 +225,7 @@ struct groot_model {
   groot::DevBuf<float> bias;        // layers >= 1: 32 each
   groot::DevBuf<float> naive_w;     // fp32 row-major weights for the naive debug path
   groot::DevBuf<float> head;        // W_out[32 x classes] then b_out[classes]
+  groot::DevBuf<uint32_t> hbimg;    // last layer's tensor-core head: 4 KB W_out smem image (hi/lo)
   float headw[32 * 8 + 8 + 32];     // same, classes padded to 8, + layer bias; kernel parameters
   std::vector<float> bias_h;        // layers >= 1 biases (host copy for the parameter block)
 };

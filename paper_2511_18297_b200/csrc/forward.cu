@@ -60,6 +60,15 @@ constexpr uint32_t kTmemCols = 512;
 static_assert(kAccCol0 + 2 * kAccCols <= kTmemCols, "tensor memory budget");
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr int kMaxClasses = 8;
+// Last layer: the 32 -> classes head runs on the tensor core too. The epilogue
+// writes relu(acc + b) split into TF32 hi (over the accumulator it just read)
+// and lo (kHeadLoCol); one MMA group of N = 16 (classes zero-padded) leaves the
+// logits in kHeadDCol.
+constexpr uint32_t kHeadN = 16;
+constexpr uint32_t kHeadLoCol = kAccCol0 + 2 * kAccCols;  // 448
+constexpr uint32_t kHeadDCol = kHeadLoCol + kAccCols;     // 480
+static_assert(kHeadDCol + kHeadN <= kTmemCols, "tensor memory budget (head)");
+constexpr uint32_t kHeadBBytes = 2 * kHeadN * 128;        // W_out hi/lo, K-major SW128, N = 16 rows
 // Column c (0..31) of an A block in tensor memory holds input feature
 // kcol_feature(c): lane j of a row's 4-lane group loads features 8j..8j+7
 // (one 32-byte load) and 16x256b stores put its values in columns 8i+2j+e.
@@ -170,6 +179,7 @@ struct LayerArgs {
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
   const float* ktable_self;   // kModeXform: Ts (entry rows . W_self)
+  const uint32_t* hbimg;      // kModeLast: 4 KB W_out image (hi/lo), K permuted by kcol_feature, N padded to 16
   const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused; tiles x 128), see l0_key_kernel
   const uint8_t* hids;        //                entry ids of the halo rows (tiles x kTpHaloCap, as the halo list)
   const float* ktable;        //                kTkTableRows x 32 rows of the entries
@@ -241,9 +251,9 @@ struct TkCfg {
   static constexpr int kMetaLead = kMetaStages - kRowStages;
   static constexpr uint32_t kRowMem = kKeyed ? 0u : kRowStages * kTkRowBytes;
   static constexpr uint32_t kTableMem = kKeyed ? 2u * kTkTableRows * 128u : 0u;  // entry rows (Tn) | Ts
-  static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes +
+  static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes + kHeadBBytes +
                                     (256 + 32 + kTileRing) * 4 + 16 * kMetaStages +
-                                    8 * (2 * kStages + 4 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
+                                    8 * (2 * kStages + 5 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
   static_assert(kMetaLead + kRowStages + kStages + 4 < static_cast<int>(kTileRing), "tile ring covers every role's lag");
   static_assert(kSmem <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
   static_assert(kMetaLead >= 2, "plan records lead the rows");
@@ -299,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   uint8_t* sPlan = sRows + Cfg::kRowMem;                 // [kTkMetaStages] lrp | lcol | halo list
   uint8_t* sTable = sPlan + kTkMetaStages * kTkMetaBytes;  // keyed layer 1: entry rows
   uint8_t* sB = sTable + Cfg::kTableMem;
-  float* sInv = reinterpret_cast<float*>(sB + kBBytes);  // 1/d, d < 256
+  uint8_t* sHB = sB + kBBytes;                            // head W_out image (last layer)
+  float* sInv = reinterpret_cast<float*>(sHB + kHeadBBytes);  // 1/d, d < 256
   float* sBias = sInv + 256;                              // layer bias by output feature
   uint32_t* sTile = reinterpret_cast<uint32_t*>(sBias + 32);  // [kTileRing] tile of iteration i (kEndTile: done)
   uint4* sMeta = reinterpret_cast<uint4*>(sTile + kTileRing);  // [kTkMetaStages] TileMeta of the staged plan
@@ -312,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   uint64_t* m_empty = m_full + kTkMetaStages;
   uint64_t* r_full = m_empty + kTkMetaStages;  // [kTkRowStages] tile + halo rows landed
   uint64_t* r_empty = r_full + kTkRowStages;
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(r_empty + kTkRowStages);
+  uint64_t* hdone = r_empty + kTkRowStages;  // last layer: head MMA of the current tile complete
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(hdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n = a.n;
@@ -323,6 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   if (kMma)
     for (uint32_t i = threadIdx.x; i < kBBytes / 16; i += kThreads)
       reinterpret_cast<uint4*>(sB)[i] = __ldg(reinterpret_cast<const uint4*>(a.bimg) + i);
+  if (kMode == kModeLast)
+    for (uint32_t i = threadIdx.x; i < kHeadBBytes / 16; i += kThreads)
+      reinterpret_cast<uint4*>(sHB)[i] = __ldg(reinterpret_cast<const uint4*>(a.hbimg) + i);
   if (kKeyed)
     for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
       reinterpret_cast<uint4*>(sTable)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
@@ -350,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_init(&r_full[s], 1 + 32 * kCopiers);  // TMA box (expect_tx) + each copier lane's cp.async arrival
       ptx::mbar_init(&r_empty[s], kProdWarps * 32);
     }
+    ptx::mbar_init(hdone, 1);
     ptx::mbar_fence_init();
   }
   if (kMma && warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
@@ -807,23 +823,54 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
                           make_float4(o[4], o[5], o[6], o[7]));
           }
       } else {
+        // last layer: relu(acc + b) split into TF32 hi (written back over the
+        // accumulator just read) and lo, then the 32 -> classes head as one
+        // tensor-core MMA group issued by warp 0 once all four quadrants are in
+        // TMEM; each lane takes its row's logits and the first maximum
         float r[32];
         ptx::tmem_ld_32x32b_x32(tq, r);
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {  // column c holds output feature kcol_feature(c)
+          const float x = fmaxf(r[c] + hw.bias[kcol_feature(c)], 0.0f);
+          hi[c] = __float_as_uint(x) & 0xFFFFE000u;
+          lo[c] = __float_as_uint(x - __uint_as_float(hi[c]));
+        }
+        ptx::tmem_st_32x32b_x32(tq, hi);
+        ptx::tmem_st_32x32b_x32(tmem_base + kHeadLoCol + ((q * 32u) << 16), lo);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(1, kEpiWarps * 32);
+        if (warp == 0) {
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            constexpr uint32_t hdesc = ptx::idesc_tf32<kTileM, kHeadN>();
+            const uint32_t ahi = tmem_base + kAccCol0 + acc * kAccCols, alo = tmem_base + kHeadLoCol;
+            const uint32_t hb = ptx::smem_addr(sHB);
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              const uint64_t bhi = ptx::umma_desc_sw128(hb + kk * 32), blo = ptx::umma_desc_sw128(hb + kHeadN * 128 + kk * 32);
+              ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, bhi, hdesc, kk != 0);
+              ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, blo, hdesc, 1);
+              ptx::mma_tf32_ts(tmem_base + kHeadDCol, alo + kk * 8, bhi, hdesc, 1);
+            }
+            ptx::mma_commit(hdone);
+          }
+          __syncwarp();
+        }
+        ptx::mbar_wait(hdone, e & 1);
+        ptx::tc_fence_after();
+        float lg[8];
+        ptx::tmem_ld_32x32b_x8(tmem_base + kHeadDCol + ((q * 32u) << 16), lg);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
-        // column c holds output feature kcol_feature(c)
-#pragma unroll
-        for (int c = 0; c < 32; ++c) r[c] = fmaxf(r[c] + hw.bias[kcol_feature(c)], 0.0f);
         const uint32_t row = row0 + lane;
         float best = 0.f;
         uint32_t arg = 0;
 #pragma unroll
         for (int cl = 0; cl < kMaxClasses; ++cl) {
           if (cl < static_cast<int>(a.classes)) {
-            float sc = 0.f;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) sc = fmaf(r[kcol_inverse(k)], hw.w[k][cl], sc);
-            sc += hw.b[cl];
+            const float sc = lg[cl] + hw.b[cl];
             if (cl == 0 || sc > best) { best = sc; arg = cl; }
             if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + cl] = sc;
           }
@@ -1893,6 +1940,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   a.tile_end = std::min(tile_end, ntiles);
   a.hout = hout;
   a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
+  a.hbimg = m->hbimg.p;
   a.classes = m->classes;
   a.cls = cls;
   a.logits = logits;
@@ -2201,6 +2249,20 @@ void model_upload(groot_model* m) {
     for (uint32_t c = 0; c < C; ++c) hw.w[k][c] = head[k * C + c];
   for (uint32_t c = 0; c < C; ++c) hw.b[c] = head[H * C + c];
   std::memcpy(m->headw, &hw, sizeof(hw));
+  // head B image for the last layer's tensor-core head: row n = class (zero
+  // rows past C), K element c = hidden feature kcol_feature(c) (the
+  // accumulator's column order), TF32 hi | lo, K-major 128-B swizzle
+  std::vector<uint32_t> himg(kHeadBBytes / 4, 0);
+  for (uint32_t nn = 0; nn < kHeadN; ++nn)
+    for (uint32_t k = 0; k < 32; ++k) {
+      const float v = nn < C ? head[kcol_feature(k) * C + nn] : 0.0f;
+      const float hi = tf32_rna_host(v), lo = v - hi;
+      const uint32_t o = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
+      std::memcpy(reinterpret_cast<uint8_t*>(himg.data()) + o, &hi, 4);
+      std::memcpy(reinterpret_cast<uint8_t*>(himg.data()) + kHeadN * 128 + o, &lo, 4);
+    }
+  m->hbimg.alloc(himg.size());
+  m->hbimg.upload(himg.data(), himg.size());
   m->bimg.alloc(img.size());
   m->bimg.upload(img.data(), img.size());
   m->bias.alloc(bias.size());
