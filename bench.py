@@ -9,11 +9,17 @@ One JSON line on rank 0.
 A *step* is one pass of the hot path over the resident batch: layer forward of
 the 4-layer GraphSAGE + classify (argmax + confusion) over every node of
 batch(encode(gen_csa_multiplier(1024)), 16) — 134,103,056 nodes, 268,107,776
-edges per GPU (weak scaling: every rank owns 16 copies; global batch 16*N).
-``value`` = edges (undirected fwd_edges, all ranks) / max-over-ranks device
-time. ``e2e`` = the same metric through the public C ABI call
-groot_classify_aig with the AIG in pinned host memory: H2D of the AIG literals
-+ labels, device encode -> batch -> forward -> classify, D2H of the classes.
+edges (BASELINE config 5). With N GPUs the 16 copies are split across the
+ranks (strong scaling, --scaling strong, the default): every rank owns whole
+copies, so there is no data-path exchange; the integer confusion matrix is
+all-reduced. ``value`` = edges (undirected fwd_edges, all ranks) /
+max-over-ranks device time. ``e2e`` = the same metric through the public C ABI
+call groot_classify_aig with the AIG in pinned host memory: H2D of the AIG
+literals + labels, device encode -> batch -> forward -> classify, D2H of the
+classes. Side measurements (same line): per-kernel rooflines, the
+materialized-layer-0 forward, the forward with make_context rebuilt every step,
+the standalone SpMM, the partitioned chain topo -> regrow -> predict, and the
+GPU on the exact sample the reference arm times (like-for-like).
 """
 from __future__ import annotations
 
@@ -45,9 +51,13 @@ def parse():
     p.add_argument("--width", type=int, default=1024)
     p.add_argument("--circuit", choices=["csa", "booth"], default="csa",
                    help="multiplier family (booth = BASELINE config 3's radix-4 Booth AIG)")
-    p.add_argument("--batch", type=int, default=16, help="copies per GPU")
+    p.add_argument("--batch", type=int, default=16, help="copies (in total with --scaling strong, per GPU with weak)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="strong: --batch copies in total, split over the ranks; weak: --batch copies per rank")
+    p.add_argument("--parts-k", type=int, default=64, help="topo partitions of the partitioned-chain measurement")
+    p.add_argument("--no-side", action="store_true", help="skip the side measurements (development)")
     return p.parse_args()
 
 
@@ -198,6 +208,41 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def copies_of(rank, world, batch, scaling):
+    """Batch copies owned by `rank`: strong scaling splits `batch` copies into
+    contiguous runs (whole copies: no edge crosses ranks); weak gives each rank `batch`."""
+    if scaling == "weak":
+        return batch
+    return batch * (rank + 1) // world - batch * rank // world
+
+
+def kernel_bytes(n, nnz, num_hd, hd_nnz):
+    """SURVEY 8(d) algorithmic bytes per launch of each forward kernel (u32 CSR
+    indices, fp32 rows, u8 features/ids/classes; 1/deg derived, no value array)."""
+    ld_nnz = nnz - hd_nnz
+    csr, ld = 4 * (n + 1) + 4 * nnz, 4 * (n + 1) + 4 * ld_nnz
+    return {
+        "l0_keys": csr + 4 * n + n,                               # records: CSR walk + features; u8 id per row
+        "sage_layer0": csr + 4 * n + 128 * n,                     # materialized layer 0: features in, rows out
+        "sage_layer1_xform": ld + n + 128 * n + 128 * num_hd,     # keyed transform-first layer 1: ids in, rows out
+        "sage_layer_tc": ld + 128 * n + 128 * n + 128 * num_hd,   # fused 32->32 layer
+        "sage_layer_tc_keyed": ld + n + 128 * n + 128 * num_hd,   # keyed layer 1 on the tensor cores
+        "sage_layer_tc_last": ld + 128 * n + n + 128 * num_hd,    # last layer + head + argmax: rows in, u8 out
+        "hd_mean32": 4 * hd_nnz + 128 * hd_nnz + 128 * num_hd,    # HD rows: col + gathered rows, means out
+        "confusion": 2 * n,
+    }
+
+
+def load_traffic(key):
+    """Measured DRAM bytes per launch (ncu --set full, dram__bytes_read+write) for
+    this exact configuration, if a capture of it is committed; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -214,20 +259,53 @@ def run_ours(args):
     api.set_stream(stream.cuda_stream)
     L = lib()
 
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
     # ---- setup (untimed): AIG on host, encode + batch on device ----
+    copies = copies_of(rank, world, args.batch, args.scaling)
     circ = (api.gen_booth_multiplier if args.circuit == "booth" else api.gen_csa_multiplier)(args.width)
     g1 = api.encode(circ.aig, circ.labels)
-    g = api.batch(g1, args.batch) if args.batch > 1 else g1
+    g = api.batch(g1, copies) if copies > 1 else g1
     n, nnz, E = g.n, g.nnz, g.num_undirected_edges()
+    E_all = sum_over_ranks(E)
     model = api.load_model(MODEL_FILE)
     cls = torch.empty(n, dtype=torch.uint8, device="cuda")
     conf = torch.zeros(25, dtype=torch.int64, device="cuda")
 
-    def step():
-        check(L.groot_predict_full_dev(model.handle, g.handle, C.c_void_p(cls.data_ptr()), None,
+    def step(graph=None):
+        check(L.groot_predict_full_dev(model.handle, (graph or g).handle, C.c_void_p(cls.data_ptr()), None,
                                        C.c_void_p(conf.data_ptr())))
         if world > 1:  # global confusion / accuracy: the only exchange of the path
             dist.all_reduce(conf)
+
+    def timed(fn, steps, pre=None):
+        """max-over-ranks device ms per call of fn, CUDA events on the library stream."""
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        total = 0.0
+        for _ in range(steps):
+            if pre:
+                pre()
+            ev0.record(stream)
+            fn()
+            ev1.record(stream)
+            ev1.synchronize()
+            total += ev0.elapsed_time(ev1)
+        return max_over_ranks(total / steps)
 
     for _ in range(max(args.warmup, 3)):
         conf.zero_()
@@ -252,110 +330,132 @@ def run_ours(args):
         dist.barrier()
     launches = L.groot_kernel_launches() - launches0
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
 
     # per-kernel event totals over the timed region (recorded on the launching stream)
-    maxk = 32
-    names = C.create_string_buffer(48 * maxk)
-    tot = (C.c_double * maxk)()
-    cnt = (C.c_uint64 * maxk)()
-    nk = C.c_uint32()
-    check(L.groot_profile_read(maxk, names, tot, cnt, C.byref(nk)))
-    L.groot_profile_enable(0)
-    kernels = {}
-    for i in range(min(nk.value, maxk)):
-        nm = names.raw[48 * i:48 * (i + 1)].split(b"\0")[0].decode()
-        kernels[nm] = {"ms_per_launch": tot[i] / max(cnt[i], 1), "launches": int(cnt[i]),
+    def read_profile():
+        maxk = 32
+        names = C.create_string_buffer(48 * maxk)
+        tot = (C.c_double * maxk)()
+        cnt = (C.c_uint64 * maxk)()
+        nk = C.c_uint32()
+        check(L.groot_profile_read(maxk, names, tot, cnt, C.byref(nk)))
+        out = {}
+        for i in range(min(nk.value, maxk)):
+            nm = names.raw[48 * i:48 * (i + 1)].split(b"\0")[0].decode()
+            out[nm] = {"ms_per_launch": tot[i] / max(cnt[i], 1), "launches": int(cnt[i]),
                        "ms_per_step": tot[i] / args.steps}
-
-    # the same forward with layer 0 materialized (GROOT_L0_KEYED=0: n x 128 B layer-0 rows
-    # written and read back), reported beside the keyed default for transparency
-    os.environ["GROOT_L0_KEYED"] = "0"
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    del os.environ["GROOT_L0_KEYED"]
-    ms_mat = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_mat], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_mat = float(t.item())
+        return out
+    kernels = read_profile()
+    L.groot_profile_enable(0)
 
     # row classifier output (HD band) for the algorithmic-byte accounting
-    deg = None
-    num_hd = 0
-    hd_nnz = 0
-    try:
-        rp = g.row_ptr
-        deg = np.diff(rp)
-        thr = int(os.environ.get("GROOT_HD_THRESHOLD", "128"))
-        num_hd = int((deg >= thr).sum())
-        hd_nnz = int(deg[deg >= thr].sum())
-        del rp
-    except Exception:
-        pass
-
+    rp = g.row_ptr
+    deg = np.diff(rp)
+    thr = int(os.environ.get("GROOT_HD_THRESHOLD", "128"))
+    num_hd = int((deg >= thr).sum())
+    hd_nnz = int(deg[deg >= thr].sum())
+    del rp, deg
     peak, peak_src = measured_peaks()
-    # dominant kernel: the fused 32->32 layer (gather + tcgen05 transform + epilogue)
-    ld_nnz = nnz - hd_nnz
-    bytes_tc = 4 * (n + 1) + 4 * ld_nnz + 128 * n + 128 * n + 128 * num_hd
-    k_tc = kernels.get("sage_layer_tc")
+    kb = kernel_bytes(n, nnz, num_hd, hd_nnz)
+    cfg_key = f"{args.circuit}{args.width}_b{copies}"
+
+    def rooflines(kern):
+        out = {}
+        for name, k in kern.items():
+            if name in kb:
+                ach = kb[name] / (k["ms_per_launch"] * 1e-3) / 1e9
+                out[name] = {"ms_per_launch": k["ms_per_launch"], "algorithmic_bytes_per_launch": kb[name],
+                             "achieved": ach, "frac": ach / peak,
+                             "traffic": load_traffic(f"{cfg_key}:{name}")}
+        return out
+    kernel_roofs = rooflines(kernels)
+    # the dominant kernel = the single launch the step spends most time in
+    dom = max(kernel_roofs, key=lambda k: kernel_roofs[k]["ms_per_launch"]) if kernel_roofs else None
     roof = None
-    if k_tc:
-        achieved = bytes_tc / (k_tc["ms_per_launch"] * 1e-3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-                summ = json.load(f)
-                traffic = summ.get("kernels", {}).get("sage_layer_tc", {}).get("dram_bytes_per_launch")
-        except Exception:
-            pass
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sage_tile_kernel<kModeLayer> (tile-planned fused 32->32 SAGE layer)",
-                "algorithmic_bytes_per_launch": bytes_tc, "peak_source": peak_src}
-    # whole forward: CSR / plan structure, layer inputs and outputs, u8 classes.
-    # Keyed layer 0 (records -> u8 entry ids) replaces the n x 128 B layer-0 rows written by
-    # layer 0 and read back by layer 1 with one byte per row each way.
+    if dom:
+        r = kernel_roofs[dom]
+        roof = {"bound": "hbm", "achieved": r["achieved"], "peak": peak, "unit": "GB/s", "frac": r["frac"],
+                "traffic": r["traffic"], "kernel": dom, "algorithmic_bytes_per_launch": r["algorithmic_bytes_per_launch"],
+                "peak_source": peak_src,
+                "note": "dominant launch of the step (largest ms per launch); every forward kernel in kernel_rooflines"}
+    # whole forward vs SURVEY 8(d)'s 114.39 GB-equivalent bytes and vs the bytes this path moves
     keyed = "l0_keys" in kernels
     depth = 4
-    csr, ld = 4 * (n + 1) + 4 * nnz, 4 * (n + 1) + 4 * ld_nnz
-    l0 = csr + 4 * n + (n if keyed else 128 * n)
-    l1 = ld + (n if keyed else 128 * n) + 128 * n + 128 * num_hd
+    ld = 4 * (n + 1) + 4 * (nnz - hd_nnz)
+    l0_survey = 4 * (n + 1) + 4 * nnz + 4 * n + 128 * n
+    l1_survey = ld + 128 * n + 128 * n + 128 * num_hd
     mid = ld + 128 * n + 128 * n + 128 * num_hd
     last = ld + 128 * n + n + 128 * num_hd
-    full_bytes = l0 + l1 + mid * (depth - 3) + last + 2 * n
-    k_x = kernels.get("sage_layer1_xform")
-    l1_roof = None
-    if k_x:  # keyed transform-first layer 1 (a gather-sum: no input rows, table in shared memory)
-        ach = l1 / (k_x["ms_per_launch"] * 1e-3) / 1e9
-        l1_roof = {"kernel": "sage_tile_kernel<kModeXform, true> (keyed transform-first layer 1)", "bound": "hbm",
-                   "algorithmic_bytes_per_launch": l1, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
+    survey_bytes = l0_survey + l1_survey + mid * (depth - 3) + last + 2 * n
+    moved = (kb["l0_keys"] + kb["sage_layer1_xform"] if keyed else kb["sage_layer0"] + kb["sage_layer_tc"]) \
+        + mid * (depth - 3) + last + 2 * n
+    forward_roof = {"survey_bytes": survey_bytes, "survey_frac": survey_bytes / ms / 1e6 / peak,
+                    "moved_bytes": moved, "moved_frac": moved / ms / 1e6 / peak, "keyed_layer0": keyed,
+                    "note": "survey_bytes = SURVEY 8(d) forward (layer-0 rows materialized); moved_bytes = what this "
+                            "path reads/writes (keyed layer 0: u8 entry ids instead of 128-B layer-0 rows)"}
+
+    side = {}
+    if not args.no_side:
+        # the same forward with layer 0 materialized (GROOT_L0_KEYED=0): the general path
+        os.environ["GROOT_L0_KEYED"] = "0"
+        for _ in range(2):
+            step()
+        L.groot_profile_enable(1)
+        ms_mat = timed(step, args.steps)
+        kmat = read_profile()
+        L.groot_profile_enable(0)
+        del os.environ["GROOT_L0_KEYED"]
+        mat_roofs = rooflines(kmat)
+        mat_dom = max(mat_roofs, key=lambda k: mat_roofs[k]["ms_per_launch"]) if mat_roofs else None
+        side["materialized_layer0"] = {
+            "ms_per_step": ms_mat, "value": E_all / (ms_mat * 1e-3), "unit": UNIT,
+            "forward_frac": survey_bytes / ms_mat / 1e6 / peak, "kernel_rooflines": mat_roofs,
+            "dominant": mat_dom, "note": "same forward with GROOT_L0_KEYED=0 (layer-0 rows materialized: the general "
+                                         "path for graphs without few distinct layer-0 records)"}
+        # make_context rebuilt every step (the reference's predict_full redoes it per call)
+        ms_ctx = timed(step, max(3, min(args.steps, 5)), pre=lambda: L.groot_graph_release_context(g.handle))
+        side["with_context_rebuild"] = {
+            "ms_per_step": ms_ctx, "value": E_all / (ms_ctx * 1e-3), "unit": UNIT,
+            "note": "groot_graph_release_context before every step: row classifier, tile plan, HD plan and "
+                    "activations rebuilt inside the timed region (keyed-path probe included)"}
+        for _ in range(2):
+            step()
 
     # standalone SpMM (mean aggregation, f=32): the metric's "SpMM HBM GB/s"
     dense = torch.randn(n, 32, device="cuda")
     outm = torch.empty_like(dense)
+    spmm_call = lambda: check(L.groot_spmm_mean_dev(g.handle, C.c_void_p(dense.data_ptr()), 32,  # noqa: E731
+                                                     C.c_void_p(outm.data_ptr())))
     for _ in range(2):
-        check(L.groot_spmm_mean_dev(g.handle, C.c_void_p(dense.data_ptr()), 32, C.c_void_p(outm.data_ptr())))
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        check(L.groot_spmm_mean_dev(g.handle, C.c_void_p(dense.data_ptr()), 32, C.c_void_p(outm.data_ptr())))
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    spmm_ms = ev0.elapsed_time(ev1) / args.steps
+        spmm_call()
+    spmm_ms = timed(spmm_call, args.steps)
     spmm_bytes = 4 * (n + 1) + 4 * nnz + 2 * 128 * n
     spmm = {"ms": spmm_ms, "algorithmic_bytes": spmm_bytes, "achieved_gbs": spmm_bytes / spmm_ms / 1e6,
-            "frac": spmm_bytes / spmm_ms / 1e6 / peak}
+            "frac": spmm_bytes / spmm_ms / 1e6 / peak, "traffic": load_traffic(f"{cfg_key}:spmm_mean32")}
     del dense, outm
+
+    # partitioned chain on the device (src/experiment.cpp:128-153): topo k -> regrow -> predict
+    if not args.no_side and world == 1:
+        L.groot_graph_release_context(g.handle)
+        k = args.parts_k
+        api.predict(model, g, api.regrow(g, api.partition_topo_chunks(g, k)))  # warm the allocator
+        t0 = time.perf_counter()
+        pa = api.partition_topo_chunks(g, k)
+        t1 = time.perf_counter()
+        parts = api.regrow(g, pa)
+        t2 = time.perf_counter()
+        pred = api.predict(model, g, parts)
+        t3 = time.perf_counter()
+        side["partitioned"] = {
+            "k": k, "topo_ms": 1e3 * (t1 - t0), "regrow_ms": 1e3 * (t2 - t1),
+            "predict_ms": 1e3 * (t3 - t2), "chain_ms": 1e3 * (t3 - t0),
+            "value": E_all / (t3 - t0), "unit": UNIT, "crossing_fraction": api.crossing_fraction(g, pa),
+            "augmented_nodes": int(sum(parts.sizes(p)[0] + parts.sizes(p)[1] for p in range(k))),
+            "accuracy": pred.accuracy,
+            "note": "host-synchronous C-ABI calls, wall clock: predict = materialize all parts as one block-diagonal "
+                    "graph, forward, scatter core classes, device confusion, classes to host"}
+        del parts, pa, pred
 
     # ---- e2e through the public C ABI with pinned host buffers ----
     del g
@@ -367,10 +467,10 @@ def run_ours(args):
     conf_h = (C.c_uint64 * 25)()
     acc = C.c_double()
 
-    def e2e_call():
+    def e2e_call(cp=copies):
         check(L.groot_classify_aig(model.handle, circ.aig.num_inputs, circ.aig.num_ands,
                                    C.c_void_p(ands_h.data_ptr()), int(outs_h.numel()),
-                                   C.c_void_p(outs_h.data_ptr()), C.c_void_p(lab_h.data_ptr()), args.batch,
+                                   C.c_void_p(outs_h.data_ptr()), C.c_void_p(lab_h.data_ptr()), cp,
                                    C.c_void_p(pred_h.data_ptr()), conf_h, C.byref(acc)))
 
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
@@ -383,17 +483,25 @@ def run_ours(args):
     for _ in range(e2e_steps):
         e2e_call()
     torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     h2d = ands_h.numel() * 4 + outs_h.numel() * 4 + lab_h.numel()
     d2h = pred_h.numel() + 25 * 8
     accuracy = acc.value
 
-    # ---- CPU baseline (rank 0, N=1 only) ----
+    # weak-scaling secondary line (N > 1): --batch copies on every rank
+    if world > 1 and args.scaling == "strong" and not args.no_side:
+        gw = api.batch(g1, args.batch)
+        for _ in range(2):
+            step(gw)
+        ms_w = timed(lambda: step(gw), max(3, min(args.steps, 10)))
+        side["weak_scaling"] = {"batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                                "ms_per_step": ms_w, "value": gw.num_undirected_edges() * world / (ms_w * 1e-3),
+                                "unit": UNIT}
+        del gw
+
+    # ---- CPU baseline and the like-for-like pair (rank 0, N=1 only) ----
     cpu = None
+    like = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             s = RefSample(args.width, args.circuit)
@@ -402,39 +510,60 @@ def run_ours(args):
             tt = sum(s.step() for _ in range(reps))
             cpu = {"value": s.edges * reps / tt, "unit": UNIT, "cores": s.workers, "kind": s.kind,
                    "sample": s.desc}
+            # the GPU on exactly the sample the reference times: the same k regrown
+            # parts of one copy, predict over parts [first, first+count)
+            gs = api.encode(circ.aig, circ.labels)
+            ps = api.regrow(gs, api.partition_topo_chunks(gs, s.k))
+            ids = np.arange(s.first, s.first + s.count, dtype=np.uint32)
+            api.predict_parts(model, gs, ps, ids)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                api.predict_parts(model, gs, ps, ids)
+            gpu_s = (time.perf_counter() - t0) / reps
+            like = {"same_config": True, "sample": s.desc, "edges": s.edges,
+                    "gpu_value": s.edges / gpu_s, "gpu_ms": 1e3 * gpu_s,
+                    "reference_value": cpu["value"], "reference_ms": 1e3 * tt / reps,
+                    "ratio": (s.edges / gpu_s) / cpu["value"], "unit": UNIT,
+                    "note": "groot_predict_parts (host labels in/out, synchronous) vs the reference's predict over "
+                            "the same parts on all host threads"}
+            del gs, ps
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        value = E * world / (ms * 1e-3)
+        value = E_all / (ms * 1e-3)
+        strong = args.scaling == "strong"
+        global_batch = args.batch if strong else args.batch * world
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if strong and world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate)",
             "data": f"synthetic (deterministic {args.circuit.upper()} multiplier generator; trained 8-bit ASG1 weights)",
-            "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {args.batch} per GPU "
+            "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {global_batch} "
                                    f"(4-layer GraphSAGE 4-32-32-32-32 + 32->5 head, predict_full)",
-                       "width": args.width, "batch_per_gpu": args.batch, "global_batch": args.batch * world,
-                       "nodes_per_gpu": n, "edges_per_gpu": E, "nnz_per_gpu": nnz,
-                       "parallelism": f"dp{world} (whole batch copies per GPU)" if world > 1 else "single GPU",
-                       "l2": "inputs (>40 GB resident) far exceed L2; no flush"},
+                       "width": args.width, "global_batch": global_batch, "batch_per_gpu": copies,
+                       "nodes_per_gpu": n, "edges_per_gpu": E, "edges_total": int(E_all), "nnz_per_gpu": nnz,
+                       "parallelism": (f"{world} GPUs, whole batch copies per rank ({args.scaling} scaling), "
+                                       f"confusion all-reduce only") if world > 1 else "single GPU",
+                       "l2": "inputs (>40 GB resident at b16) far exceed L2; no flush"},
             "roofline": roof,
-            "layer1_roofline": l1_roof,
-            "materialized_layer0": {"ms_per_step": ms_mat, "value": E * world / (ms_mat * 1e-3), "unit": UNIT,
-                                    "note": "same forward with GROOT_L0_KEYED=0 (layer-0 rows materialized)"},
-            "forward_roofline": ({"algorithmic_bytes": full_bytes, "achieved_gbs": full_bytes / ms / 1e6,
-                                  "frac": full_bytes / ms / 1e6 / peak, "keyed_layer0": keyed} if full_bytes else None),
+            "kernel_rooflines": kernel_roofs,
+            "forward_roofline": forward_roof,
             "spmm": spmm,
             "kernels": kernels,
             "cpu_baseline": cpu,
-            "e2e": {"value": E * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "like_for_like": like,
+            "e2e": {"value": E_all / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                     "path": "groot_classify_aig (pinned host AIG -> encode -> batch -> predict_full -> host classes)"},
             "accuracy": accuracy,
+            "accuracy_note": "trained 8-bit CSA ASG1 (reference recipe run through the oracle restatement of train)",
             "clocks": clocks,
             "gpu_launches": int(launches),
         }
+        line.update(side)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -48,6 +48,7 @@ def test_our_arm_line():
     for k in BASE_KEYS + ("e2e", "roofline", "clocks", "gpu_launches", "spmm", "kernels"):
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["scaling"] == "weak"
+    assert d["roofline"]["kernel"] in d["kernel_rooflines"] and d["like_for_like"] is None
     assert "workload" in d["config"]
     edges = d["config"]["edges_per_gpu"]
     assert abs(d["value"] - edges / (d["ms_per_step"] * 1e-3)) <= 1e-6 * d["value"]
