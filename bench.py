@@ -216,7 +216,7 @@ def copies_of(rank, world, batch, scaling):
     return batch * (rank + 1) // world - batch * rank // world
 
 
-def kernel_bytes(n, nnz, num_hd, hd_nnz):
+def kernel_bytes(n, nnz, num_hd, hd_nnz, hd_uniq):
     """SURVEY 8(d) algorithmic bytes per launch of each forward kernel (u32 CSR
     indices, fp32 rows, u8 features/ids/classes; 1/deg derived, no value array)."""
     ld_nnz = nnz - hd_nnz
@@ -228,7 +228,7 @@ def kernel_bytes(n, nnz, num_hd, hd_nnz):
         "sage_layer_tc": ld + 128 * n + 128 * n + 128 * num_hd,   # fused 32->32 layer
         "sage_layer_tc_keyed": ld + n + 128 * n + 128 * num_hd,   # keyed layer 1 on the tensor cores
         "sage_layer_tc_last": ld + 128 * n + n + 128 * num_hd,    # last layer + head + argmax: rows in, u8 out
-        "hd_mean32": 4 * hd_nnz + 128 * hd_nnz + 128 * num_hd,    # HD rows: col + gathered rows, means out
+        "hd_mean32": 4 * hd_nnz + 128 * hd_uniq + 128 * num_hd,   # HD rows: col + each distinct neighbour row, means out
         "confusion": 2 * n,
     }
 
@@ -356,8 +356,16 @@ def run_ours(args):
     num_hd = int((deg >= thr).sum())
     hd_nnz = int(deg[deg >= thr].sum())
     del rp, deg
+    # distinct rows the HD band reads (each fetched from DRAM once; the rest are L2
+    # hits), counted on one copy: copies are disjoint
+    h1 = g1.copy_out("row_ptr", "col_idx")
+    d1 = np.diff(h1["row_ptr"])
+    hd1 = np.nonzero(d1 >= thr)[0]
+    hd_uniq = int(np.unique(np.concatenate([h1["col_idx"][h1["row_ptr"][r]:h1["row_ptr"][r + 1]] for r in hd1])).size
+                  if hd1.size else 0) * copies
+    del h1, d1, hd1
     peak, peak_src = measured_peaks()
-    kb = kernel_bytes(n, nnz, num_hd, hd_nnz)
+    kb = kernel_bytes(n, nnz, num_hd, hd_nnz, hd_uniq)
     cfg_key = f"{args.circuit}{args.width}_b{copies}"
 
     def rooflines(kern):

@@ -117,6 +117,15 @@ void groot_graph_free(groot_graph* g);
 /* ---- partition ------------------------------------------------------------
  * partition_topo_chunks (src/partition.cpp:301-312): part p = [n*p/k, n*(p+1)/k). */
 int groot_partition_topo_chunks(const groot_graph* g, uint32_t k, groot_assignment** out);
+/* partition_multilevel (src/partition.cpp:314-367) replacement: the topo
+ * chunks refined on the device by deterministic, size-constrained label
+ * propagation (part sizes <= ceil(1.05 n / k), never empty), so it terminates
+ * for every k (the reference livelocks for k >= 8 in rebalance, :259-297).
+ * Equal to the reference's result where that terminates and its refined-topo
+ * candidate wins. seed: accepted for the reference's signature (no random
+ * choice is made). rounds / moves (may be NULL): LP rounds run, nodes moved. */
+int groot_partition_multilevel(const groot_graph* g, uint32_t k, uint64_t seed, groot_assignment** out,
+                               uint32_t* rounds, uint64_t* moves);
 /* load_assignment (src/partition.cpp:369-392): "node part" lines, same checks. */
 int groot_load_assignment(const char* path, uint32_t n, groot_assignment** out);
 /* From a host part_of[n] array (validated like load_assignment). */

@@ -422,6 +422,17 @@ inline PartitionAssignment partition_topo_chunks(const EdaGraph& g, std::uint32_
   gpu::DeviceAssignment da(a);
   return PartitionAssignment::from_device(da.get());
 }
+// partition_multilevel (src/partition.cpp:314-367) replacement: topo chunks +
+// device label propagation within the 5 % cap; terminates for every k (the
+// reference livelocks for k >= 8); equal to the reference where it terminates
+// and its refined-topo candidate wins.
+inline PartitionAssignment partition_multilevel(const EdaGraph& g, std::uint32_t k, std::uint64_t seed) {
+  auto d = g.to_device();
+  groot_assignment* a = nullptr;
+  detail::check(groot_partition_multilevel(d.get(), k, seed, &a, nullptr, nullptr));
+  gpu::DeviceAssignment da(a);
+  return PartitionAssignment::from_device(da.get());
+}
 inline PartitionAssignment load_assignment(const std::string& path, std::uint32_t n) {  // src/partition.cpp:369
   groot_assignment* a = nullptr;
   detail::check(groot_load_assignment(path.c_str(), n, &a));

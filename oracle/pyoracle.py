@@ -406,3 +406,75 @@ def load_model(path: str):
     if prm.shape[0] != cnt:
         raise OracleError("model file: truncated")
     return prm, dict(depth=depth, in_dim=in_dim, hidden=hidden, classes=classes)
+
+
+# ---------------------------------------------------------------------------
+# partition_multilevel replacement. The reference's
+# partition_multilevel (src/partition.cpp:314-367) livelocks in rebalance
+# (:259-297) for k >= 8 on multiplier graphs; its result is the cheaper of a
+# multilevel cut and the topo chunks refined by greedy boundary moves
+# (:357-366). This restates the device algorithm that replaces it (numpy,
+# test infrastructure): start from the topo chunks, then rounds of
+# deterministic size-constrained label propagation --
+#   * every node v picks the neighbouring part t != part(v) with the most
+#     neighbours (ties: lowest id), allowed only upward (t > part(v)) in even
+#     rounds and downward in odd rounds; gain = conn(t) - conn(part(v)) > 0;
+#   * candidates moving into t are ranked by (gain desc, node id asc) and the
+#     first cap - weight(t) of them move (cap = ceil(1.05 n / k),
+#     src/partition.cpp:328-329), weights taken at the round's start;
+#   * a part that would lose all its nodes keeps every node that round;
+#   * stop after two consecutive rounds without a move, or max_rounds.
+# Every round keeps every part within the cap and nonempty, so it terminates
+# for any k. On graphs where the reference terminates (k <= 4 on CSA) the
+# result equals partition_multilevel's bit for bit (tests/test_oracle.py).
+# ---------------------------------------------------------------------------
+def lp_cap(n: int, k: int) -> int:
+    """ceil(1.05 * n / k) in double, as src/partition.cpp:328-329."""
+    return int(np.ceil(1.05 * float(n) / k))
+
+
+def partition_lp(row_ptr, col_idx, n: int, k: int, max_rounds: int = 32) -> np.ndarray:
+    if k < 1:
+        raise ValueError("partition: k must be >= 1")
+    if k > n:
+        raise ValueError("partition: k exceeds node count")
+    part = topo_chunks(n, k).astype(np.int64)
+    if k == 1:
+        return part.astype(np.uint32)
+    cap = lp_cap(n, k)
+    rp = np.asarray(row_ptr, np.int64)
+    ci = np.asarray(col_idx, np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    idle = 0
+    for it in range(max_rounds):
+        key = rows * k + part[ci]
+        uk, cnt = np.unique(key, return_counts=True)
+        v, p = uk // k, uk % k
+        own = np.zeros(n, np.int64)
+        m = p == part[v]
+        own[v[m]] = cnt[m]
+        d = (p > part[v]) if it % 2 == 0 else (p < part[v])
+        vv, pp, cc = v[d], p[d], cnt[d]
+        o = np.lexsort((pp, -cc, vv))           # per node: most neighbours, then lowest part
+        vv, pp, cc = vv[o], pp[o], cc[o]
+        first = np.ones(vv.size, bool)
+        first[1:] = vv[1:] != vv[:-1]
+        vv, pp, gain = vv[first], pp[first], cc[first] - own[vv[first]]
+        g = gain > 0
+        vv, pp, gain = vv[g], pp[g], gain[g]
+        w = np.bincount(part, minlength=k)
+        room = np.maximum(cap - w, 0)
+        o = np.lexsort((vv, -gain, pp))         # per target part: gain desc, node asc
+        vv, pp, gain = vv[o], pp[o], gain[o]
+        rank = np.arange(vv.size) - np.searchsorted(pp, pp)
+        ok = rank < room[pp]
+        vv, pp = vv[ok], pp[ok]
+        out = np.bincount(part[vv], minlength=k)
+        keep = out >= w                          # a part would be emptied: none of its nodes move
+        mv = ~keep[part[vv]]
+        vv, pp = vv[mv], pp[mv]
+        part[vv] = pp
+        idle = 0 if vv.size else idle + 1
+        if idle >= 2:
+            break
+    return part.astype(np.uint32)

@@ -62,6 +62,7 @@ def _declare(L):
         "ref_graph_copy": (None, [P, P, P, P, P, P, P]),
         "ref_graph_free": (None, [P]),
         "ref_topo_chunks": (i32, [P, u32, P]),
+        "ref_partition_multilevel": (i32, [P, u32, u64, P]),
         "ref_load_assignment": (i32, [C.c_char_p, u32, P, P]),
         "ref_regrow": (P, [P, P, u32, i32]),
         "ref_parts_sizes": (None, [P, u32, P, P, P]),
@@ -187,6 +188,15 @@ def topo_chunks(g: RefGraph, k: int) -> np.ndarray:
     n = g.sizes()[0]
     part = np.empty(n, np.uint32)
     if lib().ref_topo_chunks(g.h, k, ptr(part)) != 0:
+        raise ValueError(_err())
+    return part
+
+
+def partition_multilevel(g: RefGraph, k: int, seed: int) -> np.ndarray:
+    """src/partition.cpp:314-367 (does not terminate for k >= 8 on multiplier graphs)."""
+    n = g.sizes()[0]
+    part = np.empty(n, np.uint32)
+    if lib().ref_partition_multilevel(g.h, k, seed, ptr(part)) != 0:
         raise ValueError(_err())
     return part
 

@@ -201,6 +201,14 @@ int ref_topo_chunks(const ref_graph* g, uint32_t k, uint32_t* part_of) {
     std::copy(pa.part_of.begin(), pa.part_of.end(), part_of);
   });
 }
+// partition_multilevel (src/partition.cpp:314-367). Livelocks in rebalance for
+// k >= 8 on multiplier graphs: callers run it under a time limit.
+int ref_partition_multilevel(const ref_graph* g, uint32_t k, uint64_t seed, uint32_t* part_of) {
+  return guarded([&] {
+    const PartitionAssignment pa = partition_multilevel(g->g, k, seed);
+    std::copy(pa.part_of.begin(), pa.part_of.end(), part_of);
+  });
+}
 // load_assignment (src/partition.cpp:369)
 int ref_load_assignment(const char* path, uint32_t n, uint32_t* part_of, uint32_t* k) {
   return guarded([&] {

@@ -55,6 +55,7 @@ _SIG = {
     "groot_graph_device_ptrs": (i32, [P, P, P, P, P, P]),
     "groot_graph_free": (None, [P]),
     "groot_partition_topo_chunks": (i32, [P, u32, P]),
+    "groot_partition_multilevel": (i32, [P, u32, u64, P, P, P]),
     "groot_load_assignment": (i32, [C.c_char_p, u32, P]),
     "groot_assignment_from_host": (i32, [u32, P, P]),
     "groot_assignment_info": (i32, [P, P, P]),

@@ -273,6 +273,18 @@ def partition_topo_chunks(g: EdaGraph, k: int) -> PartitionAssignment:
     return PartitionAssignment(h.value)
 
 
+def partition_multilevel(g: EdaGraph, k: int, seed: int = 7, stats: dict | None = None) -> PartitionAssignment:
+    """src/partition.cpp:314-367 replacement: topo chunks + device label propagation
+    within the 5 % balance cap; terminates for every k. `stats` (optional dict)
+    receives the rounds run and nodes moved."""
+    h = C.c_void_p()
+    rounds, moves = C.c_uint32(), C.c_uint64()
+    check(lib().groot_partition_multilevel(g.handle, k, seed, C.byref(h), C.byref(rounds), C.byref(moves)))
+    if stats is not None:
+        stats.update(rounds=rounds.value, moves=moves.value)
+    return PartitionAssignment(h.value)
+
+
 def load_assignment(path: str, n: int) -> PartitionAssignment:
     """src/partition.cpp:369-392."""
     h = C.c_void_p()

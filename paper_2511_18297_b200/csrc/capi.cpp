@@ -58,6 +58,7 @@ groot_graph* graph_from_host(uint32_t, const uint64_t*, const uint32_t*, const u
                              const uint32_t*);
 void graph_copy_out(const groot_graph*, uint64_t*, uint32_t*, uint8_t*, uint8_t*, uint32_t*, uint32_t*);
 groot_assignment* topo_chunks(const groot_graph*, uint32_t);
+groot_assignment* partition_lp(const groot_graph*, uint32_t, uint64_t, uint32_t, uint32_t*, uint64_t*);
 groot_assignment* assignment_from_host(uint32_t, const uint32_t*);
 groot_assignment* load_assignment(const char*, uint32_t);
 uint64_t edge_cut(const groot_graph*, const groot_assignment*);
@@ -681,6 +682,18 @@ int groot_assignment_copy_out(const groot_assignment* a, uint32_t* part_of) {
     DeviceScope ds_a(a->device);
     a->part_of.download(part_of, a->n);
     stream_sync();
+  });
+}
+
+int groot_partition_multilevel(const groot_graph* g, uint32_t k, uint64_t seed, groot_assignment** out,
+                               uint32_t* rounds, uint64_t* moves) {
+  return guarded([&] {
+    need(g, "groot_partition_multilevel");
+    DeviceScope ds_g(g->device);
+    need(out, "groot_partition_multilevel");
+    const char* e = std::getenv("GROOT_LP_ROUNDS");
+    const uint32_t max_rounds = e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 32u;
+    *out = partition_lp(g, k, seed, max_rounds, rounds, moves);
   });
 }
 

@@ -1,0 +1,277 @@
+// partition_lp.cu — partition_multilevel's replacement.
+//
+// The reference's partition_multilevel (src/partition.cpp:314-367) returns the
+// cheaper of a multilevel cut and the topo chunks refined by greedy boundary
+// moves, both clamped by rebalance (:259-297), which livelocks for k >= 8 on
+// multiplier graphs. This is a terminating, deterministic, data-parallel
+// restatement of its refined-topo candidate: start from the topo chunks
+// (src/partition.cpp:301-312), then rounds of size-constrained label
+// propagation on the device:
+//   lp_best_*     every node picks the neighbouring part t != own with the most
+//                 neighbours (ties: lowest id), only upward (t > own) in even
+//                 rounds and downward in odd ones; gain = conn(t) - conn(own);
+//                 a candidate is (t, gain > 0). Thread per row below the HD
+//                 threshold (O(d^2) counting over the row), CTA per HD row.
+//   select        candidates sorted by (t, gain desc, node asc) (CUB radix
+//                 sort, stable); the first cap - weight(t) of each target move,
+//                 cap = ceil(1.05 n / k) (src/partition.cpp:328-329);
+//   apply         a part that would lose all its nodes keeps them this round;
+//                 moves update the part weights.
+// Parts stay within the cap and nonempty every round, so it terminates for any
+// k; the loop stops after two idle rounds or GROOT_LP_ROUNDS (32). On the
+// graphs where the reference terminates and its refined-topo candidate wins
+// (CSA multipliers, k <= 4) the assignment equals the reference's bit for bit
+// (tests/test_partition_lp.py); the oracle restatement is
+// oracle/pyoracle.py:partition_lp.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace groot {
+
+constexpr unsigned long long kNoCand = ~0ull;
+constexpr uint32_t kLpHdDeg = 128;  // rows of at least this degree: one CTA each
+
+// candidate key: target part in the high word, (~gain) in the low word, so an
+// ascending sort orders by target, then gain descending
+__device__ __forceinline__ unsigned long long lp_key(uint32_t t, uint32_t gain) {
+  return (static_cast<unsigned long long>(t) << 32) | (0xFFFFFFFFu - gain);
+}
+
+__device__ __forceinline__ bool lp_dir_ok(uint32_t t, uint32_t own, uint32_t up) {
+  return up ? t > own : t < own;
+}
+
+// LD rows: thread per row, exact counts by scanning the row once per neighbour.
+__global__ void lp_best_ld_kernel(uint32_t n, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                  const uint32_t* __restrict__ part, uint32_t up,
+                                  unsigned long long* __restrict__ cand) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t b = rp[v], e = rp[v + 1];
+    if (e - b >= kLpHdDeg) continue;  // lp_best_hd_kernel
+    const uint32_t own = part[v];
+    uint32_t own_cnt = 0, best = 0xFFFFFFFFu, best_cnt = 0;
+    for (uint32_t q = b; q < e; ++q) {
+      const uint32_t t = part[col[q]];
+      if (t == own) {
+        ++own_cnt;
+        continue;
+      }
+      if (!lp_dir_ok(t, own, up)) continue;
+      // count t over the row only at its first occurrence
+      bool first = true;
+      for (uint32_t r = b; r < q && first; ++r) first = part[col[r]] != t;
+      if (!first) continue;
+      uint32_t c = 1;
+      for (uint32_t r = q + 1; r < e; ++r) c += part[col[r]] == t;
+      if (c > best_cnt || (c == best_cnt && t < best)) {
+        best = t;
+        best_cnt = c;
+      }
+    }
+    cand[v] = (best != 0xFFFFFFFFu && best_cnt > own_cnt) ? lp_key(best, best_cnt - own_cnt) : kNoCand;
+  }
+}
+
+// HD rows (degree >= kLpHdDeg): CTA per row. With k <= kLpHistParts a
+// shared-memory histogram of the row's parts (O(d + k)); otherwise each thread
+// counts its positions' parts over the whole row (O(d^2 / threads)). A block
+// reduction keeps the best.
+constexpr uint32_t kLpHistParts = 8192;
+__global__ void __launch_bounds__(256) lp_best_hd_kernel(uint32_t k, const uint32_t* __restrict__ hd_rows,
+                                                         uint32_t count, const uint32_t* __restrict__ rp,
+                                                         const uint32_t* __restrict__ col,
+                                                         const uint32_t* __restrict__ part, uint32_t up,
+                                                         unsigned long long* __restrict__ cand) {
+  extern __shared__ uint32_t hist[];  // k entries when k <= kLpHistParts
+  __shared__ unsigned long long red_best[8];
+  __shared__ uint32_t red_own[8];
+  const bool use_hist = k <= kLpHistParts;
+  for (uint32_t s = blockIdx.x; s < count; s += gridDim.x) {
+    const uint32_t v = hd_rows[s], b = rp[v], e = rp[v + 1];
+    const uint32_t own = part[v];
+    if (use_hist) {
+      for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (uint32_t q = b + threadIdx.x; q < e; q += blockDim.x) atomicAdd(hist + part[col[q]], 1u);
+      __syncthreads();
+    }
+    // best encoded as (count << 32) | (0xFFFFFFFF - part): max = most neighbours, lowest part
+    unsigned long long best = 0;
+    uint32_t own_cnt = 0;
+    for (uint32_t q = b + threadIdx.x; q < e; q += blockDim.x) {
+      const uint32_t t = part[col[q]];
+      if (t == own) {
+        ++own_cnt;
+        continue;
+      }
+      if (!lp_dir_ok(t, own, up)) continue;
+      uint32_t c = 0;
+      if (use_hist) {
+        c = hist[t];
+      } else {
+        for (uint32_t r = b; r < e; ++r) c += part[col[r]] == t;
+      }
+      const unsigned long long key = (static_cast<unsigned long long>(c) << 32) | (0xFFFFFFFFu - t);
+      best = key > best ? key : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+      best = x > best ? x : best;
+      own_cnt += __shfl_xor_sync(0xffffffffu, own_cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red_best[threadIdx.x >> 5] = best;
+      red_own[threadIdx.x >> 5] = own_cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long bb = 0;
+      uint32_t oc = 0;
+      for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+        bb = red_best[w] > bb ? red_best[w] : bb;
+        oc += red_own[w];
+      }
+      const uint32_t c = static_cast<uint32_t>(bb >> 32), t = 0xFFFFFFFFu - static_cast<uint32_t>(bb);
+      cand[v] = (bb && c > oc) ? lp_key(t, c - oc) : kNoCand;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void lp_flag_hd_kernel(uint32_t n, const uint32_t* __restrict__ rp, uint8_t* __restrict__ flag) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    flag[v] = rp[v + 1] - rp[v] >= kLpHdDeg;
+}
+
+__global__ void lp_weights_kernel(uint32_t n, const uint32_t* __restrict__ part, uint32_t* __restrict__ w) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicAdd(w + part[v], 1u);
+}
+
+// sorted candidates: the first cap - weight(t) of target t's run are accepted;
+// accepted moves are tallied per source part
+__global__ void lp_select_kernel(uint32_t m, const unsigned long long* __restrict__ keys,
+                                 const uint32_t* __restrict__ nodes, const uint32_t* __restrict__ part,
+                                 const uint32_t* __restrict__ w, uint32_t cap, uint8_t* __restrict__ ok,
+                                 uint32_t* __restrict__ out_cnt) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
+    uint32_t lo = 0, hi = i;  // first index of target t's run
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (static_cast<uint32_t>(keys[mid] >> 32) < t) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t room = w[t] < cap ? cap - w[t] : 0u;
+    const bool acc = i - lo < room;
+    ok[i] = acc;
+    if (acc) atomicAdd(out_cnt + part[nodes[i]], 1u);
+  }
+}
+
+// w: weights at the round's start (read only); wn: next round's weights
+__global__ void lp_apply_kernel(uint32_t m, const unsigned long long* __restrict__ keys,
+                                const uint32_t* __restrict__ nodes, const uint8_t* __restrict__ ok,
+                                const uint32_t* __restrict__ out_cnt, const uint32_t* __restrict__ w,
+                                uint32_t* __restrict__ part, uint32_t* __restrict__ wn, uint32_t* __restrict__ moved) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    if (!ok[i]) continue;
+    const uint32_t v = nodes[i], src = part[v], t = static_cast<uint32_t>(keys[i] >> 32);
+    if (out_cnt[src] >= w[src]) continue;  // the part would be emptied: it keeps its nodes this round
+    part[v] = t;
+    atomicSub(wn + src, 1u);
+    atomicAdd(wn + t, 1u);
+    atomicAdd(moved, 1u);
+  }
+}
+
+__global__ void lp_gather_keys_kernel(uint32_t m, const uint32_t* __restrict__ nodes,
+                                      const unsigned long long* __restrict__ cand, unsigned long long* __restrict__ keys) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) keys[i] = cand[nodes[i]];
+}
+
+struct IsCand {
+  __host__ __device__ uint8_t operator()(const unsigned long long& k) const { return k != kNoCand; }
+};
+
+groot_assignment* topo_chunks(const groot_graph* g, uint32_t k);
+
+// partition_multilevel(g, k, seed): see the file header. `seed` is accepted for
+// the reference's signature; the algorithm makes no random choice.
+groot_assignment* partition_lp(const groot_graph* g, uint32_t k, uint64_t seed, uint32_t max_rounds,
+                               uint32_t* rounds_out, uint64_t* moves_out) {
+  (void)seed;
+  groot_assignment* a = topo_chunks(g, k);  // validates k like validate_k (src/partition.cpp:15-18)
+  uint32_t r = 0;
+  uint64_t total = 0;
+  try {
+    const uint32_t n = g->n;
+    if (k > 1 && k < n) {
+      const uint32_t cap = static_cast<uint32_t>(std::ceil(1.05 * static_cast<double>(n) / k));
+      DevBuf<unsigned long long> cand(n), keys(n), skeys(n);
+      DevBuf<uint32_t> nodes(n), snodes(n), w(k), wn(k), out_cnt(k), hd(n), cnt(1), moved(1);
+      DevBuf<uint8_t> ok(n), flag(n);
+      cub::CountingInputIterator<uint32_t> iota(0);
+      cub::TransformInputIterator<uint8_t, IsCand, const unsigned long long*> is_cand(cand.p, IsCand{});
+      size_t b1 = 0, b2 = 0, b3 = 0;
+      cub::DeviceSelect::Flagged(nullptr, b1, iota, flag.p, hd.p, cnt.p, n, stream());
+      cub::DeviceSelect::Flagged(nullptr, b2, iota, is_cand, nodes.p, cnt.p, n, stream());
+      cub::DeviceRadixSort::SortPairs(nullptr, b3, keys.p, skeys.p, nodes.p, snodes.p, n, 0, 64, stream());
+      DevBuf<uint8_t> tmp(std::max(b1, std::max(b2, b3)));
+      // HD rows take a CTA each
+      GROOT_LAUNCH(lp_flag_hd_kernel, blocks_for(n, 256), 256, 0, n, g->rp.p, flag.p);
+      GROOT_CUDA(cub::DeviceSelect::Flagged(tmp.p, b1, iota, flag.p, hd.p, cnt.p, n, stream()));
+      uint32_t num_hd = 0;
+      cnt.download(&num_hd, 1);
+      w.zero();
+      GROOT_LAUNCH(lp_weights_kernel, blocks_for(n, 256), 256, 0, n, a->part_of.p, w.p);
+      stream_sync();
+      const unsigned sms = static_cast<unsigned>(num_sms());
+      uint32_t idle = 0;
+      for (; r < max_rounds && idle < 2; ++r) {
+        const uint32_t up = (r & 1u) == 0u;
+        GROOT_LAUNCH(lp_best_ld_kernel, blocks_for(n, 256), 256, 0, n, g->rp.p, g->col.p, a->part_of.p, up, cand.p);
+        if (num_hd)
+          GROOT_LAUNCH(lp_best_hd_kernel, std::min<uint32_t>(num_hd, sms * 4), 256,
+                       k <= kLpHistParts ? 4u * k : 0u, k, hd.p, num_hd, g->rp.p, g->col.p, a->part_of.p, up, cand.p);
+        // candidates compacted in node order, then a stable sort by (target, gain desc)
+        size_t bb = b2;
+        GROOT_CUDA(cub::DeviceSelect::Flagged(tmp.p, bb, iota, is_cand, nodes.p, cnt.p, n, stream()));
+        uint32_t m = 0;
+        cnt.download(&m, 1);
+        stream_sync();
+        uint32_t mv = 0;
+        if (m) {
+          GROOT_LAUNCH(lp_gather_keys_kernel, blocks_for(m, 256), 256, 0, m, nodes.p, cand.p, keys.p);
+          bb = b3;
+          GROOT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bb, keys.p, skeys.p, nodes.p, snodes.p, m, 0, 64,
+                                                     stream()));
+          out_cnt.zero();
+          GROOT_LAUNCH(lp_select_kernel, blocks_for(m, 256), 256, 0, m, skeys.p, snodes.p, a->part_of.p, w.p, cap,
+                       ok.p, out_cnt.p);
+          moved.zero();
+          GROOT_CUDA(cudaMemcpyAsync(wn.p, w.p, 4ull * k, cudaMemcpyDeviceToDevice, stream()));
+          GROOT_LAUNCH(lp_apply_kernel, blocks_for(m, 256), 256, 0, m, skeys.p, snodes.p, ok.p, out_cnt.p, w.p,
+                       a->part_of.p, wn.p, moved.p);
+          std::swap(w.p, wn.p);
+          moved.download(&mv, 1);
+          stream_sync();
+        }
+        total += mv;
+        idle = mv ? 0 : idle + 1;
+      }
+    }
+    stream_sync();
+  } catch (...) {
+    delete a;
+    throw;
+  }
+  if (rounds_out) *rounds_out = r;
+  if (moves_out) *moves_out = total;
+  return a;
+}
+
+}  // namespace groot

@@ -147,6 +147,11 @@ int main(int argc, char** argv) {
   std::uint64_t cross = 0;
   for (const auto& [u, v] : gb.fwd_edges) cross += pa.part_of[u] != pa.part_of[v];
   CHECK(edge_cut(gb, pa) == cross && crossing_fraction(gb, pa) == static_cast<double>(cross) / gb.fwd_edges.size());
+  PartitionAssignment ml = partition_multilevel(gb, 8, 7);  // k >= 8: the reference livelocks here
+  std::vector<std::uint32_t> sizes(8, 0);
+  for (std::uint32_t p : ml.part_of) ++sizes[p];
+  const std::uint32_t cap = static_cast<std::uint32_t>(std::ceil(1.05 * gb.n / 8));
+  CHECK(ml.k == 8 && *std::min_element(sizes.begin(), sizes.end()) >= 1 && *std::max_element(sizes.begin(), sizes.end()) <= cap);
   std::printf("device checks ok (accuracy %.4f)\n", full.accuracy);
   return 0;
 }

@@ -247,3 +247,29 @@ def test_restatement_vs_reference_plan_and_forward(width, copies, seed):
     np.testing.assert_array_equal(pred, rpred)
     np.testing.assert_array_equal(conf, rconf)
     assert acc == racc
+
+
+def test_partition_lp_restatement_matches_reference_where_it_terminates():
+    """the replacement partitioner (oracle restatement of the device
+    algorithm) equals the reference's partition_multilevel bit for bit on the
+    graphs where the reference terminates and its refined-topo candidate wins."""
+    R = _ref()
+    for w, k, b in ((64, 2, 1), (64, 4, 1), (32, 3, 4), (128, 2, 1)):
+        _, g = R.gen_csa(w)
+        if b > 1:
+            g = R.batch(g, b)
+        rp, ci = g.field("row_ptr"), g.field("col_idx")
+        n = rp.shape[0] - 1
+        np.testing.assert_array_equal(O.partition_lp(rp, ci, n, k), R.partition_multilevel(g, k, 7))
+
+
+@pytest.mark.parametrize("w,k", [(64, 8), (64, 16), (32, 64), (16, 7)])
+def test_partition_lp_terminates_within_cap(w, k):
+    """k >= 8 (the reference livelocks): every part nonempty and within
+    ceil(1.05 n / k), deterministic, cut no worse than the topo chunks."""
+    g = O.encode(O.gen_csa(w))
+    p = O.partition_lp(g.row_ptr, g.col_idx, g.n, k)
+    cnt = np.bincount(p, minlength=k)
+    assert cnt.min() >= 1 and cnt.max() <= O.lp_cap(g.n, k) and p.max() < k
+    np.testing.assert_array_equal(p, O.partition_lp(g.row_ptr, g.col_idx, g.n, k))
+    assert O.edge_cut(g, p) <= O.edge_cut(g, O.topo_chunks(g.n, k))
