@@ -73,6 +73,11 @@ int groot_csa_sizes(uint32_t width, uint32_t* num_inputs, uint32_t* num_ands,
                     uint32_t* num_outputs);
 int groot_gen_csa(uint32_t width, uint32_t* and_lits /*2*num_ands*/, uint32_t* out_lits,
                   uint8_t* labels);
+/* GroundTruth::supports of gen_csa_multiplier (src/circuitgen.cpp:30-32,
+ * 50-62): per adder root (HA sum / carry, FA sum / MAJ root) 5 u32 -- root
+ * node, arity (2 or 3), three support literals (third 0 when arity 2).
+ * records may be NULL (count only). */
+int groot_csa_supports(uint32_t width, uint32_t* count, uint32_t* records);
 /* Radix-4 Booth multiplier AIG (BASELINE config 3; no reference generator
  * exists): unsigned width x width -> 2*width product bits,
  * same input/output conventions and label classes as groot_gen_csa; encoder
@@ -193,6 +198,22 @@ void groot_model_free(groot_model* m);
 int groot_graph_prepare(const groot_graph* g);
 int groot_graph_release_context(const groot_graph* g);
 
+/* ---- training: train / loss_and_grads (src/gnn.cpp:180-255) --------------------
+ * Full-batch training on the resident graph in fp64 on the device: forward with
+ * the whole cache, softmax cross entropy averaged over nodes, backward with the
+ * transposed mean aggregation (a_mean_t), Adam with bias correction.
+ * init_params NULL -> init_model(seed) (Glorot, mt19937_64). params_out gets
+ * the trained parameters (ASG1 order); loss_out / accuracy_out (epochs
+ * entries each, may be NULL) the per-epoch training loss and accuracy before
+ * that epoch's update (TrainStats). Supported: in_dim 4, hidden <= 64,
+ * classes <= 8. Throws (GROOT_ERUNTIME) on a non-finite loss. */
+int groot_train(const groot_graph* g, uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                uint32_t epochs, double learning_rate, uint64_t seed, double beta1, double beta2, double adam_eps,
+                const double* init_params, double* params_out, double* loss_out, double* accuracy_out);
+/* loss_and_grads (src/gnn.cpp:180-209): mean loss and its gradient (ASG1 order). */
+int groot_loss_and_grads(const groot_graph* g, uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                         const double* params, double* grads_out, double* loss);
+
 /* ---- layer forward + classify ------------------------------------------------
  * forward (src/gnn.cpp:172-178): logits n x classes, fp32 on device (written to
  * host buffer logits_host). */
@@ -237,6 +258,31 @@ int groot_classify_aig(const groot_model* m, uint32_t num_inputs, uint32_t num_a
  * (no tensor cores, no HD/LD split). Not used by the product entry points. */
 int groot_debug_forward_naive(const groot_model* m, const groot_graph* g, float* logits_host,
                               uint8_t* labels_host);
+
+/* ---- verification consumer of the classes (src/verify.cpp:220-418) -----------
+ * backward_rewrite: label-guided backward rewriting of a width-bit multiplier
+ * candidate's output word polynomial against (sum 2^i a_i)(sum 2^j b_j);
+ * labels (num_labels >= 1 + ni + na, classes as NodeClass) steer XOR / MAJ
+ * substitutions, each validated on its cone's truth table first, so wrong
+ * labels cost time, never soundness. support_off (num_nodes+1) / support_nodes
+ * give per-node supports (node ids; both may be NULL). monomial_cap 0 = the
+ * reference's 2,000,000. Outputs (any may be NULL): equivalent, inconclusive
+ * (cap hit), residual term count, counts[3] = {substitutions, shortcuts,
+ * fallbacks}. groot_backward_rewrite_residual(): the residual as text (first
+ * 64 terms, "coeff*x3*x9 + ..."; thread-local, valid until the next call). */
+int groot_backward_rewrite(uint32_t num_inputs, uint32_t num_ands, const uint32_t* and_lits, uint32_t num_outputs,
+                           const uint32_t* out_lits, const uint8_t* labels, uint32_t num_labels,
+                           const uint32_t* support_off, const uint32_t* support_nodes, uint32_t width,
+                           uint64_t monomial_cap, int32_t* equivalent, int32_t* inconclusive,
+                           uint64_t* residual_terms, uint64_t* counts);
+const char* groot_backward_rewrite_residual(void);
+/* truth_table_equiv (src/verify.cpp:398-416): exhaustive simulation against
+ * the integer product, 2*width <= 20. */
+int groot_truth_table_equiv(uint32_t num_inputs, uint32_t num_ands, const uint32_t* and_lits, uint32_t num_outputs,
+                            const uint32_t* out_lits, uint32_t width, int32_t* equivalent);
+/* simulate (src/aig.cpp:115-138): output bits for one input assignment. */
+int groot_simulate(uint32_t num_inputs, uint32_t num_ands, const uint32_t* and_lits, uint32_t num_outputs,
+                   const uint32_t* out_lits, const uint8_t* inputs, uint8_t* outputs);
 
 /* ---- degree-polarised aggregation (src/spmm.cpp, inc/spmm.hpp) ---------------
  * build_plan (src/spmm.cpp:37-127) row classifier on device: per-band counts

@@ -42,6 +42,7 @@ _SIG = {
     "groot_empty_cache": (i32, []),
     "groot_csa_sizes": (i32, [u32, P, P, P]),
     "groot_gen_csa": (i32, [u32, P, P, P]),
+    "groot_csa_supports": (i32, [u32, P, P]),
     "groot_booth_sizes": (i32, [u32, P, P, P]),
     "groot_gen_booth": (i32, [u32, P, P, P]),
     "groot_aiger_sizes": (i32, [C.c_char_p, C.c_size_t, P, P, P]),
@@ -81,6 +82,8 @@ _SIG = {
     "groot_model_info": (i32, [P, P, P, P, P]),
     "groot_model_params": (i32, [P, P]),
     "groot_model_free": (None, [P]),
+    "groot_train": (i32, [P, u32, u32, u32, u32, u32, dbl, u64, dbl, dbl, dbl, P, P, P, P]),
+    "groot_loss_and_grads": (i32, [P, u32, u32, u32, u32, P, P, P]),
     "groot_forward": (i32, [P, P, P]),
     "groot_debug_forward_naive": (i32, [P, P, P, P]),
     "groot_predict_full": (i32, [P, P, P, P, P]),
@@ -90,6 +93,10 @@ _SIG = {
     "groot_predict_parts": (i32, [P, P, P, P, u32, P]),
     "groot_classify_aig": (i32, [P, u32, u32, P, u32, P, P, u32, P, P, P]),
     "groot_build_plan": (i32, [P, u32, u32, u32, P, P, P, P, P, P]),
+    "groot_backward_rewrite": (i32, [u32, u32, P, u32, P, P, u32, P, P, u32, u64, P, P, P, P]),
+    "groot_backward_rewrite_residual": (C.c_char_p, []),
+    "groot_truth_table_equiv": (i32, [u32, u32, P, u32, P, u32, P]),
+    "groot_simulate": (i32, [u32, u32, P, u32, P, P, P]),
     "groot_spmm_mean": (i32, [P, P, u32, P]),
     "groot_spmm_mean_dev": (i32, [P, P, u32, P]),
     "groot_spmm_csr": (i32, [u32, u32, P, P, P, P, u32, u32, P]),

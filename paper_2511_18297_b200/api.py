@@ -47,10 +47,30 @@ class Aig:
 
 @dataclass
 class CsaCircuit:
-    """gen_csa_multiplier result (inc/circuitgen.hpp:27-33): aig + GroundTruth labels."""
+    """gen_csa_multiplier result (inc/circuitgen.hpp:27-33): aig + GroundTruth labels.
+    `supports` (GroundTruth::supports: adder root -> support literals) is built on
+    first access for CSA circuits."""
     aig: Aig
     labels: np.ndarray
     width: int
+    kind: str = "csa"
+    _supports: dict | None = field(default=None, repr=False)
+
+    @property
+    def supports(self) -> dict:
+        if self._supports is None:
+            self._supports = csa_supports(self.width) if self.kind == "csa" else {}
+        return self._supports
+
+
+def csa_supports(width: int) -> dict:
+    """GroundTruth::supports of gen_csa_multiplier (src/circuitgen.cpp:30-32, 50-62):
+    {root node: [support literals 2v+inv]}."""
+    cnt = C.c_uint32()
+    check(lib().groot_csa_supports(width, C.byref(cnt), None))
+    rec = np.empty((cnt.value, 5), np.uint32)
+    check(lib().groot_csa_supports(width, C.byref(cnt), ptr(rec)))
+    return {int(r[0]): [int(x) for x in r[2:2 + int(r[1])]] for r in rec}
 
 
 def gen_csa_multiplier(width: int) -> CsaCircuit:
@@ -74,7 +94,7 @@ def gen_booth_multiplier(width: int) -> CsaCircuit:
     outs = np.empty(no.value, np.uint32)
     labels = np.empty(1 + ni.value + na.value + no.value, np.uint8)
     check(lib().groot_gen_booth(width, ptr(ands), ptr(outs), ptr(labels)))
-    return CsaCircuit(Aig(ni.value, ands, outs), labels, width)
+    return CsaCircuit(Aig(ni.value, ands, outs), labels, width, "booth")
 
 
 def parse_aiger(text: str | bytes) -> Aig:
@@ -497,6 +517,57 @@ def save_model(path: str, model: Model):
 
 
 @dataclass
+class TrainStats:
+    """inc/gnn.hpp:47-50: per-epoch loss and training accuracy."""
+    loss: np.ndarray
+    accuracy: np.ndarray
+
+
+def train(g: EdaGraph, epochs: int = 100, learning_rate: float = 1e-3, seed: int = 7, beta1: float = 0.9,
+          beta2: float = 0.999, adam_eps: float = 1e-8, depth: int = 4, hidden: int = 32,
+          classes: int = NUM_CLASSES, init=None, stats: TrainStats | None = None) -> Model:
+    """train (src/gnn.cpp:211-255) on the device, fp64: full-batch Adam from
+    init_model(seed) (or `init`, a parameter vector in ASG1 order)."""
+    np_ = param_count(depth, 4, hidden, classes)
+    out = np.empty(np_, np.float64)
+    loss = np.empty(max(epochs, 1), np.float64)
+    acc = np.empty(max(epochs, 1), np.float64)
+    ini = None if init is None else np.ascontiguousarray(init, np.float64)
+    check(lib().groot_train(g.handle, depth, 4, hidden, classes, epochs, learning_rate, seed, beta1, beta2, adam_eps,
+                            ptr(ini), ptr(out), ptr(loss), ptr(acc)))
+    if stats is not None:
+        stats.loss, stats.accuracy = loss[:epochs], acc[:epochs]
+    return Model.from_params(out, depth, 4, hidden, classes)
+
+
+def loss_and_grads(params, g: EdaGraph, depth: int = 4, hidden: int = 32, classes: int = NUM_CLASSES):
+    """loss_and_grads (src/gnn.cpp:180-209) on the device: (loss, grads in ASG1 order)."""
+    prm = np.ascontiguousarray(params, np.float64)
+    grads = np.empty_like(prm)
+    loss = C.c_double()
+    check(lib().groot_loss_and_grads(g.handle, depth, 4, hidden, classes, ptr(prm), ptr(grads), C.byref(loss)))
+    return loss.value, grads
+
+
+def grad_check(params, g: EdaGraph, epsilon: float = 1e-4, depth: int = 4, hidden: int = 32,
+               classes: int = NUM_CLASSES) -> float:
+    """grad_check (inc/gnn.hpp:88-90): max over parameters of |a - n| / max(|a|, |n|, 1),
+    analytic (device backward) vs central differences (device forward losses)."""
+    prm = np.ascontiguousarray(params, np.float64)
+    _, ana = loss_and_grads(prm, g, depth, hidden, classes)
+    worst = 0.0
+    for i in range(prm.shape[0]):
+        p = prm.copy()
+        p[i] += epsilon
+        lp, _ = loss_and_grads(p, g, depth, hidden, classes)
+        p[i] -= 2 * epsilon
+        lm, _ = loss_and_grads(p, g, depth, hidden, classes)
+        num = (lp - lm) / (2 * epsilon)
+        worst = max(worst, abs(ana[i] - num) / max(abs(ana[i]), abs(num), 1.0))
+    return worst
+
+
+@dataclass
 class Prediction:
     """inc/gnn.hpp:75-79."""
     labels: np.ndarray
@@ -601,6 +672,71 @@ def classify_aig(model: Model, aig: Aig, labels, copies: int = 1) -> Prediction:
     check(lib().groot_classify_aig(model.handle, aig.num_inputs, aig.num_ands, ptr(ands), outs.shape[0],
                                    ptr(outs), ptr(lab), copies, ptr(pred), ptr(conf), C.byref(acc)))
     return Prediction(pred, conf, acc.value)
+
+
+# ---------------------------------------------------------------------------
+# verification consumer of the classes (inc/verify.hpp, src/verify.cpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class VerifyReport:
+    """inc/verify.hpp:19-27 (the residual as text, first 64 terms)."""
+    equivalent: bool
+    inconclusive: bool
+    residual_terms: int
+    residual: str
+    substitution_count: int
+    shortcut_count: int
+    fallback_count: int
+
+
+def backward_rewrite(aig: Aig, labels, width: int, supports: dict | None = None,
+                     monomial_cap: int = 2_000_000) -> VerifyReport:
+    """src/verify.cpp:220-395: label-guided backward rewriting (host, BigInt)."""
+    ands = np.ascontiguousarray(aig.and_lits, np.uint32)
+    outs = np.ascontiguousarray(aig.out_lits, np.uint32)
+    lab = np.ascontiguousarray(labels, np.uint8)
+    off = nodes = None
+    if supports:
+        nn = aig.num_nodes
+        cnt = np.zeros(nn, np.uint32)
+        for v, sup in supports.items():
+            if v < nn:
+                cnt[v] = len(sup)
+        off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint32)
+        nodes = np.zeros(int(off[-1]), np.uint32)
+        for v, sup in supports.items():
+            if v < nn:
+                nodes[off[v]:off[v + 1]] = [x >> 1 for x in sup]
+    eq, inc = C.c_int32(), C.c_int32()
+    rt = C.c_uint64()
+    counts = np.zeros(3, np.uint64)
+    check(lib().groot_backward_rewrite(aig.num_inputs, aig.num_ands, ptr(ands), outs.shape[0], ptr(outs), ptr(lab),
+                                       lab.shape[0], ptr(off), ptr(nodes), width, monomial_cap, C.byref(eq),
+                                       C.byref(inc), C.byref(rt), ptr(counts)))
+    return VerifyReport(bool(eq.value), bool(inc.value), rt.value, lib().groot_backward_rewrite_residual().decode(),
+                        int(counts[0]), int(counts[1]), int(counts[2]))
+
+
+def truth_table_equiv(aig: Aig, width: int) -> bool:
+    """src/verify.cpp:398-416 (2*width <= 20)."""
+    ands = np.ascontiguousarray(aig.and_lits, np.uint32)
+    outs = np.ascontiguousarray(aig.out_lits, np.uint32)
+    eq = C.c_int32()
+    check(lib().groot_truth_table_equiv(aig.num_inputs, aig.num_ands, ptr(ands), outs.shape[0], ptr(outs), width,
+                                        C.byref(eq)))
+    return bool(eq.value)
+
+
+def simulate(aig: Aig, inputs) -> np.ndarray:
+    """src/aig.cpp:130-138: output bits for one input assignment."""
+    ands = np.ascontiguousarray(aig.and_lits, np.uint32)
+    outs = np.ascontiguousarray(aig.out_lits, np.uint32)
+    inp = np.ascontiguousarray(inputs, np.uint8)
+    if inp.shape[0] != aig.num_inputs:
+        raise GrootInvalidArgument(1, "simulate: assignment length != number of inputs")
+    out = np.empty(outs.shape[0], np.uint8)
+    check(lib().groot_simulate(aig.num_inputs, aig.num_ands, ptr(ands), outs.shape[0], ptr(outs), ptr(inp), ptr(out)))
+    return out
 
 
 # ---------------------------------------------------------------------------

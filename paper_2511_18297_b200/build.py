@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libgroot_b200.so")
-SOURCES = ["graph_build.cu", "forward.cu", "tile_plan.cu", "plan.cu", "partition_lp.cu", "capi.cpp", "runtime.cpp"]
+SOURCES = ["graph_build.cu", "forward.cu", "tile_plan.cu", "plan.cu", "partition_lp.cu", "train.cu", "capi.cpp", "runtime.cpp", "verify.cpp"]
 HEADERS = ["common.cuh", "ptx.cuh", "tile_plan.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -104,6 +104,9 @@ struct Csa {
   std::vector<uint32_t> ands;    // (left, right) literal pairs
   std::vector<uint8_t> labels;   // const + PIs + ANDs (+ POs at the end)
   std::vector<uint32_t> outs;
+  // GroundTruth::supports (src/circuitgen.cpp:30-32, 50-62): root node, arity,
+  // 3 support literals (the third unused for a half adder)
+  std::vector<uint32_t> sup;
 
   explicit Csa(uint32_t width) : w(width), inputs(2 * width) {
     labels.assign(1 + inputs, kAnd);
@@ -125,7 +128,9 @@ struct Csa {
       const uint32_t c = node(a, b, kMaj);
       const uint32_t nr = node(a ^ 1, b ^ 1, kAnd);
       *carry = c;
-      return node(c ^ 1, nr ^ 1, kXor);
+      const uint32_t sum = node(c ^ 1, nr ^ 1, kXor);
+      sup.insert(sup.end(), {sum >> 1, 2u, a, b, 0u, c >> 1, 2u, a, b, 0u});
+      return sum;
     }
     const uint32_t cin = in[2];  // gen_full_adder
     const uint32_t c1 = node(a, b, kAnd);
@@ -136,6 +141,7 @@ struct Csa {
     const uint32_t s = node(c2 ^ 1, n2 ^ 1, kXor);
     const uint32_t mj = node(c1 ^ 1, c2 ^ 1, kMaj);
     *carry = mj ^ 1;
+    sup.insert(sup.end(), {s >> 1, 3u, a, b, cin, mj >> 1, 3u, a, b, cin});
     return s;
   }
   void build() {
@@ -451,6 +457,13 @@ groot_model* model_create(uint32_t depth, uint32_t in_dim, uint32_t hidden, uint
 
 }  // namespace
 
+void init_model_params(uint64_t seed, uint32_t in_dim, uint32_t hidden, uint32_t classes, uint32_t depth, double* prm) {
+  init_params(seed, in_dim, hidden, classes, depth, prm);
+}
+void train_device(const groot_graph*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, double, uint64_t, double, double,
+                  double, const double*, double*, double*, double*);
+double loss_and_grads_device(const groot_graph*, uint32_t, uint32_t, uint32_t, uint32_t, const double*, double*);
+
 void set_last_error(const std::string& msg) { g_error = msg; }
 
 static void need(const void* p, const char* what) {
@@ -528,6 +541,17 @@ int groot_gen_csa(uint32_t width, uint32_t* and_lits, uint32_t* out_lits, uint8_
     if (and_lits) std::copy(c.ands.begin(), c.ands.end(), and_lits);
     if (out_lits) std::copy(c.outs.begin(), c.outs.end(), out_lits);
     if (labels) std::copy(c.labels.begin(), c.labels.end(), labels);
+  });
+}
+
+int groot_csa_supports(uint32_t width, uint32_t* count, uint32_t* records) {
+  return guarded([&] {
+    if (width < 2) fail(GROOT_EINVAL, "gen_csa_multiplier: width must be >= 2");
+    need(count, "groot_csa_supports");
+    Csa c(width);
+    c.build();
+    *count = static_cast<uint32_t>(c.sup.size() / 5);
+    if (records) std::copy(c.sup.begin(), c.sup.end(), records);
   });
 }
 
@@ -868,6 +892,30 @@ int groot_model_params(const groot_model* m, double* params) {
 }
 
 void groot_model_free(groot_model* m) { delete m; }
+
+// ---- training (src/gnn.cpp:180-255) --------------------------------------------------
+int groot_train(const groot_graph* g, uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                uint32_t epochs, double learning_rate, uint64_t seed, double beta1, double beta2, double adam_eps,
+                const double* init_params, double* params_out, double* loss_out, double* accuracy_out) {
+  return guarded([&] {
+    need(g, "groot_train");
+    DeviceScope ds_g(g->device);
+    need(params_out, "groot_train");
+    train_device(g, depth, in_dim, hidden, classes, epochs, learning_rate, seed, beta1, beta2, adam_eps, init_params,
+                 params_out, loss_out, accuracy_out);
+  });
+}
+
+int groot_loss_and_grads(const groot_graph* g, uint32_t depth, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                         const double* params, double* grads_out, double* loss) {
+  return guarded([&] {
+    need(g, "groot_loss_and_grads");
+    DeviceScope ds_g(g->device);
+    need(params, "groot_loss_and_grads");
+    const double l = loss_and_grads_device(g, depth, in_dim, hidden, classes, params, grads_out);
+    if (loss) *loss = l;
+  });
+}
 
 // ---- forward / predict -------------------------------------------------------------
 static void finish_confusion(const uint64_t* conf, uint32_t n, uint64_t* confusion, double* accuracy) {
