@@ -9,8 +9,8 @@
 //    operator()(i,j)) instead of Eigen::Matrix (Eigen is not a dependency).
 //  * forward() returns fp32 logits widened to double (the device path computes
 //    in fp32 with a 3xTF32 tensor-core transform).
-//  * GroundTruth::supports is not populated by gen_csa_multiplier (it only
-//    feeds the verifier, which is outside the hot path).
+//  * VerifyReport carries the residual polynomial as text plus its term count
+//    (the reference's Polynomial is a Boost.Multiprecision type).
 //  * aigsage::gpu::DeviceGraph keeps a graph resident in HBM across calls;
 //    the value-returning functions copy to the host like the reference does.
 //
@@ -21,6 +21,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <fstream>
@@ -152,7 +153,7 @@ inline constexpr std::uint32_t kNumClasses = 5;
 struct GroundTruth {
   std::vector<std::uint8_t> labels;
   std::vector<std::uint32_t> po_nodes;
-  std::map<std::uint32_t, std::vector<Literal>> supports;  // not populated (verifier input only)
+  std::map<std::uint32_t, std::vector<Literal>> supports;  // adder roots -> support literals (CSA generator)
 };
 
 struct CsaCircuit {
@@ -189,6 +190,14 @@ inline CsaCircuit gen_csa_multiplier(std::uint32_t width) {
   detail::check(groot_gen_csa(width, ands.data(), outs.data(), c.gt.labels.data()));
   c.aig = Aig::from_lits(ni, ands, outs);
   for (std::uint32_t k = 0; k < no; ++k) c.gt.po_nodes.push_back(c.aig.num_nodes() + k);
+  std::uint32_t nsup = 0;  // GroundTruth::supports (src/circuitgen.cpp:30-32, 50-62)
+  detail::check(groot_csa_supports(width, &nsup, nullptr));
+  std::vector<std::uint32_t> rec(5ull * nsup);
+  detail::check(groot_csa_supports(width, &nsup, rec.data()));
+  for (std::uint32_t i = 0; i < nsup; ++i) {
+    std::vector<Literal>& sup = c.gt.supports[rec[5 * i]];
+    for (std::uint32_t a = 0; a < rec[5 * i + 1]; ++a) sup.push_back(decode_lit(rec[5 * i + 2 + a]));
+  }
   // Adder counts by replaying the column-slot occupancy of the generator
   // (src/circuitgen.cpp:90-127); reduce() makes a HA for 2 inputs, a FA for 3.
   const std::uint32_t w = width;
@@ -237,6 +246,93 @@ inline void write_labels(const std::string& path, const std::vector<std::uint8_t
   std::ofstream out(path);
   if (!out) throw std::runtime_error("cannot write label file: " + path);
   for (std::size_t i = 0; i < labels.size(); ++i) out << i << ' ' << static_cast<int>(labels[i]) << '\n';
+}
+
+// write_supports / load_supports (src/circuitgen.cpp:200-227): "root arity lit..." lines
+inline void write_supports(const std::string& path, const std::map<std::uint32_t, std::vector<Literal>>& supports) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write support file: " + path);
+  for (const auto& [root, sup] : supports) {
+    out << root << ' ' << sup.size();
+    for (const Literal& l : sup) out << ' ' << encode_lit(l);
+    out << '\n';
+  }
+}
+inline std::map<std::uint32_t, std::vector<Literal>> load_supports(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open support file: " + path);
+  std::map<std::uint32_t, std::vector<Literal>> supports;
+  std::uint32_t root;
+  std::size_t arity;
+  while (in >> root >> arity) {
+    std::vector<Literal> sup;
+    for (std::size_t i = 0; i < arity; ++i) {
+      std::uint64_t enc;
+      if (!(in >> enc)) throw std::runtime_error("support file: truncated entry");
+      sup.push_back(decode_lit(static_cast<std::uint32_t>(enc)));
+    }
+    supports[root] = std::move(sup);
+  }
+  return supports;
+}
+
+// ---- inc/verify.hpp: the consumer of the classes ------------------------------------
+struct VerifyOptions {
+  std::size_t monomial_cap = 2'000'000;
+};
+// The residual polynomial is returned as text (first 64 terms) with its term
+// count: the reference's Polynomial is a Boost.Multiprecision type.
+struct VerifyReport {
+  bool equivalent = false;
+  bool inconclusive = false;
+  std::string residual;
+  std::uint64_t residual_terms = 0;
+  std::uint64_t substitution_count = 0;
+  std::uint64_t shortcut_count = 0;
+  std::uint64_t fallback_count = 0;
+};
+// backward_rewrite (src/verify.cpp:220-395), host.
+inline VerifyReport backward_rewrite(const Aig& g, const std::vector<std::uint8_t>& labels,
+                                     const std::map<std::uint32_t, std::vector<Literal>>& supports, std::uint32_t width,
+                                     const VerifyOptions& opts = {}) {
+  const auto ands = g.and_lits();
+  const auto outs = g.out_lits();
+  std::vector<std::uint32_t> off(g.num_nodes() + 1ull, 0), nodes;
+  for (std::uint32_t v = 0; v < g.num_nodes(); ++v) {
+    if (auto it = supports.find(v); it != supports.end())
+      for (const Literal& l : it->second) nodes.push_back(l.node);
+    off[v + 1] = static_cast<std::uint32_t>(nodes.size());
+  }
+  VerifyReport r;
+  std::int32_t eq = 0, inc = 0;
+  std::uint64_t counts[3];
+  detail::check(groot_backward_rewrite(g.num_inputs(), g.num_ands(), ands.data(), static_cast<std::uint32_t>(outs.size()),
+                                       outs.data(), labels.data(), static_cast<std::uint32_t>(labels.size()), off.data(),
+                                       nodes.data(), width, opts.monomial_cap, &eq, &inc, &r.residual_terms, counts));
+  r.equivalent = eq != 0;
+  r.inconclusive = inc != 0;
+  r.residual = groot_backward_rewrite_residual();
+  r.substitution_count = counts[0];
+  r.shortcut_count = counts[1];
+  r.fallback_count = counts[2];
+  return r;
+}
+inline bool truth_table_equiv(const Aig& g, std::uint32_t width) {  // src/verify.cpp:398-416
+  const auto ands = g.and_lits();
+  const auto outs = g.out_lits();
+  std::int32_t eq = 0;
+  detail::check(groot_truth_table_equiv(g.num_inputs(), g.num_ands(), ands.data(), static_cast<std::uint32_t>(outs.size()),
+                                        outs.data(), width, &eq));
+  return eq != 0;
+}
+inline std::vector<std::uint8_t> simulate(const Aig& g, const std::vector<std::uint8_t>& assignment) {  // src/aig.cpp:130
+  if (assignment.size() != g.num_inputs()) throw std::invalid_argument("simulate: assignment length != number of inputs");
+  const auto ands = g.and_lits();
+  const auto outs = g.out_lits();
+  std::vector<std::uint8_t> out(outs.size());
+  detail::check(groot_simulate(g.num_inputs(), g.num_ands(), ands.data(), static_cast<std::uint32_t>(outs.size()),
+                               outs.data(), assignment.data(), out.data()));
+  return out;
 }
 
 // ---- device-resident handles -------------------------------------------------------
@@ -605,6 +701,55 @@ inline Model load_model(const std::string& path) {  // src/gnn.cpp:349-372
 inline void save_model(const std::string& path, const Model& model) {  // src/gnn.cpp:330-345
   auto m = model.to_device();
   detail::check(groot_model_save(m.get(), path.c_str()));
+}
+
+// ---- training (inc/gnn.hpp:38-50, src/gnn.cpp:180-255), fp64 on the device ---------------
+struct TrainConfig {
+  std::uint32_t epochs = 100;
+  double learning_rate = 1e-3;
+  std::uint64_t seed = 7;
+  double beta1 = 0.9;
+  double beta2 = 0.999;
+  double adam_eps = 1e-8;
+};
+struct TrainStats {
+  std::vector<double> loss;
+  std::vector<double> accuracy;
+};
+inline Model train(const EdaGraph& g, const TrainConfig& cfg, TrainStats* stats = nullptr) {
+  if (cfg.learning_rate <= 0) throw std::invalid_argument("train: learning rate must be positive");
+  auto d = g.to_device();
+  const std::uint32_t depth = 4, in = 4, hid = 32, cls = kNumClasses;
+  std::vector<double> p(groot_param_count(depth, in, hid, cls)), loss(cfg.epochs), acc(cfg.epochs);
+  detail::check(groot_train(d.get(), depth, in, hid, cls, cfg.epochs, cfg.learning_rate, cfg.seed, cfg.beta1, cfg.beta2,
+                            cfg.adam_eps, nullptr, p.data(), loss.data(), acc.data()));
+  if (stats) {
+    stats->loss = loss;
+    stats->accuracy = acc;
+  }
+  return Model::from_params(p, depth, in, hid, cls);
+}
+// grad_check (inc/gnn.hpp:88-90): max |a - n| / max(|a|, |n|, 1) over every
+// parameter, analytic (device backward) vs central differences (device loss).
+inline double grad_check(const Model& model, const EdaGraph& g, double epsilon = 1e-4) {
+  auto d = g.to_device();
+  const std::uint32_t depth = static_cast<std::uint32_t>(model.layers.size()), in = model.in_dim(),
+                      hid = static_cast<std::uint32_t>(model.layers.front().w_self.cols()), cls = model.num_classes();
+  std::vector<double> p = model.params(), ana(p.size()), scratch(p.size());
+  double loss = 0, worst = 0;
+  detail::check(groot_loss_and_grads(d.get(), depth, in, hid, cls, p.data(), ana.data(), &loss));
+  for (std::size_t i = 0; i < p.size(); ++i) {
+    const double keep = p[i];
+    double lp = 0, lm = 0;
+    p[i] = keep + epsilon;
+    detail::check(groot_loss_and_grads(d.get(), depth, in, hid, cls, p.data(), nullptr, &lp));
+    p[i] = keep - epsilon;
+    detail::check(groot_loss_and_grads(d.get(), depth, in, hid, cls, p.data(), nullptr, &lm));
+    p[i] = keep;
+    const double num = (lp - lm) / (2 * epsilon);
+    worst = std::max(worst, std::abs(ana[i] - num) / std::max({std::abs(ana[i]), std::abs(num), 1.0}));
+  }
+  return worst;
 }
 
 struct Prediction {

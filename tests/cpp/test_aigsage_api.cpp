@@ -57,6 +57,17 @@ int main(int argc, char** argv) {
   pool.for_each(hit.size(), [&](std::size_t i) { hit[i] += 1; });
   CHECK(pool.workers() == 4 && std::count(hit.begin(), hit.end(), 1) == 100);
   CHECK(default_pool().workers() >= 1);
+  // verifier (host): ground-truth labels and the generator's supports prove the multiplier
+  CsaCircuit c6 = gen_csa_multiplier(6);
+  CHECK(c6.gt.supports.size() == 2u * 6 * 5);
+  VerifyReport vr = backward_rewrite(c6.aig, c6.gt.labels, c6.gt.supports, 6);
+  CHECK(vr.equivalent && !vr.inconclusive && vr.shortcut_count == 30 && vr.residual.empty());
+  CHECK(truth_table_equiv(c6.aig, 6));
+  std::vector<std::uint8_t> in12(12, 1);
+  std::vector<std::uint8_t> prod = simulate(c6.aig, in12);  // 63 * 63 = 3969
+  std::uint32_t word = 0;
+  for (std::size_t k = 0; k < prod.size(); ++k) word |= static_cast<std::uint32_t>(prod[k]) << k;
+  CHECK(word == 63u * 63u);
   if (!gpu) {
     std::printf("host checks ok\n");
     return 0;
@@ -147,6 +158,11 @@ int main(int argc, char** argv) {
   std::uint64_t cross = 0;
   for (const auto& [u, v] : gb.fwd_edges) cross += pa.part_of[u] != pa.part_of[v];
   CHECK(edge_cut(gb, pa) == cross && crossing_fraction(gb, pa) == static_cast<double>(cross) / gb.fwd_edges.size());
+  TrainStats ts;
+  TrainConfig tc;
+  tc.epochs = 10;
+  Model tm = train(g, tc, &ts);
+  CHECK(ts.loss.size() == 10 && ts.loss.back() < ts.loss.front() && tm.layers.size() == 4);
   PartitionAssignment ml = partition_multilevel(gb, 8, 7);  // k >= 8: the reference livelocks here
   std::vector<std::uint32_t> sizes(8, 0);
   for (std::uint32_t p : ml.part_of) ++sizes[p];

@@ -62,7 +62,9 @@ def test_loss_and_grads_and_grad_check(api):
     """Analytic gradient vs central differences (SPEC acceptance #11, inc/gnn.hpp:88-90),
     on a depth-2, hidden-8 model of a 4-bit CSA (every parameter checked)."""
     g = graph(api, 4)
-    prm = O.init_model(5, hidden=8, depth=2)
+    # perturbed so no pre-activation sits exactly on the ReLU kink (zero biases put
+    # the isolated constant node's z at 0, where central differences are one-sided)
+    prm = O.init_model(5, hidden=8, depth=2) + np.random.default_rng(1).normal(0, 0.05, O.param_count(2, 4, 8, 5))
     loss, grads = api.loss_and_grads(prm, g, depth=2, hidden=8)
     assert np.isfinite(loss) and grads.shape == prm.shape and np.abs(grads).max() > 0
     assert api.grad_check(prm, g, epsilon=1e-5, depth=2, hidden=8) <= 1e-6
@@ -72,3 +74,23 @@ def test_train_errors(api):
     g = graph(api, 4)
     with pytest.raises(ValueError, match="learning rate must be positive"):
         api.train(g, epochs=1, learning_rate=0.0)
+
+
+def test_verify_from_predicted_classes(api, golden_dir):
+    """The paper's loop: classes predicted on the device by the
+    device-trained model drive backward_rewrite to prove 8/16/32-bit CSA
+    multipliers; the same classes on a mutated multiplier give a nonzero residual."""
+    model = api.load_model(os.path.join(golden_dir, "trained_csa64_gpu.asg1"))
+    for w in (8, 16, 32):
+        c = api.gen_csa_multiplier(w)
+        pred = api.predict_full(model, api.encode(c.aig, c.labels))
+        rep = api.backward_rewrite(c.aig, pred.labels, w)
+        assert rep.equivalent and not rep.inconclusive, (w, rep)
+        assert rep.shortcut_count > 0
+    c = api.gen_csa_multiplier(8)
+    pred = api.predict_full(model, api.encode(c.aig, c.labels))
+    bad = api.Aig(c.aig.num_inputs, c.aig.and_lits.copy(), c.aig.out_lits.copy())
+    bad.and_lits[len(bad.and_lits) // 2, 0] ^= 1  # one inverted fan-in
+    rep = api.backward_rewrite(bad, pred.labels, 8)
+    assert not rep.equivalent and rep.residual_terms > 0
+    assert not api.truth_table_equiv(bad, 8)
