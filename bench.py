@@ -58,6 +58,9 @@ def parse():
                    help="strong: --batch copies in total, split over the ranks; weak: --batch copies per rank")
     p.add_argument("--parts-k", type=int, default=64, help="topo partitions of the partitioned-chain measurement")
     p.add_argument("--no-side", action="store_true", help="skip the side measurements (development)")
+    p.add_argument("--mode", choices=["copies", "halo"], default="copies",
+                   help="copies: whole batch copies per rank (default); halo: one partition per rank "
+                        "(partition_multilevel, k = ranks) forwarded with a per-layer NCCL halo exchange (mode X)")
     return p.parse_args()
 
 
@@ -577,8 +580,89 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_halo(args):
+    """Mode X: the global graph cut into k = ranks parts by the
+    partition_multilevel replacement, rank r forwards its regrown part layer by
+    layer (groot_layer_dev) and exchanges its boundary rows with the owners
+    after every layer but the last (device-resident index lists, one NCCL
+    all-to-all per layer). Every core row's logits equal the whole graph's."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_18297_b200 import api, shard
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    api.set_stream(stream.cuda_stream)
+    circ = (api.gen_booth_multiplier if args.circuit == "booth" else api.gen_csa_multiplier)(args.width)
+    g1 = api.encode(circ.aig, circ.labels)
+    g = api.batch(g1, args.batch) if args.batch > 1 else g1
+    E = g.num_undirected_edges()
+    pa = api.partition_multilevel(g, world) if world > 1 else api.partition_topo_chunks(g, 1)
+    parts = api.regrow(g, pa)
+    cores = [parts[p].core_nodes for p in range(world)]
+    bnds = [parts[p].boundary_nodes for p in range(world)]
+    plans = shard.halo_plans(pa.part_of, cores, bnds)
+    cut = api.edge_cut(g, pa)
+    loc = api.materialize(g, parts, rank)
+    del g, g1, parts
+    model = api.load_model(MODEL_FILE)
+    layer = shard.device_layer_fn(model, loc)
+    depth = model.info()["depth"]
+    ex = shard.HaloExchanger(plans[rank], 32, "cuda") if world > 1 else None
+
+    def step():
+        h = None
+        for l in range(depth):
+            h = layer(l, h)
+            if ex is not None and l + 1 < depth:
+                ex(h)
+        return h
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local).start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    halo_bytes = ex.bytes_per_call * (depth - 1) if ex is not None else 0
+    if world > 1:
+        t = torch.tensor([ms, float(halo_bytes)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:])
+        ms, halo_bytes = float(t[0].item()), int(t[1].item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": E / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate)",
+            "data": f"synthetic (deterministic {args.circuit.upper()} multiplier generator; trained 8-bit ASG1 weights)",
+            "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {args.batch}, "
+                                   f"{world} partitions (partition_multilevel), exact halo (mode X)",
+                       "width": args.width, "global_batch": args.batch, "parallelism": f"{world} parts, NCCL halo",
+                       "edge_cut": int(cut), "halo_rows_per_rank": [int(sum(x.shape[0] for x in pl.recv)) for pl in plans]},
+            "halo": {"bytes_per_step_all_ranks": halo_bytes, "exchanges_per_step": depth - 1},
+            "clocks": clocks, "gpu_launches": None}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.mode == "halo" and args.impl == "ours":
+        run_halo(args)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
         rank, world, _ = dist_env()

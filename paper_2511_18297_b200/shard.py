@@ -206,19 +206,41 @@ def halo_plans(part_of: np.ndarray, cores: Sequence[np.ndarray], boundaries: Seq
     return plans
 
 
+class HaloExchanger:
+    """Device-resident exchange of one rank's boundary rows (mode X).
+
+    The plan's index lists are uploaded once (send rows gathered by one
+    index_select, received rows scattered by one index_copy_) and the send /
+    receive buffers are allocated once for the row width; each call is then
+    gather -> all_to_all_single (NCCL over NVLink on the box) -> scatter with
+    no host work and no host<->device copy."""
+
+    def __init__(self, plan: HaloPlan, f: int, device, dtype=None):
+        import torch
+        self.plan = plan
+        dtype = dtype or torch.float32
+        send = np.concatenate(plan.send) if plan.send else np.zeros(0, np.int64)
+        recv = np.concatenate(plan.recv) if plan.recv else np.zeros(0, np.int64)
+        self.send_idx = torch.as_tensor(send.astype(np.int64), device=device)
+        self.recv_idx = torch.as_tensor(recv.astype(np.int64), device=device)
+        self.send_buf = torch.empty((self.send_idx.shape[0], f), dtype=dtype, device=device)
+        self.recv_buf = torch.empty((self.recv_idx.shape[0], f), dtype=dtype, device=device)
+        self.send_counts = plan.send_counts
+        self.recv_counts = plan.recv_counts
+        self.bytes_per_call = int(self.send_buf.numel() + self.recv_buf.numel()) * self.send_buf.element_size()
+
+    def __call__(self, h, plan=None):
+        import torch
+        torch.index_select(h, 0, self.send_idx, out=self.send_buf)
+        _dist().all_to_all_single(self.recv_buf, self.send_buf, self.recv_counts, self.send_counts)
+        h.index_copy_(0, self.recv_idx, self.recv_buf)
+        return h
+
+
 def exchange_halo(h, plan: HaloPlan):
-    """All-to-all of the boundary rows of a (num_local x f) torch tensor, in place."""
-    import torch
-    dist = _dist()
-    f = h.shape[1]
-    dev = h.device
-    send_idx = torch.as_tensor(np.concatenate(plan.send) if plan.send else np.zeros(0, np.int64), device=dev)
-    recv_idx = torch.as_tensor(np.concatenate(plan.recv) if plan.recv else np.zeros(0, np.int64), device=dev)
-    out = torch.empty((int(recv_idx.shape[0]), f), dtype=h.dtype, device=dev)
-    inp = h.index_select(0, send_idx.long()).contiguous()
-    dist.all_to_all_single(out, inp, plan.recv_counts, plan.send_counts)
-    h.index_copy_(0, recv_idx.long(), out)
-    return h
+    """One-shot all-to-all of the boundary rows of a (num_local x f) torch tensor,
+    in place (builds a HaloExchanger; reuse one across layers instead)."""
+    return HaloExchanger(plan, h.shape[1], h.device, h.dtype)(h)
 
 
 def predict_exact(plan: HaloPlan, depth: int, layer: Callable, exchange: Callable = exchange_halo):

@@ -126,30 +126,37 @@ def np_layer_fn(hg, prm, depth=4, in_dim=4, hidden=32, classes=5):
     return layer
 
 
-def _xworker(rank, world, port, out_dir):
+def _xworker(rank, world, port, out_dir, partitioner="topo"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import torch
         prm = O.init_model(7)
-        g = O.encode(O.gen_csa(16))  # one copy: topo parts straddle the circuit
-        part_of = O.topo_chunks(g.n, world)
+        g = O.encode(O.gen_csa(16))  # one copy: the parts straddle the circuit
+        if partitioner == "topo":
+            part_of = O.topo_chunks(g.n, world)
+        else:  # the partition_multilevel replacement's cut
+            part_of = O.partition_lp(g.row_ptr, g.col_idx, g.n, world)
         parts = O.regrow(g, part_of, world)
         plans = shard.halo_plans(part_of, [p.core_nodes for p in parts], [p.boundary_nodes for p in parts])
         local = O.materialize(g, parts[rank])
-        logits = shard.predict_exact(plans[rank], 4, np_layer_fn(local, prm))
+        ex = shard.HaloExchanger(plans[rank], 32, "cpu", torch.float64)  # index lists built once
+        logits = shard.predict_exact(plans[rank], 4, np_layer_fn(local, prm), exchange=ex)
         np.savez(os.path.join(out_dir, f"x{rank}.npz"), core=parts[rank].core_nodes, logits=logits.numpy())
     finally:
         dist.destroy_process_group()
 
 
-def test_exact_halo_mode_matches_whole_graph(tmp_path):
-    """Mode X over 3 gloo ranks (topo parts straddling one 16-bit CSA copy):
-    the core rows' logits equal the whole-graph forward (predict_full semantics),
-    which the reference's partitioned predict (mode R) does not reproduce."""
+@pytest.mark.parametrize("partitioner", ["topo", "lp"])
+def test_exact_halo_mode_matches_whole_graph(tmp_path, partitioner):
+    """Mode X over 3 gloo ranks (parts straddling one 16-bit CSA copy; topo chunks
+    or the LP partitioner's cut): the core rows' logits equal the whole-graph
+    forward (predict_full semantics), which the reference's partitioned predict
+    (mode R) does not reproduce."""
     world = 3
-    mp.spawn(_xworker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_xworker, args=(world, _free_port(), str(tmp_path), partitioner), nprocs=world, join=True)
     g = O.encode(O.gen_csa(16))
     prm = O.init_model(7)
     ref = O.forward(g, prm)
