@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgroot_b200.so")
+LIB_PATH = os.environ.get("GROOT_LIB") or os.path.join(_PKG, "libgroot_b200.so")  # GROOT_LIB: experiment variant
 _LIB = None
 
 P = C.c_void_p

@@ -13,8 +13,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libgroot_b200.so")
+# GROOT_BUILD_TAG=x builds an experiment variant (objects in _build_x/, library
+# libgroot_b200_x.so, selected at run time with GROOT_LIB); the product is untagged.
+_TAG = os.environ.get("GROOT_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, "libgroot_b200" + (f"_{_TAG}" if _TAG else "") + ".so")
 SOURCES = ["graph_build.cu", "forward.cu", "tile_plan.cu", "plan.cu", "partition_lp.cu", "train.cu", "capi.cpp", "runtime.cpp", "verify.cpp"]
 HEADERS = ["common.cuh", "ptx.cuh", "tile_plan.cuh"]
 

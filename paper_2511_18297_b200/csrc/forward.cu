@@ -60,11 +60,14 @@ constexpr uint32_t kTmemCols = 512;
 static_assert(kAccCol0 + 2 * kAccCols <= kTmemCols, "tensor memory budget");
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr int kMaxClasses = 8;
-// Last layer: the 32 -> classes head runs on the tensor core too. The epilogue
-// writes relu(acc + b) split into TF32 hi (over the accumulator it just read)
-// and lo (kHeadLoCol); one MMA group of N = 16 (classes zero-padded) leaves the
+// Last layer: the 32 -> classes head runs on the tensor core too. The last
+// layer keeps ONE accumulator (the epilogue frees it right after loading it)
+// and uses the second accumulator's columns for the head's A operand: the
+// epilogue writes relu(acc + b) split into TF32 hi (kHeadHiCol) and lo
+// (kHeadLoCol); one MMA group of N = 16 (classes zero-padded) leaves the
 // logits in kHeadDCol.
 constexpr uint32_t kHeadN = 16;
+constexpr uint32_t kHeadHiCol = kAccCol0 + kAccCols;      // 416 (the unused second accumulator)
 constexpr uint32_t kHeadLoCol = kAccCol0 + 2 * kAccCols;  // 448
 constexpr uint32_t kHeadDCol = kHeadLoCol + kAccCols;     // 480
 static_assert(kHeadDCol + kHeadN <= kTmemCols, "tensor memory budget (head)");
@@ -228,6 +231,14 @@ constexpr uint32_t kTkMetaBytes = ((kTkHidOff + kTpHaloCap + 127u) / 128u) * 128
 #ifndef GROOT_GRAB
 #define GROOT_GRAB 8
 #endif
+// Poll intervals (ns) of the waits off the critical path (ptx::mbar_wait_poll);
+// 0 = the previous forms (spinning loader, suspend-hint epilogue).
+#ifndef GROOT_EPI_POLL_NS
+#define GROOT_EPI_POLL_NS 0
+#endif
+#ifndef GROOT_LOAD_POLL_NS
+#define GROOT_LOAD_POLL_NS 0
+#endif
 constexpr uint32_t kTileRing = 32;     // tile ids of the CTA's iterations (dynamic scheduler)
 constexpr uint32_t kEndTile = 0xFFFFFFFFu;
 constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8)
@@ -297,6 +308,7 @@ template <int kMode, bool kKeyed = false>
 __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
                                                                 const __grid_constant__ CUtensorMap tmap_in) {
   constexpr bool kMma = kMode == kModeLayer || kMode == kModeLast;
+  constexpr uint32_t kAccBufs = kMode == kModeLast ? 1u : 2u;  // last layer: see kHeadHiCol
   constexpr bool kXform = kMode == kModeXform;
   static_assert(!kXform || kKeyed, "transform-first mode reads the entry tables");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -411,7 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       auto issue_plan = [&](uint32_t i, uint32_t t, const uint4& m) {
         if (end_published) return;
         const uint32_t ms = i % kTkMetaStages;
-        ptx::mbar_wait(&m_empty[ms], ((i / kTkMetaStages) & 1) ^ 1);
+        if (GROOT_LOAD_POLL_NS) ptx::mbar_wait_poll(&m_empty[ms], ((i / kTkMetaStages) & 1) ^ 1, GROOT_LOAD_POLL_NS);
+        else ptx::mbar_wait(&m_empty[ms], ((i / kTkMetaStages) & 1) ^ 1);
         sTile[i % kTileRing] = t;
         if (t == kEndTile) {
           end_published = true;
@@ -465,7 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if (t == kEndTile) break;
         // rows of iteration it
         const uint32_t rs = it % kTkRowStages;
-        ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
+        if (GROOT_LOAD_POLL_NS) ptx::mbar_wait_poll(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, GROOT_LOAD_POLL_NS);
+        else ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
         tstamp(a.trace, it, 0);
         if (kKeyed) {  // keyed: rows are read from the entry table
           ptx::mbar_arrive(&r_full[rs]);
@@ -538,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     const uint32_t b0s = ptx::smem_addr(sB);
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+      const uint32_t acc = kAccBufs == 2 ? (it & 1) : 0u, aph = kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1);
       ptx::mbar_wait(&full[s], ph);
       if (lane == 0) tstamp(a.trace, it, 8);
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -790,8 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
 #pragma unroll
     for (int k = 0; k < 8; ++k) b8[k] = sBias[8 * j + k];
     for (uint32_t e = 0;; ++e) {
-      const uint32_t acc = e & 1, ph = (e >> 1) & 1;
-      ptx::mbar_wait_sleep(&tfull[acc], ph, 200);
+      const uint32_t acc = kAccBufs == 2 ? (e & 1) : 0u, ph = kAccBufs == 2 ? ((e >> 1) & 1) : (e & 1);
+      if (GROOT_EPI_POLL_NS) ptx::mbar_wait_poll(&tfull[acc], ph, GROOT_EPI_POLL_NS);
+      else ptx::mbar_wait_sleep(&tfull[acc], ph, 200);
       const uint32_t t = sTile[e % kTileRing];
       if (t == kEndTile) break;
       if (warp == 0 && lane == 0) tstamp(a.trace, e, 11);
@@ -823,12 +838,18 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
                           make_float4(o[4], o[5], o[6], o[7]));
           }
       } else {
-        // last layer: relu(acc + b) split into TF32 hi (written back over the
-        // accumulator just read) and lo, then the 32 -> classes head as one
-        // tensor-core MMA group issued by warp 0 once all four quadrants are in
-        // TMEM; each lane takes its row's logits and the first maximum
+        // last layer: the accumulator is freed as soon as it is loaded; relu(acc + b)
+        // split into TF32 hi / lo goes to the head's TMEM columns, then the 32 ->
+        // classes head runs as one tensor-core MMA group issued by warp 0 once all
+        // four quadrants are in; each lane takes its row's logits and the first maximum
         float r[32];
         ptx::tmem_ld_32x32b_x32(tq, r);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+#ifdef GROOT_EXP_LAST_NOHEAD  // timing experiment only (wrong classes): the last layer without any head
+        if (row0 + lane < n) a.cls[row0 + lane] = r[0] > r[1];
+        continue;
+#endif
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) {  // column c holds output feature kcol_feature(c)
@@ -836,16 +857,20 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           hi[c] = __float_as_uint(x) & 0xFFFFE000u;
           lo[c] = __float_as_uint(x - __uint_as_float(hi[c]));
         }
-        ptx::tmem_st_32x32b_x32(tq, hi);
+        ptx::tmem_st_32x32b_x32(tmem_base + kHeadHiCol + ((q * 32u) << 16), hi);
         ptx::tmem_st_32x32b_x32(tmem_base + kHeadLoCol + ((q * 32u) << 16), lo);
         ptx::tmem_wait_st();
+#ifdef GROOT_EXP_LAST_SPLITONLY  // timing experiment only (wrong classes): split + stores, no head MMA
+        if (row0 + lane < n) a.cls[row0 + lane] = hi[0] > lo[1];
+        continue;
+#endif
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, kEpiWarps * 32);
         if (warp == 0) {
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             constexpr uint32_t hdesc = ptx::idesc_tf32<kTileM, kHeadN>();
-            const uint32_t ahi = tmem_base + kAccCol0 + acc * kAccCols, alo = tmem_base + kHeadLoCol;
+            const uint32_t ahi = tmem_base + kHeadHiCol, alo = tmem_base + kHeadLoCol;
             const uint32_t hb = ptx::smem_addr(sHB);
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -858,12 +883,11 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           }
           __syncwarp();
         }
-        ptx::mbar_wait(hdone, e & 1);
+        if (GROOT_EPI_POLL_NS) ptx::mbar_wait_poll(hdone, e & 1, 32);
+        else ptx::mbar_wait(hdone, e & 1);
         ptx::tc_fence_after();
         float lg[8];
         ptx::tmem_ld_32x32b_x8(tmem_base + kHeadDCol + ((q * 32u) << 16), lg);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[acc]);
         const uint32_t row = row0 + lane;
         float best = 0.f;
         uint32_t arg = 0;

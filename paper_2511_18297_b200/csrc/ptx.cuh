@@ -28,6 +28,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
   uint32_t done;
   do {
+#ifdef GROOT_EXP_WAIT_HINT  // experiment: suspend in the try_wait until the phase flips (or the hint elapses)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(GROOT_EXP_WAIT_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -35,7 +44,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+#endif
   } while (!done);
+}
+
+// For waiters off the critical path, polling: one try_wait, then a plain
+// nanosleep of `ns` between polls. Unlike the suspend-hint form (which wakes on
+// any mbarrier traffic of the CTA and re-polls dozens of times per tile), the
+// warp stays off the scheduler, so it does not take issue slots from the
+// producers sharing its sub-partition.
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_addr(bar);
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
 }
 
 // Same, for waiters off the critical path: each try_wait may suspend the
