@@ -241,7 +241,8 @@ def load_traffic(key):
     this exact configuration, if a capture of it is committed; else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(key)
+            v = json.load(f).get(key)
+            return float(v) if isinstance(v, (int, float)) else None
     except Exception:
         return None
 

@@ -2066,7 +2066,7 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   cudaEvent_t ev_half = evh.e, ev_side = evs.e;
   // the last layer in kReadbackParts tile ranges: the classes of the copies a
   // range completes go to the host on the side stream while the next computes
-  constexpr uint32_t kReadbackParts = 4;
+  constexpr uint32_t kReadbackParts = 8;
   uint32_t k1 = 0;
   if (D == 1) {
     layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true, false);

@@ -224,46 +224,43 @@ __global__ void check_edges_kernel(uint64_t ne, const uint2* __restrict__ e, uin
 // ---------------------------------------------------------------------------
 // K3: batch (src/encode.cpp:70-101)
 // ---------------------------------------------------------------------------
+// The replicate kernels read each source element once and write it to every
+// copy (thread per source element, loop over copies): no per-element division.
 __global__ void batch_rp_kernel(uint32_t n, uint32_t copies, uint32_t nnz,
                                 const uint32_t* __restrict__ rp, uint32_t* __restrict__ orp) {
-  const uint64_t total = (uint64_t)n * copies;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = static_cast<uint32_t>(i / n), v = static_cast<uint32_t>(i - (uint64_t)k * n);
-    orp[i] = k * nnz + rp[v];
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t x = rp[v];
+    for (uint32_t k = 0; k < copies; ++k) orp[static_cast<uint64_t>(k) * n + v] = k * nnz + x;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) orp[total] = nnz * copies;
+  if (blockIdx.x == 0 && threadIdx.x == 0) orp[static_cast<uint64_t>(n) * copies] = nnz * copies;
 }
 
 // dst[k*len + i] = src[i] + k*offset, vectorised by 4 when len % 4 == 0.
 __global__ void replicate_offset_kernel(uint64_t len, uint32_t copies, uint32_t offset,
                                         const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
-  const uint64_t total = len * copies;
   if ((len & 3) == 0) {
-    const uint64_t len4 = len >> 2, total4 = total >> 2;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total4;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-      const uint64_t k = i / len4, j = i - k * len4;
-      uint4 v = reinterpret_cast<const uint4*>(src)[j];
-      const uint32_t o = static_cast<uint32_t>(k) * offset;
-      v.x += o; v.y += o; v.z += o; v.w += o;
-      reinterpret_cast<uint4*>(dst)[i] = v;
+    const uint64_t len4 = len >> 2;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < len4; j += (uint64_t)gridDim.x * blockDim.x) {
+      const uint4 v = reinterpret_cast<const uint4*>(src)[j];
+      for (uint32_t k = 0; k < copies; ++k) {
+        const uint32_t o = k * offset;
+        reinterpret_cast<uint4*>(dst)[k * len4 + j] = make_uint4(v.x + o, v.y + o, v.z + o, v.w + o);
+      }
     }
     return;
   }
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = i / len;
-    dst[i] = src[i - k * len] + static_cast<uint32_t>(k) * offset;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < len; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = src[j];
+    for (uint32_t k = 0; k < copies; ++k) dst[k * len + j] = v + k * offset;
   }
 }
 
 __global__ void replicate_bytes_kernel(uint64_t len, uint32_t copies, const uint8_t* __restrict__ src,
                                        uint8_t* __restrict__ dst) {
-  const uint64_t total = len * copies;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = src[i % len];
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < len; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t v = src[j];
+    for (uint32_t k = 0; k < copies; ++k) dst[k * len + j] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -511,18 +508,18 @@ groot_graph* batch(const groot_graph* g, uint32_t copies) {
   o->binary_feat = g->binary_feat;
   try {
     const uint32_t n = g->n;
-    GROOT_LAUNCH(batch_rp_kernel, blocks_for(n64, 256), 256, 0, n, copies,
+    GROOT_LAUNCH(batch_rp_kernel, blocks_for(n, 256), 256, 0, n, copies,
                  static_cast<uint32_t>(g->nnz), g->rp.p, o->rp.p);
     if (g->nnz)
-      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->nnz * copies / 4 + 1, 256), 256, 0, g->nnz,
+      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->nnz / 4 + 1, 256), 256, 0, g->nnz,
                    copies, n, g->col.p, o->col.p);
     if (g->ne)
-      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->ne * copies / 2 + 1, 256), 256, 0, 2 * g->ne,
+      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->ne / 2 + 1, 256), 256, 0, 2 * g->ne,
                    copies, n, g->edges.p, o->edges.p);
-    GROOT_LAUNCH(replicate_offset_kernel, blocks_for(n64 / 4 + 1, 256), 256, 0, static_cast<uint64_t>(n),
+    GROOT_LAUNCH(replicate_offset_kernel, blocks_for(n / 4 + 1, 256), 256, 0, static_cast<uint64_t>(n),
                  copies, 0u, reinterpret_cast<const uint32_t*>(g->feat.p),
                  reinterpret_cast<uint32_t*>(o->feat.p));
-    GROOT_LAUNCH(replicate_bytes_kernel, blocks_for(n64, 256), 256, 0, static_cast<uint64_t>(n), copies,
+    GROOT_LAUNCH(replicate_bytes_kernel, blocks_for(n, 256), 256, 0, static_cast<uint64_t>(n), copies,
                  g->labels.p, o->labels.p);
     stream_sync();
   } catch (...) {
@@ -543,16 +540,18 @@ __global__ void batch_padded_rows_kernel(uint32_t n, uint32_t P, uint32_t copies
                                          const uint32_t* __restrict__ rp, const uint32_t* __restrict__ feat,
                                          const uint8_t* __restrict__ lab, uint32_t* __restrict__ orp,
                                          uint32_t* __restrict__ ofeat, uint8_t* __restrict__ olab) {
-  const uint64_t total = (uint64_t)P * copies;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = static_cast<uint32_t>(i / P), v = static_cast<uint32_t>(i - (uint64_t)k * P);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < P; v += gridDim.x * blockDim.x) {
     const bool real = v < n;
-    orp[i] = k * nnz + (real ? rp[v] : nnz);
-    ofeat[i] = real ? feat[v] : 0u;
-    olab[i] = real ? lab[v] : 0xFFu;
+    const uint32_t r = real ? rp[v] : nnz, f = real ? feat[v] : 0u;
+    const uint8_t l = real ? lab[v] : 0xFFu;
+    for (uint32_t k = 0; k < copies; ++k) {
+      const uint64_t i = static_cast<uint64_t>(k) * P + v;
+      orp[i] = k * nnz + r;
+      ofeat[i] = f;
+      olab[i] = l;
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) orp[total] = nnz * copies;
+  if (blockIdx.x == 0 && threadIdx.x == 0) orp[static_cast<uint64_t>(P) * copies] = nnz * copies;
 }
 
 groot_graph* batch_padded(const groot_graph* g, uint32_t copies, uint32_t P) {
@@ -570,11 +569,11 @@ groot_graph* batch_padded(const groot_graph* g, uint32_t copies, uint32_t P) {
     o->col.alloc(o->nnz);
     o->feat.alloc(4 * n64);
     o->labels.alloc(n64);
-    GROOT_LAUNCH(batch_padded_rows_kernel, blocks_for(n64, 256), 256, 0, g->n, P, copies,
+    GROOT_LAUNCH(batch_padded_rows_kernel, blocks_for(P, 256), 256, 0, g->n, P, copies,
                  static_cast<uint32_t>(g->nnz), g->rp.p, reinterpret_cast<const uint32_t*>(g->feat.p),
                  g->labels.p, o->rp.p, reinterpret_cast<uint32_t*>(o->feat.p), o->labels.p);
     if (g->nnz)
-      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->nnz * copies / 4 + 1, 256), 256, 0, g->nnz, copies, P,
+      GROOT_LAUNCH(replicate_offset_kernel, blocks_for(g->nnz / 4 + 1, 256), 256, 0, g->nnz, copies, P,
                    g->col.p, o->col.p);
   } catch (...) {
     delete o;

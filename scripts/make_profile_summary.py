@@ -14,6 +14,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary as N  # noqa: E402
 
+CONFIG = "csa1024_b16"  # the workload the reports were captured on (bench.py cfg_key)
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
@@ -78,6 +79,33 @@ def main(rnd, out, reports):
             res[k] = {"dram_bytes_per_launch": kernels[k]["dram_bytes_per_launch"]}
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
+    # measured DRAM bytes per launch for bench.py's `traffic` (profiles/ncu_traffic.json),
+    # keyed "<config>:<profiler scope>"; multi-kernel scopes are the sum of their kernels'
+    # mean bytes per launch
+    per = {}
+    for rep in reports:
+        for m in N.raw(rep):
+            name = short_name(m["kernel"])
+            rd, wr = val(m, "dram__bytes_read.sum", True), val(m, "dram__bytes_write.sum", True)
+            per.setdefault(name, []).append((rd or 0) + (wr or 0))
+    mean = {k: sum(v) / len(v) for k, v in per.items()}
+    scopes = {
+        "l0_keys": ["hd_key_kernel", "l0_key_kernel", "dict_finalize_kernel", "l0_xlat_kernel", "l0_ids_kernel",
+                    "l0_halo_ids_kernel", "l0_hd_ids_kernel"],
+        "hd_mean32": ["hd_chunk_kernel", "hd_reduce_kernel"],
+        "spmm_mean32": ["spmm_mean32", "hd_chunk_kernel", "hd_reduce_kernel"],
+    }
+    traffic = {}
+    for k, v in mean.items():
+        if k in ("sage_layer_tc", "sage_layer_tc_last", "sage_layer1_xform", "sage_layer_tc_keyed", "sage_layer0",
+                 "confusion", "tile_plan"):
+            traffic[f"{CONFIG}:{k}"] = v
+    for scope, members in scopes.items():
+        if any(m in mean for m in members):
+            traffic[f"{CONFIG}:{scope}"] = sum(mean.get(m, 0.0) for m in members)
+    tpath = os.path.join(os.path.dirname(out), "ncu_traffic.json")
+    with open(tpath, "w") as f:
+        json.dump(dict(sorted(traffic.items()), _source=res["source"]), f, indent=1)
 
 
 if __name__ == "__main__":
