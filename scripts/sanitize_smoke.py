@@ -1,8 +1,9 @@
-"""Small end-to-end pass over every device kernel family (keyed layer 0 by default;
-GROOT_L0_KEYED=0 for the materialized one), for compute-sanitizer
-(memcheck / racecheck / synccheck / initcheck):
+"""Small runs of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck): keyed and materialized forward (tile kernels incl. the tensor-core
+head), HD rows, classify_aig, partitions + predict, the LP partitioner,
+training, f64 SpMM.
 
-    compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
+usage: compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
 """
 import os
 import sys
@@ -10,23 +11,28 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("GROOT_L0_KEYED_MIN_ROWS", "0")  # key the small graphs too
 from paper_2511_18297_b200 import api  # noqa: E402
 
-os.environ.setdefault("GROOT_L0_KEYED_MIN_ROWS", "0")  # key these small graphs too
-
-prm_model = api.init_model(7)
-for maker, w, b in ((api.gen_csa_multiplier, 16, 3), (api.gen_booth_multiplier, 12, 2), (api.gen_csa_multiplier, 160, 1)):
-    c = maker(w)
-    g = api.batch(api.encode(c.aig, c.labels), b) if b > 1 else api.encode(c.aig, c.labels)
-    lg = api.forward(prm_model, g)
-    pred = api.predict_full(prm_model, g)
-    x = np.random.default_rng(0).uniform(-1, 1, (g.n, 32)).astype(np.float32)
-    api.spmm_mean(g, x)
-    pa = api.partition_topo_chunks(g, 3)
-    parts = api.regrow(g, pa)
-    api.predict(prm_model, g, parts)
-    sub = api.materialize(g, parts, 1)
-    api.forward(prm_model, sub)
-    api.classify_aig(prm_model, c.aig, c.labels, 3)  # tile-aligned batch, periodic plan, split last layer
-    print(maker.__name__, w, b, "n", g.n, "acc", round(pred.accuracy, 4), "finite", bool(np.isfinite(lg).all()))
-print("sanitize smoke done")
+model = api.init_model(7)
+for gen, w, b in ((api.gen_csa_multiplier, 16, 3), (api.gen_booth_multiplier, 12, 2), (api.gen_csa_multiplier, 160, 1)):
+    c = gen(w)
+    g = api.encode(c.aig, c.labels)
+    if b > 1:
+        g = api.batch(g, b)
+    lg = api.forward(model, g)
+    p = api.predict_full(model, g)
+    print(gen.__name__, w, b, "n", g.n, "acc %.4f" % p.accuracy, "finite", bool(np.isfinite(lg).all()), flush=True)
+c = api.gen_csa_multiplier(24)
+print("classify_aig", api.classify_aig(model, c.aig, c.labels, 3).accuracy, flush=True)
+g = api.batch(api.encode(c.aig, c.labels), 2)
+pa = api.partition_multilevel(g, 5)
+parts = api.regrow(g, pa)
+print("lp + predict", api.edge_cut(g, pa), api.predict(model, g, parts).accuracy, flush=True)
+st = api.TrainStats(None, None)
+api.train(api.encode(c.aig, c.labels), epochs=3, learning_rate=1e-2, stats=st)
+print("train", st.loss, flush=True)
+rp = np.array([0, 2, 3, 600], np.uint64)
+ci = np.concatenate([[0, 1, 2], np.arange(597) % 3]).astype(np.uint32)
+print("spmm f64", float(api.spmm_csr_f64(rp, ci, np.ones(600), np.ones((3, 4)), hd_threshold=512).sum()), flush=True)
+print("sanitize smoke done", flush=True)
