@@ -272,12 +272,26 @@ __global__ void topo_kernel(uint32_t n, uint32_t k, uint32_t* __restrict__ part)
     part[v] = static_cast<uint32_t>(((uint64_t)k * (v + 1) - 1) / n);
 }
 
+// Per-part histograms: lanes of a warp holding the same part add once (parts
+// are contiguous runs of nodes / edges, so a warp mostly adds one count instead
+// of 32 atomics on the same few counters). Call with every lane of the warp;
+// key kNoKey adds nothing.
+constexpr uint32_t kNoKey = 0xFFFFFFFFu;
+__device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t key) {
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  if (key != kNoKey && (threadIdx.x & 31u) == static_cast<uint32_t>(__ffs(peers) - 1))
+    atomicAdd(hist + key, static_cast<uint32_t>(__popc(peers)));
+}
+
+// the loops below step whole blocks (blockDim % 32 == 0), so every lane of a
+// warp runs the same trip count and may join the warp-wide histogram adds
 __global__ void check_parts_kernel(uint32_t n, uint32_t k, const uint32_t* __restrict__ part,
                                    uint32_t* __restrict__ hist, uint32_t* bad) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t p = part[v];
-    if (p >= k) atomicMin(bad, v);
-    else atomicAdd(&hist[p], 1u);
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    const uint32_t p = v < n ? part[v] : kNoKey;
+    if (v < n && p >= k) atomicMin(bad, v);
+    hist_add_warp(hist, p < k ? p : kNoKey);
   }
 }
 
@@ -335,11 +349,15 @@ __global__ void cross_emit_kernel(uint32_t n, const uint32_t* __restrict__ rp,
 
 __global__ void split_keys_kernel(uint64_t count, const unsigned long long* __restrict__ keys,
                                   uint32_t* __restrict__ node, uint32_t* __restrict__ hist) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long key = keys[i];
-    node[i] = static_cast<uint32_t>(key);
-    atomicAdd(&hist[key >> 32], 1u);
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < count; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t p = kNoKey;
+    if (i < count) {
+      const unsigned long long key = keys[i];
+      node[i] = static_cast<uint32_t>(key);
+      p = static_cast<uint32_t>(key >> 32);
+    }
+    hist_add_warp(hist, p);
   }
 }
 
@@ -359,20 +377,25 @@ __global__ void edge_emit_kernel(uint64_t ne, const uint2* __restrict__ e,
                                  const uint32_t* __restrict__ part, int with_b,
                                  const uint32_t* __restrict__ off, uint32_t* __restrict__ key,
                                  uint32_t* __restrict__ val, uint32_t* __restrict__ hist) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 uv = e[i];
-    const uint32_t pu = part[uv.x], pv = part[uv.y];
-    uint32_t o = off[i];
-    if (pu == pv) {
-      key[o] = pu; val[o] = static_cast<uint32_t>(i);
-      atomicAdd(&hist[pu], 1u);
-    } else if (with_b) {
-      key[o] = pu; val[o] = static_cast<uint32_t>(i);
-      key[o + 1] = pv; val[o + 1] = static_cast<uint32_t>(i);
-      atomicAdd(&hist[pu], 1u);
-      atomicAdd(&hist[pv], 1u);
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < ne; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t hu = kNoKey, hv = kNoKey;
+    if (i < ne) {
+      const uint2 uv = e[i];
+      const uint32_t pu = part[uv.x], pv = part[uv.y];
+      const uint32_t o = off[i];
+      if (pu == pv) {
+        key[o] = pu; val[o] = static_cast<uint32_t>(i);
+        hu = pu;
+      } else if (with_b) {
+        key[o] = pu; val[o] = static_cast<uint32_t>(i);
+        key[o + 1] = pv; val[o + 1] = static_cast<uint32_t>(i);
+        hu = pu;
+        hv = pv;
+      }
     }
+    hist_add_warp(hist, hu);
+    hist_add_warp(hist, hv);
   }
 }
 

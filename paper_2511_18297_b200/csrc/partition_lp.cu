@@ -147,9 +147,16 @@ __global__ void lp_flag_hd_kernel(uint32_t n, const uint32_t* __restrict__ rp, u
     flag[v] = rp[v + 1] - rp[v] >= kLpHdDeg;
 }
 
+// part weights: lanes holding the same part add once (parts are long runs of
+// nodes); the loop steps whole blocks so every lane joins the warp-wide match
 __global__ void lp_weights_kernel(uint32_t n, const uint32_t* __restrict__ part, uint32_t* __restrict__ w) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    atomicAdd(w + part[v], 1u);
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    const uint32_t p = v < n ? part[v] : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, p);
+    if (v < n && (threadIdx.x & 31u) == static_cast<uint32_t>(__ffs(peers) - 1))
+      atomicAdd(w + p, static_cast<uint32_t>(__popc(peers)));
+  }
 }
 
 // sorted candidates: the first cap - weight(t) of target t's run are accepted;
