@@ -187,6 +187,7 @@ struct groot_graph {
   groot::DevBuf<uint32_t> tp_meta;  // TileMeta per tile (4 x u32)
   groot::DevBuf<uint16_t> tp_lrp;   // kTpLrp u16 per tile
   groot::DevBuf<uint16_t> tp_lcol;  // local neighbour slots
+  groot::DevBuf<unsigned long long> tp_rec;  // row records (tile_plan.cuh), tiles x 128
   groot::DevBuf<uint32_t> tp_halo;  // halo rows per tile
   // Keyed layer 0 (forward.cu, l0_key_kernel): per-row records and entry ids,
   // the record dictionary and the entry rows; l0_mode 0 unknown, 1 keyable, 2 not
@@ -194,6 +195,7 @@ struct groot_graph {
   groot::DevBuf<unsigned long long> l0_key, l0_dict, l0_ctab;  // l0_key: HD rows' records
   groot::DevBuf<uint16_t> l0_slot;                             // LD rows: slot in their CTA's table
   groot::DevBuf<uint8_t> l0_id, l0_idmap, l0_hid, l0_xlat;
+  groot::DevBuf<unsigned long long> l0_krec;  // keyed row records: entry-row offsets (tiles x 128)
   groot::DevBuf<float> l0_table;
   groot::DevBuf<float> l0_xtab;  // keyed layer 1, transform first: Tn | Ts (entry rows . W_neigh / W_self)
   groot::DevBuf<uint32_t> l0_flags;

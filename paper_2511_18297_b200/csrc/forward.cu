@@ -175,6 +175,7 @@ struct LayerArgs {
   const uint16_t* lrp;
   const uint16_t* lcol;
   const uint32_t* halo;
+  const unsigned long long* rec;  // row records (tiles x 128), tile_plan.cuh
   float* spmm_out;       // SpMM mode: n x 32 neighbour means (LD rows)
   unsigned long long* trace;  // diagnostic timeline of CTA 0 (GROOT_TRACE): [64 tiles][16 clock64 stamps]
   uint32_t plan_period;       // > 0: the plan is one copy's (tiles 0..period-1), tile t uses t % period
@@ -227,7 +228,8 @@ constexpr uint32_t kTkLcolOff = kTpLrp * 2u + 16u;
 constexpr uint32_t kTkHaloOff = kTkLcolOff + kTpColCap * 2u;
 constexpr uint32_t kTkKidOff = kTkHaloOff + kTpHaloCap * 4u;  // keyed: entry ids of the tile rows
 constexpr uint32_t kTkHidOff = kTkKidOff + kTpRows;             //        and of the halo rows
-constexpr uint32_t kTkMetaBytes = ((kTkHidOff + kTpHaloCap + 127u) / 128u) * 128u;
+constexpr uint32_t kTkRecOff = kTkHidOff + kTpHaloCap;           // row records (8 B per tile row)
+constexpr uint32_t kTkMetaBytes = ((kTkRecOff + kTpRows * 8u + 127u) / 128u) * 128u;
 #ifndef GROOT_GRAB
 #define GROOT_GRAB 8
 #endif
@@ -271,22 +273,9 @@ struct TkCfg {
 };
 static_assert(kTkRowBytes % 1024 == 0, "row stages keep 1024-B alignment");
 static_assert(kTkLcolOff % 16 == 0 && kTkHaloOff % 16 == 0 && kTkKidOff % 16 == 0 && kTkHidOff % 16 == 0 &&
+                  kTkRecOff % 16 == 0 &&
                   kTpHaloCap % 16 == 0,
               "bulk-copy destinations and keyed halo-id sources must be 16-B aligned");
-
-#ifndef GROOT_XFORM_PAIR
-#define GROOT_XFORM_PAIR 1
-#endif
-#ifndef GROOT_MMA_PAIR
-#define GROOT_MMA_PAIR 1
-#endif
-#ifndef GROOT_MMA_PB
-#define GROOT_MMA_PB 2u
-#endif
-#ifndef GROOT_PAIR_BATCH
-#define GROOT_PAIR_BATCH 4
-#endif
-constexpr uint32_t kPairBatch = GROOT_PAIR_BATCH;  // kModeXform: neighbours per row per batch, both rows together
 
 __device__ __forceinline__ void acc_row(float2 (&m)[4], const float4& x0, const float4& x1) {
   m[0] = ptx::fadd2(m[0], make_float2(x0.x, x0.y));
@@ -350,9 +339,15 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   if (kMode == kModeLast)
     for (uint32_t i = threadIdx.x; i < kHeadBBytes / 16; i += kThreads)
       reinterpret_cast<uint4*>(sHB)[i] = __ldg(reinterpret_cast<const uint4*>(a.hbimg) + i);
+  // the zero row of the row records: entry 255 of the keyed table (entry ids
+  // are < kDictCap = 255), the last halo slot of every row stage otherwise
   if (kKeyed)
     for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
-      reinterpret_cast<uint4*>(sTable)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
+      reinterpret_cast<uint4*>(sTable)[i] =
+          i >= (kTkTableRows - 1) * 8 ? make_uint4(0, 0, 0, 0) : __ldg(reinterpret_cast<const uint4*>(a.ktable) + i);
+  else
+    for (uint32_t i = threadIdx.x; i < kTkRowStages * 8; i += kThreads)
+      reinterpret_cast<uint4*>(sRows + (i >> 3) * kTkRowBytes + kTpZeroSlot * 128u)[i & 7] = make_uint4(0, 0, 0, 0);
   if (kXform)
     for (uint32_t i = threadIdx.x; i < kTkTableRows * 8; i += kThreads)
       reinterpret_cast<uint4*>(sTable + kTkTableRows * 128)[i] = __ldg(reinterpret_cast<const uint4*>(a.ktable_self) + i);
@@ -437,15 +432,21 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const bool slow = (m.w & kTpSlow) != 0;
         const uint32_t hpad = (slow || kKeyed) ? 0u : (m.w + 3u) & ~3u;  // keyed: halo ids instead of rows
         const uint32_t kpad = kKeyed ? (slow ? 0u : (m.w + 15u) & ~15u) : 0u;
-        ptx::mbar_arrive_expect_tx(&m_full[ms], kTpLrp * 2u + m.z * 2u + hpad * 4u + (kKeyed ? kTpRows + kpad : 0u));
+        // row offsets and slot list only for tiles with rows of degree > 4 (m.z > 0)
+        ptx::mbar_arrive_expect_tx(&m_full[ms], (m.z ? kTpLrp * 2u + m.z * 2u : 0u) + hpad * 4u + (kKeyed ? kTpRows + kpad : 0u) +
+                                                    (slow ? 0u : kTpRows * 8u));
         if (kKeyed) {
           ptx::bulk_load(sp + kTkKidOff, a.keys + static_cast<size_t>(t) * kTpRows, kTpRows, &m_full[ms]);
           if (kpad) ptx::bulk_load(sp + kTkHidOff, a.hids + static_cast<size_t>(t) * kTpHaloCap, kpad, &m_full[ms]);
         }
         const uint32_t pt = a.plan_period ? t % a.plan_period : t;
-        ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(pt) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
-        if (m.z) ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
+        if (m.z) {
+          ptx::bulk_load(sp + kTkLrpOff, a.lrp + static_cast<size_t>(pt) * kTpLrp, kTpLrp * 2u, &m_full[ms]);
+          ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
+        }
         if (hpad) ptx::bulk_load(sp + kTkHaloOff, a.halo + m.y, hpad * 4u, &m_full[ms]);
+        if (!slow)  // (keyed: entry-row records by plan tile, l0_halo_ids_kernel)
+          ptx::bulk_load(sp + kTkRecOff, a.rec + static_cast<size_t>(pt) * kTpRows, kTpRows * 8u, &m_full[ms]);
       };
       uint32_t rows_tile[kTkMetaLead];  // tiles of iterations it .. it + kTkMetaLead - 1
       for (int i = 0; i < kTkMetaLead; ++i) {
@@ -598,6 +599,18 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     const float* hin_j = a.hin + 8 * j;
     unsigned long long wt0 = 0, wt1 = 0, wt2 = 0, wt3 = 0;
     unsigned long long acc_rows = 0, acc_gather = 0, acc_wait = 0, acc_store = 0;
+    // The A stage of tile i is handed to the MMA (tcgen05.wait::st, fence,
+    // arrive) after the gather of tile i + 1: the TMEM stores complete behind
+    // the next tile's shared-memory reads instead of stalling the warp.
+    uint32_t pend = kStages;  // stage with stores in flight (kStages: none)
+    auto hand_over = [&]() {
+      if (kMma && pend < kStages) {
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&full[pend]);
+        pend = kStages;
+      }
+    };
     for (uint32_t it = 0;; ++it) {
       const uint32_t rs = it % kTkRowStages, ms = it % kTkMetaStages;
       unsigned long long* tr = (warp == kEpiWarps && lane == 0) ? a.trace : nullptr;
@@ -608,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
       const uint32_t t = sTile[it % kTileRing];
       if (t == kEndTile) {  // hand the MMA an empty stage so it sees the end too
+        hand_over();
         if (kMma) {
           const uint32_t s = it % kStages;
           ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
@@ -635,6 +649,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       float2 m[2][4];
       uint32_t d[2];
       bool hd[2];
+      float inv[2];
+      float4 hs[2][2], mm[2][2];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -642,61 +658,54 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       if (!slow) {
         const uint16_t* lr = reinterpret_cast<const uint16_t*>(sp + kTkLrpOff);
         const uint16_t* lc = reinterpret_cast<const uint16_t*>(sp + kTkLcolOff);
-        uint32_t lo[2];
+        // one record per row: its first four neighbour slots as byte offsets
+        // (unused ones -> the zero row), so every row's neighbour reads are
+        // issued together, branch-free, right after one shared-memory load
+        uint2 rr[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t w0 = lr[li + 8 * h], w1 = lr[li + 8 * h + 1];
-          lo[h] = w0 & 0x7FFFu;
-          hd[h] = (w0 & kTpHdBit) != 0;
-          d[h] = hd[h] ? 0u : (w1 & 0x7FFFu) - lo[h];  // HD rows: mean from the HD kernel
+          rr[h] = *reinterpret_cast<const uint2*>(sp + kTkRecOff + (li + 8 * h) * 8u);
+          hd[h] = (rr[h].x & kTpRecHd) != 0;
+          d[h] = tp_rec_degree(rr[h].x);
+          inv[h] = sInv[d[h]];
         }
-        if ((kXform && GROOT_XFORM_PAIR) || (kMma && GROOT_MMA_PAIR)) {
-          // both rows' neighbour batches in flight at once (kXform holds no TMEM
-          // operands, so it affords kPairBatch = 4 neighbours per row)
-          constexpr uint32_t kPB = kXform ? kPairBatch : GROOT_MMA_PB;
-          const uint32_t dmax = d[0] > d[1] ? d[0] : d[1];
-          for (uint32_t k0 = 0; k0 < dmax; k0 += kPB) {
-            uint32_t loc[2][kPB];
+        if (kMma || kXform) {
+          const uint8_t* sself = kXform ? sTable + kTkTableRows * 128 : sTable;  // Ts, or the entry rows
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (uint32_t u = 0; u < kPB; ++u) loc[h][u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
-            float4 x[2][kPB][2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (uint32_t u = 0; u < kPB; ++u)
-                if (k0 + u < d[h]) {
-                  const uint8_t* rowp = rbase + loc[h][u] * 128u;
-                  x[h][u][0] = *reinterpret_cast<const float4*>(rowp + off0);
-                  x[h][u][1] = *reinterpret_cast<const float4*>(rowp + off1);
-                }
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (uint32_t u = 0; u < kPB; ++u)
-                if (k0 + u < d[h]) acc_row(m[h], x[h][u][0], x[h][u][1]);
+          for (int h = 0; h < 2; ++h) {  // natural half order (no parity swap; rows li, li + 1 share banks: 2-way)
+            const uint8_t* rowp = kKeyed ? sself + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
+            hs[h][0] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j);
+            hs[h][1] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j + 16u);
           }
-        } else
-        // rows one after the other (4 neighbour rows in flight per row keeps
-        // the producers inside 128 registers)
+        }
+        {
+          // 16-B shared loads (ld.shared.v4: a float4 dereference of these
+          // computed addresses compiles to pairs of 8-B loads)
+          const uint32_t rb0 = ptx::smem_addr(rbase) + off0, rb1 = ptx::smem_addr(rbase) + off1;
+          float4 x[2][kTpRecSlots][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (uint32_t u = 0; u < kTpRecSlots; ++u) {
+              const uint32_t w = u < 2 ? rr[h].x : rr[h].y;
+              const uint32_t o = ((u & 1) ? (w >> 16) : w) & kTpRecOffMask;
+              x[h][u][0] = ptx::lds_f4(rb0 + o);
+              x[h][u][1] = ptx::lds_f4(rb1 + o);
+            }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (uint32_t u = 0; u < kTpRecSlots; ++u) acc_row(m[h], x[h][u][0], x[h][u][1]);
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          for (uint32_t k0 = 0; k0 < d[h]; k0 += 4) {
-            uint32_t loc[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) loc[u] = (k0 + u < d[h]) ? lc[lo[h] + k0 + u] : 0u;
-            float4 x[4][2];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (k0 + u < d[h]) {
-                const uint8_t* rowp = rbase + loc[u] * 128u;
-                x[u][0] = *reinterpret_cast<const float4*>(rowp + off0);
-                x[u][1] = *reinterpret_cast<const float4*>(rowp + off1);
-              }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (k0 + u < d[h]) acc_row(m[h], x[u][0], x[u][1]);
+          if (rr[h].x & kTpRecLong) {  // degree > 4 (rare in an AIG): the rest from the slot list
+            const uint32_t lo = lr[li + 8 * h] & 0x7FFFu;
+            const uint32_t rb = ptx::smem_addr(rbase);
+            for (uint32_t k = kTpRecSlots; k < d[h]; ++k) {
+              const uint32_t o = rb + lc[lo + k] * 128u;
+              acc_row(m[h], ptx::lds_f4(o + off0), ptx::lds_f4(o + off1));
+            }
           }
 #pragma unroll
         for (int h = 0; h < 2; ++h) swap_halves(m[h], gp != 0);
@@ -709,6 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           const uint32_t dd = r < n ? __ldg(a.rp + r + 1) - b[h] : 0u;
           hd[h] = dd >= thr;
           d[h] = hd[h] ? 0u : dd;
+          inv[h] = sInv[d[h]];
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -721,16 +731,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
             acc_row(m[h], x0, x1);
           }
       }
-      float4 hs[2][2], mm[2][2];
-      if (kMma || kXform) {
-        const uint8_t* sself = kXform ? sTable + kTkTableRows * 128 : sTable;  // Ts, or the entry rows
+      if ((kMma || kXform) && slow) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+          const uint8_t* sself = kXform ? sTable + kTkTableRows * 128 : sTable;  // Ts, or the entry rows
           const uint8_t* rowp = kKeyed ? sself + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
-          const float4 f0 = *reinterpret_cast<const float4*>(rowp + off0);
-          const float4 f1 = *reinterpret_cast<const float4*>(rowp + off1);
-          hs[h][0] = gp ? f1 : f0;
-          hs[h][1] = gp ? f0 : f1;
+          hs[h][0] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j);
+          hs[h][1] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j + 16u);
         }
       }
       tstamp(tr, it, 5);
@@ -738,6 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       if (kTraceOn) wt2 = clock64();
       ptx::mbar_arrive(&r_empty[rs]);
       ptx::mbar_arrive(&m_empty[ms]);
+      hand_over();  // the previous tile's A stage
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t r = row0 + li + 8 * h;
@@ -748,8 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
             mm[h][1] = ptx::ldg_f4(src + 4);
           }
         } else {
-          const float inv = sInv[d[h]];
-          const float2 iv = make_float2(inv, inv);
+          const float2 iv = make_float2(inv[h], inv[h]);
 #pragma unroll
           for (int q = 0; q < 4; ++q) m[h][q] = ptx::fmul2(m[h][q], iv);
           mm[h][0] = make_float4(m[h][0].x, m[h][0].y, m[h][1].x, m[h][1].y);
@@ -779,9 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
         tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
         tmem_store_split(ta + 32, mm);  // columns 32..63 (hi), 96..127 (lo): neighbour mean
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&full[s]);
+        pend = s;                       // handed over after the next tile's gather
         tstamp(tr, it, 7);
         if (kTraceOn) {
           const unsigned long long wt4 = clock64();
@@ -1451,9 +1456,13 @@ __global__ void l0_hd_ids_kernel(uint32_t count, const uint32_t* __restrict__ hd
 __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const uint4* __restrict__ tmeta,
                                                           const uint32_t* __restrict__ halo, uint32_t period,
                                                           uint32_t period_rows, const uint8_t* __restrict__ ids,
-                                                          const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids) {
+                                                          const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids,
+                                                          const unsigned long long* __restrict__ rec,
+                                                          unsigned long long* __restrict__ krec) {
   if (flags[0]) return;
   constexpr uint32_t kPer = kTpHaloCap / 32;
+  __shared__ uint8_t sh_all[8][kTpHaloCap];  // the warp's halo ids, for the records
+  uint8_t* sh = sh_all[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
@@ -1469,7 +1478,31 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     for (uint32_t u = 0; u < kPer; ++u) iv[u] = lane + 32 * u < m.w ? __ldg(ids + shift + hv[u]) : 0u;
 #pragma unroll
     for (uint32_t u = 0; u < kPer; ++u)
-      if (lane + 32 * u < m.w) hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
+      if (lane + 32 * u < m.w) {
+        hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
+        sh[lane + 32 * u] = static_cast<uint8_t>(iv[u]);
+      }
+    __syncwarp();
+    // keyed row records of tile t: each slot byte offset -> its entry row's
+    // byte offset in the table (zero slot -> entry kTkTableRows - 1, kept zero).
+    // A periodic plan is a batch of identical copies, whose rows have the same
+    // records and so the same entry ids in every copy: the first period's
+    // tiles are enough (the kernels index them by plan tile).
+    if (period && t >= period) continue;
+    const uint8_t* tid = ids + static_cast<size_t>(t) * kTpRows;
+#pragma unroll
+    for (uint32_t i = 0; i < kTpRows / 32; ++i) {
+      const unsigned long long r = __ldg(rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
+      unsigned long long o = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < kTpRecSlots; ++k) {
+        const uint32_t f = static_cast<uint32_t>(r >> (16 * k)) & 0xFFFFu, sl = f >> 7;
+        const uint32_t id = sl < kTpRows ? __ldg(tid + sl) : (sl == kTpZeroSlot ? kTkTableRows - 1u : sh[sl - kTpRows]);
+        o |= static_cast<unsigned long long>((id << 7) | (f & 0x7Fu)) << (16 * k);
+      }
+      krec[static_cast<size_t>(t) * kTpRows + 32 * i + lane] = o;
+    }
+    __syncwarp();
   }
 }
 
@@ -1698,6 +1731,7 @@ static LayerArgs plan_args(groot_graph* g, const float* hin, const HdInfo& hd) {
   a.lrp = g->tp_lrp.p;
   a.lcol = g->tp_lcol.p;
   a.halo = g->tp_halo.p;
+  a.rec = g->tp_rec.p;
   a.plan_period = g->tp_period;
   if (!g->tile_ctr.p) g->tile_ctr.alloc(1);
   static const bool dyn = env_u32("GROOT_DYNAMIC_TILES", 1) != 0;
@@ -1867,6 +1901,7 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   if (g->l0_slot.n < n) g->l0_slot.alloc(n);
   if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
   if (g->l0_hid.n < static_cast<size_t>(ntiles) * kTpHaloCap) g->l0_hid.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
+  if (g->l0_krec.n < static_cast<size_t>(ntiles) * kTpRows) g->l0_krec.alloc(static_cast<size_t>(ntiles) * kTpRows);
   if (g->l0_ctab.n < static_cast<size_t>(key_ctas) * kDictLocal) {
     g->l0_ctab.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
     g->l0_xlat.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
@@ -1900,7 +1935,7 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
                    g->l0_dict.p, g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
     GROOT_LAUNCH(l0_halo_ids_kernel, blocks_for(ntiles * 32ull, 256, sms * 16), 256, 0,
                  ntiles, reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_halo.p, g->tp_period, g->tp_period_rows,
-                 g->l0_id.p, g->l0_flags.p, g->l0_hid.p);
+                 g->l0_id.p, g->l0_flags.p, g->l0_hid.p, g->tp_rec.p, g->l0_krec.p);
   }
   if (g->l0_mode == 0) {
     uint32_t fl[2] = {0, 0};
@@ -1957,6 +1992,7 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   if (keyed_in) {
     a.keys = g->l0_id.p;
     a.hids = g->l0_hid.p;
+    a.rec = g->l0_krec.p;  // keyed records (entry-row offsets), by plan tile
     a.ktable = xform ? g->l0_xtab.p : g->l0_table.p;
     a.ktable_self = g->l0_xtab.p + kTkTableRows * kF;
   }
@@ -2203,6 +2239,7 @@ void graph_release_context(groot_graph* g) {
   g->tp_meta.release();
   g->tp_lrp.release();
   g->tp_lcol.release();
+  g->tp_rec.release();
   g->tp_halo.release();
   g->hdp_valid = false;
   g->hdp_nunits = 0;

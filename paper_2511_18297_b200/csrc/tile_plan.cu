@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
                                                                   const uint32_t* __restrict__ col, uint32_t thr,
                                                                   uint32_t halo_cap, TileMeta* meta, uint16_t* lrp,
                                                                   uint16_t* lcol, uint32_t* halo,
-                                                                  uint32_t* slow_count) {
+                                                                  unsigned long long* rec, uint32_t* slow_count) {
   __shared__ uint32_t hk_all[kTpWarps][kHashSlots];    // set of out-of-tile columns
   __shared__ uint16_t hv_all[kTpWarps][kHashSlots];    // their rank in the sorted halo list
   __shared__ uint32_t uniq_all[kTpWarps][256];          // sorted halo list (padded to a power of 2)
@@ -138,8 +138,14 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
         }
       }
     }
+    // the slot list is staged only for tiles with a row of degree > kTpRecSlots
+    // (the records hold every other row's slots)
+    bool lng = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lng |= !hd[i] && d[i] > kTpRecSlots;
+    lng = __any_sync(0xffffffffu, lng);
     if (lane == 0) {
-      meta[t] = TileMeta{loff, t * kTpHaloCap, slow ? 0u : lcnt, slow ? kTpSlow : H};
+      meta[t] = TileMeta{loff, t * kTpHaloCap, (slow || !lng) ? 0u : lcnt, slow ? kTpSlow : H};
       if (slow) atomicAdd(slow_count, 1u);
     }
     if (!slow) {
@@ -148,6 +154,20 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
       for (int i = 0; i < 4; ++i) lr[32 * i + lane] = static_cast<uint16_t>((b[i] - loff) | (hd[i] ? kTpHdBit : 0u));
       if (lane < kTpLrp - kTpRows) lr[kTpRows + lane] = static_cast<uint16_t>(end - loff);
       for (uint32_t i = lane; i < ((H + 3u) & ~3u); i += 32) halo[t * kTpHaloCap + i] = uniq[min(i, H - 1)];
+      // row records: the first kTpRecSlots slots of each row (this lane wrote them
+      // above), unused fields -> the zero slot
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t f[kTpRecSlots];
+#pragma unroll
+        for (uint32_t k = 0; k < kTpRecSlots; ++k)
+          f[k] = (!hd[i] && k < d[i] ? static_cast<uint32_t>(lcol[b[i] + k]) : kTpZeroSlot) << 7;
+        const uint32_t dl = hd[i] ? 0u : d[i];  // LD degree < thr <= 256
+        f[0] |= dl & 0x7Fu;
+        f[1] |= (hd[i] ? 1u : 0u) | (dl > kTpRecSlots ? 2u : 0u) | ((dl >> 7) << 2);
+        rec[static_cast<size_t>(t) * kTpRows + 32 * i + lane] =
+            static_cast<unsigned long long>(f[0] | (f[1] << 16)) | (static_cast<unsigned long long>(f[2] | (f[3] << 16)) << 32);
+      }
     }
     __syncwarp();
   }
@@ -158,8 +178,9 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
 uint32_t tile_halo_cap() {
   static uint32_t cap = [] {
     const char* e = std::getenv("GROOT_TP_HALO_CAP");  // test knob: force slow tiles
-    const uint32_t v = e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : kTpHaloCap;
-    return v > kTpHaloCap ? kTpHaloCap : v;
+    // (the last halo slot is the zero row of the row records: kTpZeroSlot)
+    const uint32_t v = e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : kTpHaloCap - 1;
+    return v > kTpHaloCap - 1 ? kTpHaloCap - 1 : v;
   }();
   return cap;
 }
@@ -175,11 +196,12 @@ void build_tile_plan(groot_graph* g, uint32_t thr) {
   g->tp_lrp.alloc(static_cast<size_t>(ntiles) * kTpLrp);
   g->tp_lcol.alloc(g->nnz + 16ull);
   g->tp_halo.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
+  g->tp_rec.alloc(static_cast<size_t>(ntiles) * kTpRows);
   DevBuf<uint32_t> slow(1);
   slow.zero();
   const unsigned grid = std::min<uint32_t>((ntiles + kTpWarps - 1) / kTpWarps, static_cast<uint32_t>(num_sms()) * 16u);
   GROOT_LAUNCH(tile_plan_kernel, grid, kTpWarps * 32, 0, n, g->rp.p, g->col.p, thr, cap,
-               reinterpret_cast<TileMeta*>(g->tp_meta.p), g->tp_lrp.p, g->tp_lcol.p, g->tp_halo.p, slow.p);
+               reinterpret_cast<TileMeta*>(g->tp_meta.p), g->tp_lrp.p, g->tp_lcol.p, g->tp_halo.p, g->tp_rec.p, slow.p);
   slow.download(&g->tp_slow, 1);
   stream_sync();
   g->tp_threshold = thr;
@@ -219,6 +241,7 @@ bool replicate_forward_plan(groot_graph* src, groot_graph* dst, uint32_t copies,
   dst->tp_lrp = std::move(src->tp_lrp);
   dst->tp_lcol = std::move(src->tp_lcol);
   dst->tp_halo = std::move(src->tp_halo);
+  dst->tp_rec = std::move(src->tp_rec);
   dst->tp_threshold = src->tp_threshold;
   dst->tp_halo_cap = src->tp_halo_cap;
   dst->tp_slow = src->tp_slow * copies;

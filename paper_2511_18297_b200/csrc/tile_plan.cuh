@@ -31,14 +31,34 @@ constexpr uint32_t kTpColCap = 1024;   // LD nonzeros staged per tile
 constexpr uint32_t kTpLrp = 136;       // u16 row offsets per tile (129 used; 272 B, 16-B multiple)
 constexpr uint32_t kTpSlow = 1u << 31; // meta.w flag: gather from the global CSR
 constexpr uint32_t kTpHdBit = 0x8000u; // lrp entry flag: row is HD (mean computed by the HD kernel)
+// The last halo slot is never a halo row (at most kTpHaloCap - 1 are staged):
+// the kernels keep it zero, and row records point their unused neighbour
+// slots at it, so the gather of a row is branch-free (adding +0 to a sum that
+// starts at +0 changes nothing).
+constexpr uint32_t kTpZeroSlot = kTpRows + kTpHaloCap - 1;
+// Row record (u64 per tile row, 8 B): the row's first four local neighbour
+// slots inline, so the producers need one shared-memory load per row before
+// its neighbour rows instead of the chain row offsets -> slot list -> rows.
+// u16 field k (k = 0..3) = slot_k * 128 (the row's byte offset in the staged
+// rows; kTpZeroSlot past the degree) | low 7 bits:
+//   field 0: LD degree bits 0..6 (0 for HD rows)
+//   field 1: bit 0 HD row (mean from the HD kernel), bit 1 degree > 4 (slots
+//            4.. come from the lcol segment at the lrp offset), bit 2 degree
+//            bit 7 (LD degree < threshold <= 256)
+constexpr uint32_t kTpRecSlots = 4;
+constexpr uint32_t kTpRecOffMask = 0xFF80u;
+constexpr uint32_t kTpRecHd = 1u << 16, kTpRecLong = 1u << 17;  // in the low u32 of the record
+constexpr uint32_t tp_rec_degree(uint32_t lo32) { return (lo32 & 0x7Fu) | ((lo32 >> 11) & 0x80u); }
+static_assert((kTpZeroSlot << 7) <= 0xFFFFu, "slot byte offsets fit a u16 field");
 
-// Layout: lcol is aligned with col_idx (entry e = local slot of nonzero e;
+// Layout: rec holds one record per tile row (tiles x kTpRows); lcol is aligned with col_idx (entry e = local slot of nonzero e;
 // entries of HD rows are not written), each tile's halo list sits in a fixed
 // kTpHaloCap-entry slot, lrp holds the rows' offsets into the tile's staged
 // lcol segment [lcol_off, lcol_off + lcol_cnt) | kTpHdBit.
 // Per-tile record (16 B): lcol segment start (entries, multiple of 8), halo
 // list offset (= tile * kTpHaloCap), staged lcol entries (multiple of 8; 0 if
-// slow), halo row count | kTpSlow.
+// slow or if no row of the tile has more than kTpRecSlots neighbours: the row
+// records then hold every slot), halo row count | kTpSlow.
 struct TileMeta {
   uint32_t lcol_off, halo_off, lcol_cnt, halo;
 };
