@@ -1461,7 +1461,7 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
                                                           unsigned long long* __restrict__ krec) {
   if (flags[0]) return;
   constexpr uint32_t kPer = kTpHaloCap / 32;
-  __shared__ uint8_t sh_all[8][kTpHaloCap];  // the warp's halo ids, for the records
+  __shared__ uint8_t sh_all[8][kTpRows + kTpHaloCap];  // the warp's tile ids | halo ids, for the records
   uint8_t* sh = sh_all[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -1470,6 +1470,14 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     const uint32_t shift = period ? (t / period) * period_rows : 0u;
     const uint4 m = __ldg(tmeta + pt);
     if (m.w & kTpSlow) continue;
+    const bool recs = !(period && t >= period);
+    // records and tile ids first (independent of the halo lookups)
+    unsigned long long r[kTpRows / 32];
+    if (recs) {
+#pragma unroll
+      for (uint32_t i = 0; i < kTpRows / 32; ++i) r[i] = __ldg(rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
+      reinterpret_cast<uint32_t*>(sh)[lane] = __ldg(reinterpret_cast<const uint32_t*>(ids + static_cast<size_t>(t) * kTpRows) + lane);
+    }
     uint32_t hv[kPer];
 #pragma unroll
     for (uint32_t u = 0; u < kPer; ++u) hv[u] = lane + 32 * u < m.w ? __ldg(halo + m.y + lane + 32 * u) : 0u;
@@ -1480,24 +1488,22 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     for (uint32_t u = 0; u < kPer; ++u)
       if (lane + 32 * u < m.w) {
         hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
-        sh[lane + 32 * u] = static_cast<uint8_t>(iv[u]);
+        sh[kTpRows + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
       }
-    __syncwarp();
     // keyed row records of tile t: each slot byte offset -> its entry row's
     // byte offset in the table (zero slot -> entry kTkTableRows - 1, kept zero).
     // A periodic plan is a batch of identical copies, whose rows have the same
     // records and so the same entry ids in every copy: the first period's
     // tiles are enough (the kernels index them by plan tile).
-    if (period && t >= period) continue;
-    const uint8_t* tid = ids + static_cast<size_t>(t) * kTpRows;
+    if (!recs) continue;
+    __syncwarp();
 #pragma unroll
     for (uint32_t i = 0; i < kTpRows / 32; ++i) {
-      const unsigned long long r = __ldg(rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
       unsigned long long o = 0;
 #pragma unroll
       for (uint32_t k = 0; k < kTpRecSlots; ++k) {
-        const uint32_t f = static_cast<uint32_t>(r >> (16 * k)) & 0xFFFFu, sl = f >> 7;
-        const uint32_t id = sl < kTpRows ? __ldg(tid + sl) : (sl == kTpZeroSlot ? kTkTableRows - 1u : sh[sl - kTpRows]);
+        const uint32_t f = static_cast<uint32_t>(r[i] >> (16 * k)) & 0xFFFFu, sl = f >> 7;
+        const uint32_t id = sl == kTpZeroSlot ? kTkTableRows - 1u : sh[sl];
         o |= static_cast<unsigned long long>((id << 7) | (f & 0x7Fu)) << (16 * k);
       }
       krec[static_cast<size_t>(t) * kTpRows + 32 * i + lane] = o;
