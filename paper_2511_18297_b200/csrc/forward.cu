@@ -478,20 +478,17 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         rows_tile[kTkMetaLead - 1] = tl;
         if (t == kEndTile) break;
         // rows of iteration it
+        if (kKeyed) continue;  // keyed: no rows (the producers read the entry table)
         const uint32_t rs = it % kTkRowStages;
         if (GROOT_LOAD_POLL_NS) ptx::mbar_wait_poll(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, GROOT_LOAD_POLL_NS);
         else ptx::mbar_wait(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1);
         tstamp(a.trace, it, 0);
-        if (kKeyed) {  // keyed: rows are read from the entry table
-          ptx::mbar_arrive(&r_full[rs]);
-          continue;
-        }
         ptx::mbar_arrive_expect_tx(&r_full[rs], kTpRows * 128u);
         ptx::tma_load_2d(&tmap_in, sRows + rs * kTkRowBytes, &r_full[rs], 0, static_cast<int32_t>(t * kTileM));
       }
     }
     __syncwarp();
-  } else if (copier >= 0) {
+  } else if (copier >= 0 && !kKeyed) {  // (keyed layers stage no rows: the copiers idle)
     // ===== halo copiers: 16-B cp.async per lane, 8 lanes per row =====
     const uint32_t sRows_s = ptx::smem_addr(sRows);
     const uint32_t gl = static_cast<uint32_t>(copier) * 32u + lane;
@@ -505,25 +502,6 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_wait_sleep(&r_empty[rs], ((it / kTkRowStages) & 1) ^ 1, 100);
       const uint32_t hc = sMeta[ms].w;
       if (gl == 0) tstamp(a.trace, it, 1);
-      if (kKeyed) {
-        // keyed layer 1: no rows to copy (producers read the entry table);
-        // rewrite the tile's local slots into entry ids in place, so the
-        // producers' gather has the plain path's dependency chain
-        uint16_t* lc = reinterpret_cast<uint16_t*>(sPlan + ms * kTkMetaBytes + kTkLcolOff);
-        const uint8_t* kid = sPlan + ms * kTkMetaBytes + kTkKidOff;
-        const uint32_t cnt = sMeta[ms].z;
-#pragma unroll 4
-        // (the window also spans HD rows' and alignment entries, never read: unset)
-        for (uint32_t k = gl; k < cnt; k += 32 * kCopiers) {
-          const uint32_t v = lc[k];
-          lc[k] = v < kTpRows + kTpHaloCap ? kid[v] : 0u;
-        }
-        // the stage is refilled by bulk copies (async proxy) once the producers
-        // release it: order these generic-proxy writes before that
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&r_full[rs]);
-        continue;
-      }
       if (!(hc & kTpSlow)) {
         const uint32_t shift = a.plan_period ? (t / a.plan_period) * a.period_rows : 0u;
         const float* hin_c = a.hin + static_cast<size_t>(shift) * kF + 4 * c;
@@ -637,13 +615,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         break;
       }
       const uint32_t row0 = t * kTileM;
-      ptx::mbar_wait(&r_full[rs], (it / kTkRowStages) & 1);
+      if (!kKeyed) ptx::mbar_wait(&r_full[rs], (it / kTkRowStages) & 1);
       tstamp(tr, it, 4);
       if (kTraceOn) wt1 = clock64();
       const uint8_t* st = sRows + rs * kTkRowBytes;
       const uint8_t* sp = sPlan + ms * kTkMetaBytes;
-      // neighbour rows: staged rows, or (keyed) entry rows: the copiers have
-      // rewritten the local slots into entry ids
+      // neighbour rows: staged rows, or (keyed) entry rows: the keyed row
+      // records hold entry-row offsets (l0_halo_ids_kernel)
       const uint8_t* rbase = kKeyed ? sTable : st;
       const bool slow = (sMeta[ms].w & kTpSlow) != 0;
       float2 m[2][4];
@@ -703,7 +681,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
             const uint32_t lo = lr[li + 8 * h] & 0x7FFFu;
             const uint32_t rb = ptx::smem_addr(rbase);
             for (uint32_t k = kTpRecSlots; k < d[h]; ++k) {
-              const uint32_t o = rb + lc[lo + k] * 128u;
+              // (keyed: the slot's entry id, staged with the plan)
+              const uint32_t o = rb + (kKeyed ? static_cast<uint32_t>(sp[kTkKidOff + lc[lo + k]]) : lc[lo + k]) * 128u;
               acc_row(m[h], ptx::lds_f4(o + off0), ptx::lds_f4(o + off1));
             }
           }
@@ -743,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       tstamp(tr, it, 5);
       tstamp(tr7, it, 14);
       if (kTraceOn) wt2 = clock64();
-      ptx::mbar_arrive(&r_empty[rs]);
+      if (!kKeyed) ptx::mbar_arrive(&r_empty[rs]);
       ptx::mbar_arrive(&m_empty[ms]);
       hand_over();  // the previous tile's A stage
 #pragma unroll
