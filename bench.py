@@ -132,8 +132,16 @@ class ClockSampler:
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[3]))
+            except ValueError:
+                pass
+        capped = sum(1 for r in self.rows if r[8].lower() == "active")
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_median": statistics.median(pw) if pw else None, "power_cap_samples": capped}
 
 
 # ---------------------------------------------------------------------------
@@ -414,7 +422,10 @@ def run_ours(args):
         for _ in range(2):
             step()
         L.groot_profile_enable(1)
+        sampler_mat = ClockSampler(local).start()
+        time.sleep(0.3)
         ms_mat = timed(step, args.steps)
+        clocks_mat = sampler_mat.stop()
         kmat = read_profile()
         L.groot_profile_enable(0)
         del os.environ["GROOT_L0_KEYED"]
@@ -423,7 +434,7 @@ def run_ours(args):
         side["materialized_layer0"] = {
             "ms_per_step": ms_mat, "value": E_all / (ms_mat * 1e-3), "unit": UNIT,
             "forward_frac": survey_bytes / ms_mat / 1e6 / peak, "kernel_rooflines": mat_roofs,
-            "dominant": mat_dom, "note": "same forward with GROOT_L0_KEYED=0 (layer-0 rows materialized: the general "
+            "dominant": mat_dom, "clocks": clocks_mat, "note": "same forward with GROOT_L0_KEYED=0 (layer-0 rows materialized: the general "
                                          "path for graphs without few distinct layer-0 records)"}
         # make_context rebuilt every step (the reference's predict_full redoes it per call)
         ms_ctx = timed(step, max(3, min(args.steps, 5)), pre=lambda: L.groot_graph_release_context(g.handle))

@@ -17,7 +17,8 @@ for v in "$@"; do
 import json,sys
 try:
     d=json.load(open('gpurun_out/ab_$v.json')); k=d['kernels']
-    print('$v', round(d['ms_per_step'],2), 'e2e', round(d['e2e']['ms_per_step'],2), {x:round(v['ms_per_launch'],3) for x,v in k.items() if 'sage' in x or 'l0' in x})
+    c=d.get('clocks',{})
+    print('$v', round(d['ms_per_step'],2), 'e2e', round(d['e2e']['ms_per_step'],2), {x:round(v['ms_per_launch'],3) for x,v in k.items() if 'sage' in x or 'l0' in x}, c.get('sm_mhz'), c.get('power_w_median'), c.get('power_cap_samples'), c.get('samples'))
 except Exception as e:
     print('$v failed', e)" 
 done
