@@ -189,3 +189,47 @@ def test_small_graphs_stay_materialized(api):
     finally:
         os.environ["GROOT_L0_KEYED_MIN_ROWS"] = "0"
     assert "sage_layer0" in names and "l0_keys" not in names, names
+
+
+def local_graph(n, max_fanin, window, seed):
+    """Neighbours within `window` rows (tiles stay under the staged-halo cap, so
+    the tile kernels take the row-record path), degrees well above the four
+    slots a row record holds inline."""
+    rng = np.random.default_rng(seed)
+    e = []
+    for v in range(1, n):
+        lo = max(0, v - window)
+        for u in rng.integers(lo, v, rng.integers(1, max_fanin)):
+            e.append((int(u), v))
+    rp, ci = O.build_csr(n, np.array(e, np.uint32))
+    feat = (rng.random((n, 4)) < 0.5).astype(np.uint8)
+    return rp, ci, feat
+
+
+@pytest.mark.parametrize("seed,sparse", [(11, True), (12, True), (13, False)])
+def test_row_records_long_rows(api, seed, sparse):
+    """Rows of degree > 4 finish their neighbour sums from the staged slot list
+    (tile_plan.cuh row records hold four slots inline): forwards against the
+    oracle on graphs where most rows are that long. Sparse features: keyed
+    (and its tensor-core variant bit-identical to the materialized forward);
+    dense features: not keyable, the materialized path."""
+    rp, ci, feat = local_graph(4000, 7, 60, seed)  # no slow tiles, ~80 % of rows longer than 4
+    if sparse:
+        feat[:] = 0
+        feat[::13, 0] = 1
+    deg = np.diff(rp)
+    assert (deg > 4).mean() > 0.5 and deg.max() < 128
+    n = feat.shape[0]
+    g = api.EdaGraph.from_host(n, rp, ci, feat, np.zeros(n, np.uint8))
+    prm = O.init_model(seed)
+    model = api.Model.from_params(prm)
+    h = O.HostGraph(n, rp, ci, feat, np.zeros(n, np.uint8), deg.astype(np.uint32), np.zeros((0, 2), np.uint32))
+    ref = O.forward(h, prm)
+    lg, names = profiled_names(lambda: api.forward(model, g))
+    assert ("sage_layer0" not in names) == sparse, names
+    assert rel_err(lg, ref) <= 1e-5
+    assert_same_classes_off_ties(np.argmax(lg, 1), np.argmax(ref, 1), ref, "forward vs oracle")
+    if sparse:
+        plain = with_env("GROOT_L0_KEYED", "0", lambda: api.forward(model, g))
+        assert rel_err(plain, ref) <= 1e-5
+        np.testing.assert_array_equal(with_env("GROOT_L1_XFORM", "0", lambda: api.forward(model, g)), plain)
