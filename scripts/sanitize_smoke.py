@@ -35,4 +35,16 @@ print("train", st.loss, flush=True)
 rp = np.array([0, 2, 3, 600], np.uint64)
 ci = np.concatenate([[0, 1, 2], np.arange(597) % 3]).astype(np.uint32)
 print("spmm f64", float(api.spmm_csr_f64(rp, ci, np.ones(600), np.ones((3, 4)), hd_threshold=512).sum()), flush=True)
+# row records with degree > 4 tails (keyed: sparse features; materialized: dense)
+from oracle import pyoracle as O  # noqa: E402  (graph construction only)
+rng = np.random.default_rng(11)
+e = [(int(u), v) for v in range(1, 2000) for u in rng.integers(max(0, v - 60), v, rng.integers(1, 7))]
+rp2, ci2 = O.build_csr(2000, np.array(e, np.uint32))
+for sparse in (True, False):
+    f2 = (rng.random((2000, 4)) < 0.5).astype(np.uint8)
+    if sparse:
+        f2[:] = 0
+        f2[::13, 0] = 1
+    g2 = api.EdaGraph.from_host(2000, rp2, ci2, f2, np.zeros(2000, np.uint8))
+    print("long rows", "keyed" if sparse else "materialized", bool(np.isfinite(api.forward(model, g2)).all()), flush=True)
 print("sanitize smoke done", flush=True)
