@@ -266,7 +266,7 @@ struct TkCfg {
   static constexpr uint32_t kTableMem = kKeyed ? 2u * kTkTableRows * 128u : 0u;  // entry rows (Tn) | Ts
   static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes + kHeadBBytes +
                                     (256 + 32 + kTileRing) * 4 + 16 * kMetaStages +
-                                    8 * (2 * kStages + 5 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
+                                    8 * (2 * kStages + 6 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
   static_assert(kMetaLead + kRowStages + kStages + 4 < static_cast<int>(kTileRing), "tile ring covers every role's lag");
   static_assert(kSmem <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
   static_assert(kMetaLead >= 2, "plan records lead the rows");
@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   uint64_t* r_full = m_empty + kTkMetaStages;  // [kTkRowStages] tile + halo rows landed
   uint64_t* r_empty = r_full + kTkRowStages;
   uint64_t* hdone = r_empty + kTkRowStages;  // last layer: head MMA of the current tile complete
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(hdone + 1);
+  uint64_t* hready = hdone + 1;              // last layer: the head's A operand is in TMEM (epilogue -> MMA warp)
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(hready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n = a.n;
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       ptx::mbar_init(&r_empty[s], kProdWarps * 32);
     }
     ptx::mbar_init(hdone, 1);
+    ptx::mbar_init(hready, kEpiWarps * 32);
     ptx::mbar_fence_init();
   }
   if (kMma && warp == kMmaWarp) ptx::tmem_alloc<kTmemCols>(sTmem);
@@ -532,6 +534,26 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
       const uint32_t acc = kAccBufs == 2 ? (it & 1) : 0u, aph = kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1);
+      if (kMode == kModeLast && it > 0) {
+        // the previous tile's 32 -> classes head, once the epilogue has put its
+        // A operand (relu(acc + b) split into TF32 hi / lo) into TMEM
+        ptx::mbar_wait(hready, (it - 1) & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          constexpr uint32_t hdesc = ptx::idesc_tf32<kTileM, kHeadN>();
+          const uint32_t ahi = tmem_base + kHeadHiCol, alo = tmem_base + kHeadLoCol;
+          const uint32_t hb = ptx::smem_addr(sHB);
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint64_t bhi = ptx::umma_desc_sw128(hb + kk * 32), blo = ptx::umma_desc_sw128(hb + kHeadN * 128 + kk * 32);
+            ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, bhi, hdesc, kk != 0);
+            ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, blo, hdesc, 1);
+            ptx::mma_tf32_ts(tmem_base + kHeadDCol, alo + kk * 8, bhi, hdesc, 1);
+          }
+          ptx::mma_commit(hdone);
+        }
+        __syncwarp();
+      }
       ptx::mbar_wait(&full[s], ph);
       if (lane == 0) tstamp(a.trace, it, 8);
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -824,49 +846,30 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       } else {
         // last layer: the accumulator is freed as soon as it is loaded; relu(acc + b)
         // split into TF32 hi / lo goes to the head's TMEM columns, then the 32 ->
-        // classes head runs as one tensor-core MMA group issued by warp 0 once all
-        // four quadrants are in; each lane takes its row's logits and the first maximum
+        // classes head runs as one tensor-core MMA group, issued by the MMA warp
+        // once all four quadrants are in (hready); each lane takes its row's logits
+        // and the first maximum
         float r[32];
         ptx::tmem_ld_32x32b_x32(tq, r);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
-#ifdef GROOT_EXP_LAST_NOHEAD  // timing experiment only (wrong classes): the last layer without any head
-        if (row0 + lane < n) a.cls[row0 + lane] = r[0] > r[1];
-        continue;
-#endif
         uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {  // column c holds output feature kcol_feature(c)
-          const float x = fmaxf(r[c] + hw.bias[kcol_feature(c)], 0.0f);
-          hi[c] = __float_as_uint(x) & 0xFFFFE000u;
-          lo[c] = __float_as_uint(x - __uint_as_float(hi[c]));
+        for (int c = 0; c < 32; c += 2) {  // column c holds output feature kcol_feature(c); pairs: FADD2
+          const float2 z = ptx::fadd2(make_float2(r[c], r[c + 1]),
+                                      make_float2(hw.bias[kcol_feature(c)], hw.bias[kcol_feature(c + 1)]));
+          const float2 x = make_float2(fmaxf(z.x, 0.0f), fmaxf(z.y, 0.0f));
+          hi[c] = __float_as_uint(x.x) & 0xFFFFE000u;
+          hi[c + 1] = __float_as_uint(x.y) & 0xFFFFE000u;
+          const float2 l = ptx::fsub2(x, make_float2(__uint_as_float(hi[c]), __uint_as_float(hi[c + 1])));
+          lo[c] = __float_as_uint(l.x);
+          lo[c + 1] = __float_as_uint(l.y);
         }
         ptx::tmem_st_32x32b_x32(tmem_base + kHeadHiCol + ((q * 32u) << 16), hi);
         ptx::tmem_st_32x32b_x32(tmem_base + kHeadLoCol + ((q * 32u) << 16), lo);
         ptx::tmem_wait_st();
-#ifdef GROOT_EXP_LAST_SPLITONLY  // timing experiment only (wrong classes): split + stores, no head MMA
-        if (row0 + lane < n) a.cls[row0 + lane] = hi[0] > lo[1];
-        continue;
-#endif
         ptx::tc_fence_before();
-        ptx::named_bar_sync(1, kEpiWarps * 32);
-        if (warp == 0) {
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            constexpr uint32_t hdesc = ptx::idesc_tf32<kTileM, kHeadN>();
-            const uint32_t ahi = tmem_base + kHeadHiCol, alo = tmem_base + kHeadLoCol;
-            const uint32_t hb = ptx::smem_addr(sHB);
-#pragma unroll
-            for (uint32_t kk = 0; kk < 4; ++kk) {
-              const uint64_t bhi = ptx::umma_desc_sw128(hb + kk * 32), blo = ptx::umma_desc_sw128(hb + kHeadN * 128 + kk * 32);
-              ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, bhi, hdesc, kk != 0);
-              ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, blo, hdesc, 1);
-              ptx::mma_tf32_ts(tmem_base + kHeadDCol, alo + kk * 8, bhi, hdesc, 1);
-            }
-            ptx::mma_commit(hdone);
-          }
-          __syncwarp();
-        }
+        ptx::mbar_arrive(hready);  // the MMA warp issues the head
         if (GROOT_EPI_POLL_NS) ptx::mbar_wait_poll(hdone, e & 1, 32);
         else ptx::mbar_wait(hdone, e & 1);
         ptx::tc_fence_after();
