@@ -582,7 +582,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                     "path": "groot_classify_aig (pinned host AIG -> encode -> batch -> predict_full -> host classes)"},
             "accuracy": accuracy,
-            "accuracy_note": "trained 8-bit CSA ASG1 (reference recipe run through the oracle restatement of train)",
+            "accuracy_note": "trained 8-bit CSA ASG1 (reference recipe run through the oracle restatement of train); "
+                             "the depth-4 Weisfeiler-Lehman bound of any message-passing GNN on these features is "
+                             "0.8785 at 256 bits (scripts/wl_bound.py, DESIGN.md 5)",
             "clocks": clocks,
             "gpu_launches": int(launches),
         }
