@@ -195,7 +195,6 @@ struct groot_graph {
   groot::DevBuf<unsigned long long> l0_key, l0_dict, l0_ctab;  // l0_key: HD rows' records
   groot::DevBuf<uint16_t> l0_slot;                             // LD rows: slot in their CTA's table
   groot::DevBuf<uint8_t> l0_id, l0_idmap, l0_hid, l0_xlat;
-  groot::DevBuf<unsigned long long> l0_krec;  // keyed row records: entry-row offsets (tiles x 128)
   groot::DevBuf<float> l0_table;
   groot::DevBuf<float> l0_xtab;  // keyed layer 1, transform first: Tn | Ts (entry rows . W_neigh / W_self)
   groot::DevBuf<uint32_t> l0_flags;

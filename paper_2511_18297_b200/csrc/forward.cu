@@ -266,7 +266,7 @@ struct TkCfg {
   static constexpr uint32_t kTableMem = kKeyed ? 2u * kTkTableRows * 128u : 0u;  // entry rows (Tn) | Ts
   static constexpr uint32_t kSmem = kRowMem + kMetaStages * kTkMetaBytes + kTableMem + kBBytes + kHeadBBytes +
                                     (256 + 32 + kTileRing) * 4 + 16 * kMetaStages +
-                                    8 * (2 * kStages + 6 + 2 * kRowStages + 2 * kMetaStages) + 16 + 1024;
+                                    8 * (2 * kStages + 6 + 2 * kRowStages + 3 * kMetaStages) + 16 + 1024;
   static_assert(kMetaLead + kRowStages + kStages + 4 < static_cast<int>(kTileRing), "tile ring covers every role's lag");
   static_assert(kSmem <= 232448, "tile kernel exceeds the 227 KB shared-memory limit");
   static_assert(kMetaLead >= 2, "plan records lead the rows");
@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
   uint64_t* m_empty = m_full + kTkMetaStages;
   uint64_t* r_full = m_empty + kTkMetaStages;  // [kTkRowStages] tile + halo rows landed
   uint64_t* r_empty = r_full + kTkRowStages;
-  uint64_t* hdone = r_empty + kTkRowStages;  // last layer: head MMA of the current tile complete
+  uint64_t* m_ready = r_empty + kTkRowStages;  // [kTkMetaStages] keyed: the plan's row records translated to entry rows
+  uint64_t* hdone = m_ready + kTkMetaStages;  // last layer: head MMA of the current tile complete
   uint64_t* hready = hdone + 1;              // last layer: the head's A operand is in TMEM (epilogue -> MMA warp)
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(hready + 1);
 
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     }
     for (int s = 0; s < kTkMetaStages; ++s) {
       ptx::mbar_init(&m_full[s], 1);
+      ptx::mbar_init(&m_ready[s], 32 * kCopiers);
       ptx::mbar_init(&m_empty[s], kProdWarps * 32);
     }
     for (int s = 0; s < kTkRowStages; ++s) {
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           ptx::bulk_load(sp + kTkLcolOff, a.lcol + m.x, m.z * 2u, &m_full[ms]);
         }
         if (hpad) ptx::bulk_load(sp + kTkHaloOff, a.halo + m.y, hpad * 4u, &m_full[ms]);
-        if (!slow)  // (keyed: entry-row records by plan tile, l0_halo_ids_kernel)
+        if (!slow)  // (keyed: translated to entry rows by the copier warps)
           ptx::bulk_load(sp + kTkRecOff, a.rec + static_cast<size_t>(pt) * kTpRows, kTpRows * 8u, &m_full[ms]);
       };
       uint32_t rows_tile[kTkMetaLead];  // tiles of iterations it .. it + kTkMetaLead - 1
@@ -490,7 +492,39 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       }
     }
     __syncwarp();
-  } else if (copier >= 0 && !kKeyed) {  // (keyed layers stage no rows: the copiers idle)
+  } else if (copier >= 0 && kKeyed) {
+    // ===== keyed layers (no rows to stage): the copier warps translate each
+    // plan stage's row records in place, local slot byte offsets -> entry-row
+    // byte offsets (the zero slot -> entry kTkTableRows - 1, kept zero), a few
+    // tiles ahead of the producers =====
+    const uint32_t gl = static_cast<uint32_t>(copier) * 32u + lane;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t ms = it % kTkMetaStages;
+      ptx::mbar_wait_sleep(&m_full[ms], (it / kTkMetaStages) & 1, 100);
+      if (sTile[it % kTileRing] == kEndTile) {
+        ptx::mbar_arrive(&m_ready[ms]);  // the producers see the end through m_ready
+        break;
+      }
+      if (!(sMeta[ms].w & kTpSlow)) {
+        uint8_t* sp = sPlan + ms * kTkMetaBytes;
+        uint32_t* rw = reinterpret_cast<uint32_t*>(sp + kTkRecOff);
+        const uint8_t* kid = sp + kTkKidOff;  // entry ids of the tile rows, then of the halo rows
+        auto map = [&](uint32_t f) -> uint32_t {
+          const uint32_t sl = f >> 7;
+          return ((sl == kTpZeroSlot ? kTkTableRows - 1u : static_cast<uint32_t>(kid[sl])) << 7) | (f & 0x7Fu);
+        };
+#pragma unroll 4
+        for (uint32_t k = gl; k < 2 * kTpRows; k += 32 * kCopiers) {
+          const uint32_t w = rw[k];
+          rw[k] = map(w & 0xFFFFu) | (map(w >> 16) << 16);
+        }
+        // the stage is refilled by bulk copies (async proxy) once the producers
+        // release it: order these generic-proxy writes before that
+        ptx::fence_proxy_async_smem();
+      }
+      ptx::mbar_arrive(&m_ready[ms]);
+    }
+  } else if (copier >= 0) {
     // ===== halo copiers: 16-B cp.async per lane, 8 lanes per row =====
     const uint32_t sRows_s = ptx::smem_addr(sRows);
     const uint32_t gl = static_cast<uint32_t>(copier) * 32u + lane;
@@ -619,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       tstamp(tr, it, 3);
       tstamp(tr7, it, 13);
       if (kTraceOn) wt0 = clock64();
-      ptx::mbar_wait(&m_full[ms], (it / kTkMetaStages) & 1);
+      ptx::mbar_wait(kKeyed ? &m_ready[ms] : &m_full[ms], (it / kTkMetaStages) & 1);
       const uint32_t t = sTile[it % kTileRing];
       if (t == kEndTile) {  // hand the MMA an empty stage so it sees the end too
         hand_over();
@@ -1445,13 +1479,9 @@ __global__ void l0_hd_ids_kernel(uint32_t count, const uint32_t* __restrict__ hd
 __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const uint4* __restrict__ tmeta,
                                                           const uint32_t* __restrict__ halo, uint32_t period,
                                                           uint32_t period_rows, const uint8_t* __restrict__ ids,
-                                                          const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids,
-                                                          const unsigned long long* __restrict__ rec,
-                                                          unsigned long long* __restrict__ krec) {
+                                                          const uint32_t* __restrict__ flags, uint8_t* __restrict__ hids) {
   if (flags[0]) return;
   constexpr uint32_t kPer = kTpHaloCap / 32;
-  __shared__ uint8_t sh_all[8][kTpRows + kTpHaloCap];  // the warp's tile ids | halo ids, for the records
-  uint8_t* sh = sh_all[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
@@ -1459,14 +1489,6 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     const uint32_t shift = period ? (t / period) * period_rows : 0u;
     const uint4 m = __ldg(tmeta + pt);
     if (m.w & kTpSlow) continue;
-    const bool recs = !(period && t >= period);
-    // records and tile ids first (independent of the halo lookups)
-    unsigned long long r[kTpRows / 32];
-    if (recs) {
-#pragma unroll
-      for (uint32_t i = 0; i < kTpRows / 32; ++i) r[i] = __ldg(rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
-      reinterpret_cast<uint32_t*>(sh)[lane] = __ldg(reinterpret_cast<const uint32_t*>(ids + static_cast<size_t>(t) * kTpRows) + lane);
-    }
     uint32_t hv[kPer];
 #pragma unroll
     for (uint32_t u = 0; u < kPer; ++u) hv[u] = lane + 32 * u < m.w ? __ldg(halo + m.y + lane + 32 * u) : 0u;
@@ -1475,29 +1497,7 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
     for (uint32_t u = 0; u < kPer; ++u) iv[u] = lane + 32 * u < m.w ? __ldg(ids + shift + hv[u]) : 0u;
 #pragma unroll
     for (uint32_t u = 0; u < kPer; ++u)
-      if (lane + 32 * u < m.w) {
-        hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
-        sh[kTpRows + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
-      }
-    // keyed row records of tile t: each slot byte offset -> its entry row's
-    // byte offset in the table (zero slot -> entry kTkTableRows - 1, kept zero).
-    // A periodic plan is a batch of identical copies, whose rows have the same
-    // records and so the same entry ids in every copy: the first period's
-    // tiles are enough (the kernels index them by plan tile).
-    if (!recs) continue;
-    __syncwarp();
-#pragma unroll
-    for (uint32_t i = 0; i < kTpRows / 32; ++i) {
-      unsigned long long o = 0;
-#pragma unroll
-      for (uint32_t k = 0; k < kTpRecSlots; ++k) {
-        const uint32_t f = static_cast<uint32_t>(r[i] >> (16 * k)) & 0xFFFFu, sl = f >> 7;
-        const uint32_t id = sl == kTpZeroSlot ? kTkTableRows - 1u : sh[sl];
-        o |= static_cast<unsigned long long>((id << 7) | (f & 0x7Fu)) << (16 * k);
-      }
-      krec[static_cast<size_t>(t) * kTpRows + 32 * i + lane] = o;
-    }
-    __syncwarp();
+      if (lane + 32 * u < m.w) hids[static_cast<size_t>(t) * kTpHaloCap + lane + 32 * u] = static_cast<uint8_t>(iv[u]);
   }
 }
 
@@ -1896,7 +1896,6 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   if (g->l0_slot.n < n) g->l0_slot.alloc(n);
   if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
   if (g->l0_hid.n < static_cast<size_t>(ntiles) * kTpHaloCap) g->l0_hid.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
-  if (g->l0_krec.n < static_cast<size_t>(ntiles) * kTpRows) g->l0_krec.alloc(static_cast<size_t>(ntiles) * kTpRows);
   if (g->l0_ctab.n < static_cast<size_t>(key_ctas) * kDictLocal) {
     g->l0_ctab.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
     g->l0_xlat.alloc(static_cast<size_t>(key_ctas) * kDictLocal);
@@ -1930,7 +1929,7 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
                    g->l0_dict.p, g->l0_idmap.p, g->l0_flags.p, g->l0_id.p);
     GROOT_LAUNCH(l0_halo_ids_kernel, blocks_for(ntiles * 32ull, 256, sms * 16), 256, 0,
                  ntiles, reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_halo.p, g->tp_period, g->tp_period_rows,
-                 g->l0_id.p, g->l0_flags.p, g->l0_hid.p, g->tp_rec.p, g->l0_krec.p);
+                 g->l0_id.p, g->l0_flags.p, g->l0_hid.p);
   }
   if (g->l0_mode == 0) {
     uint32_t fl[2] = {0, 0};
@@ -1987,7 +1986,6 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   if (keyed_in) {
     a.keys = g->l0_id.p;
     a.hids = g->l0_hid.p;
-    a.rec = g->l0_krec.p;  // keyed records (entry-row offsets), by plan tile
     a.ktable = xform ? g->l0_xtab.p : g->l0_table.p;
     a.ktable_self = g->l0_xtab.p + kTkTableRows * kF;
   }
