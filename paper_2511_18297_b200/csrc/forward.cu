@@ -1233,6 +1233,37 @@ __device__ void dict_insert_global(unsigned long long* tab, uint32_t* flags, uns
   flags[0] = 1;
 }
 
+// Warp-collective: the first lane of each distinct record finds / inserts its
+// slot in the CTA's table; every lane gets its record's slot (0xFFFF: table full).
+__device__ __forceinline__ uint32_t l0_dedup_insert(unsigned long long key, unsigned long long* ltab, uint32_t* lcount,
+                                                    uint32_t* lbad, int lane) {
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const int leader = __ffs(peers) - 1;
+  uint32_t slot = 0xFFFFu;
+  if (key != kDictEmpty && leader == lane) {
+    uint32_t h = dict_hash(key) & (kDictLocal - 1);
+    for (;; h = (h + 1) & (kDictLocal - 1)) {
+      const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ltab + h);
+      if (cur == key) break;
+      if (cur == kDictEmpty) {
+        if (*reinterpret_cast<volatile uint32_t*>(lcount) >= kDictLocalMax) {
+          *lbad = 1;
+          h = 0xFFFFu;
+          break;
+        }
+        const unsigned long long prev = atomicCAS(ltab + h, kDictEmpty, key);
+        if (prev == kDictEmpty) {
+          atomicAdd(lcount, 1u);
+          break;
+        }
+        if (prev == key) break;
+      }
+    }
+    slot = h;
+  }
+  return __shfl_sync(0xffffffffu, slot, leader);
+}
+
 // LD rows: kL0KeyRows rows per thread with their gathers interleaved (a row's
 // chain row_ptr -> col -> features is three dependent memory round trips), the
 // gather of sage_layer0_kernel; warp-deduplicated records go into a per-CTA
@@ -1294,34 +1325,103 @@ __global__ void __launch_bounds__(256) l0_key_kernel(uint32_t n, const uint32_t*
                                packed[r] >> 24};
         key = l0_record(x[r], d[r], s);
       }
-      // warp-level dedup: the first lane of each record finds / inserts its slot
-      const uint32_t peers = __match_any_sync(0xffffffffu, key);
-      const int leader = __ffs(peers) - 1;
-      uint32_t slot = 0xFFFFu;
-      if (key != kDictEmpty && leader == lane) {
-        uint32_t h = dict_hash(key) & (kDictLocal - 1);
-        for (;; h = (h + 1) & (kDictLocal - 1)) {
-          const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ltab + h);
-          if (cur == key) break;
-          if (cur == kDictEmpty) {
-            if (*reinterpret_cast<volatile uint32_t*>(&lcount) >= kDictLocalMax) {
-              lbad = 1;
-              h = 0xFFFFu;
-              break;
-            }
-            const unsigned long long prev = atomicCAS(ltab + h, kDictEmpty, key);
-            if (prev == kDictEmpty) {
-              atomicAdd(&lcount, 1u);
-              break;
-            }
-            if (prev == key) break;
-          }
-        }
-        slot = h;
-      }
-      slot = __shfl_sync(0xffffffffu, slot, leader);
+      const uint32_t slot = l0_dedup_insert(key, ltab, &lcount, &lbad, lane);
       if (row < n) lslot[row] = static_cast<uint16_t>(key != kDictEmpty ? slot : 0xFFFFu);
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && lbad) flags[0] = 1;
+  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x) {
+    const unsigned long long k = ltab[i];
+    ctab[static_cast<size_t>(blockIdx.x) * kDictLocal + i] = k;
+    if (k != kDictEmpty) dict_insert_global(gtab, flags, k);
+  }
+}
+
+// The key pass through the tile plan: a warp per 128-row tile stages the
+// feature words of the tile's rows and of its halo rows in shared memory (the
+// row records name each neighbour's slot), so a row's neighbour features are
+// shared-memory reads instead of a CSR walk with 4-byte gathers from L2 (one
+// 32-byte sector each). Rows of degree > 4 finish from the CSR; slow tiles
+// take the CSR walk. Same records, dedup and tables as l0_key_kernel; the CTA
+// of a row is the CTA of its tile's warp (l0_ids_kernel, tiled).
+struct L0KeyPlan {
+  const uint4* tmeta;
+  const unsigned long long* rec;
+  const uint32_t* halo;
+  uint32_t period, period_rows;
+};
+
+__global__ void __launch_bounds__(256) l0_key_tile_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+                                                          const uint32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ feat, uint32_t thr,
+                                                          const L0KeyPlan p, uint16_t* __restrict__ lslot,
+                                                          unsigned long long* __restrict__ ctab,
+                                                          unsigned long long* __restrict__ gtab, uint32_t* flags) {
+  __shared__ unsigned long long ltab[kDictLocal];
+  __shared__ uint32_t lcount, lbad;
+  __shared__ __align__(16) uint32_t sF_all[8][kTpRows + kTpHaloCap];
+  for (uint32_t i = threadIdx.x; i < kDictLocal; i += blockDim.x) ltab[i] = kDictEmpty;
+  if (threadIdx.x == 0) lcount = lbad = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t* sF = sF_all[threadIdx.x >> 5];
+  const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t pt = p.period ? t % p.period : t;
+    const uint32_t shift = p.period ? (t / p.period) * p.period_rows : 0u;
+    const uint4 meta = __ldg(p.tmeta + pt);
+    const bool slow = (meta.w & kTpSlow) != 0;
+    const uint32_t row0 = t * kTpRows;
+    unsigned long long r[kTpRows / 32];
+    if (!slow) {
+#pragma unroll
+      for (uint32_t i = 0; i < kTpRows / 32; ++i) r[i] = __ldg(p.rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
+      if (row0 + kTpRows <= n) {
+        reinterpret_cast<uint4*>(sF)[lane] = __ldg(reinterpret_cast<const uint4*>(feat + row0) + lane);
+      } else {
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) sF[4 * lane + i] = row0 + 4 * lane + i < n ? __ldg(feat + row0 + 4 * lane + i) : 0u;
+      }
+      for (uint32_t i = lane; i < meta.w; i += 32) sF[kTpRows + i] = __ldg(feat + shift + __ldg(p.halo + meta.y + i));
+      if (lane == 0) sF[kTpZeroSlot] = 0u;
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t i = 0; i < kTpRows / 32; ++i) {
+      const uint32_t row = row0 + 32 * i + lane;
+      unsigned long long key = kDictEmpty;
+      if (row < n) {
+        uint32_t x, d, packed = 0;
+        bool hd;
+        if (slow) {
+          x = __ldg(feat + row);
+          const uint32_t b = __ldg(rp + row);
+          d = __ldg(rp + row + 1) - b;
+          hd = d >= thr;
+          for (uint32_t k = 0; k < d && !hd; ++k) packed += __ldg(feat + __ldg(col + b + k));
+        } else {
+          x = sF[32 * i + lane];
+          const uint32_t lo32 = static_cast<uint32_t>(r[i]);
+          hd = (lo32 & kTpRecHd) != 0;
+          d = tp_rec_degree(lo32);
+#pragma unroll
+          for (uint32_t k = 0; k < kTpRecSlots; ++k) packed += sF[static_cast<uint32_t>(r[i] >> (16 * k + 7)) & 0x1FFu];
+          if (lo32 & kTpRecLong) {
+            const uint32_t b = __ldg(rp + row);
+            for (uint32_t k = kTpRecSlots; k < d; ++k) packed += __ldg(feat + __ldg(col + b + k));
+          }
+        }
+        if (!hd) {
+          if ((x & 0xFEFEFEFEu) != 0u) lbad = 1;  // byte counters of binary features (d < 256) are exact
+          const uint32_t sc[4] = {packed & 0xFFu, (packed >> 8) & 0xFFu, (packed >> 16) & 0xFFu, packed >> 24};
+          key = l0_record(x, d, sc);
+        }
+      }
+      const uint32_t slot = l0_dedup_insert(key, ltab, &lcount, &lbad, lane);
+      if (row < n) lslot[row] = static_cast<uint16_t>(key != kDictEmpty ? slot : 0xFFFFu);
+    }
+    __syncwarp();  // sF is restaged for the warp's next tile
   }
   __syncthreads();
   if (threadIdx.x == 0 && lbad) flags[0] = 1;
@@ -1440,13 +1540,14 @@ __global__ void __launch_bounds__(256) l0_xlat_kernel(uint32_t ctas, const unsig
 // u8 entry id of every LD row (4 rows per thread, one 32-bit store): the row's
 // l0_key_kernel CTA (warp-strided row groups: CTA = ((row / (32 kL0KeyRows)) % warps) / 8) and
 // its slot there. HD rows are written afterwards by l0_hd_ids_kernel.
-__global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, uint32_t key_warps, const uint16_t* __restrict__ lslot,
+__global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, uint32_t key_warps, uint32_t rows_per_group,
+                                                     const uint16_t* __restrict__ lslot,
                                                      const uint8_t* __restrict__ xlat,
                                                      const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
   if (flags[0]) return;
   const uint32_t quads = (n + 3) / 4;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
-    const uint32_t cta = (((4 * q) / (32 * kL0KeyRows)) % key_warps) >> 3;  // the 4 rows share a row group
+    const uint32_t cta = (((4 * q) / rows_per_group) % key_warps) >> 3;  // the 4 rows share a row group
     const uint8_t* xl = xlat + static_cast<size_t>(cta) * kDictLocal;
     uint32_t out = 0;
     if (4 * q + 3 < n) {
@@ -1892,7 +1993,10 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   const uint32_t n = g->n;
   const uint32_t ntiles = (n + kTileM - 1) / kTileM;
   const unsigned sms = static_cast<unsigned>(num_sms());
-  const unsigned key_ctas = blocks_for((n + kL0KeyRows - 1) / kL0KeyRows, 256, sms * 8);
+  static const bool tiled_env = env_u32("GROOT_L0_KEY_TILED", 1) != 0;
+  const bool key_tiled = tiled_env && g->tp_meta.p && g->tp_rec.p && g->tp_threshold == g->hd_threshold;
+  const unsigned key_ctas = key_tiled ? blocks_for(ntiles, 8, sms * 8)  // a warp per tile
+                                      : blocks_for((n + kL0KeyRows - 1) / kL0KeyRows, 256, sms * 8);
   if (g->l0_slot.n < n) g->l0_slot.alloc(n);
   if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
   if (g->l0_hid.n < static_cast<size_t>(ntiles) * kTpHaloCap) g->l0_hid.alloc(static_cast<size_t>(ntiles) * kTpHaloCap);
@@ -1916,13 +2020,21 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
     if (g->num_hd)
       GROOT_LAUNCH(hd_key_kernel, std::min<uint32_t>(g->num_hd, sms * 8), 256, 0, g->hd_rows.p, g->num_hd, g->rp.p,
                    g->col.p, feat, g->l0_key.p, g->l0_dict.p, g->l0_flags.p);
-    GROOT_LAUNCH(l0_key_kernel, key_ctas, 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold, g->l0_slot.p,
-                 g->l0_ctab.p, g->l0_dict.p, g->l0_flags.p);
+    if (key_tiled) {
+      const L0KeyPlan kp{reinterpret_cast<const uint4*>(g->tp_meta.p), g->tp_rec.p, g->tp_halo.p, g->tp_period,
+                         g->tp_period_rows};
+      GROOT_LAUNCH(l0_key_tile_kernel, key_ctas, 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold, kp, g->l0_slot.p,
+                   g->l0_ctab.p, g->l0_dict.p, g->l0_flags.p);
+    } else {
+      GROOT_LAUNCH(l0_key_kernel, key_ctas, 256, 0, n, g->rp.p, g->col.p, feat, g->hd_threshold, g->l0_slot.p,
+                   g->l0_ctab.p, g->l0_dict.p, g->l0_flags.p);
+    }
     GROOT_LAUNCH(dict_finalize_kernel, 1, 1024, 0, g->l0_dict.p, g->l0_flags.p, *reinterpret_cast<const Layer0W*>(m->l0w),
                  g->l0_table.p, g->l0_idmap.p);
     GROOT_LAUNCH(l0_xlat_kernel, blocks_for(key_ctas * kDictLocal, 256), 256, 0, key_ctas, g->l0_ctab.p, g->l0_dict.p,
                  g->l0_idmap.p, g->l0_flags.p, g->l0_xlat.p);
-    GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, key_ctas * 8u, g->l0_slot.p,
+    GROOT_LAUNCH(l0_ids_kernel, blocks_for((n + 3) / 4, 256, sms * 8), 256, 0, n, key_ctas * 8u,
+                 key_tiled ? kTpRows : 32u * kL0KeyRows, g->l0_slot.p,
                  g->l0_xlat.p, g->l0_flags.p, g->l0_id.p);
     if (g->num_hd)
       GROOT_LAUNCH(l0_hd_ids_kernel, blocks_for(g->num_hd, 256), 256, 0, g->num_hd, g->hd_rows.p, g->l0_key.p,
