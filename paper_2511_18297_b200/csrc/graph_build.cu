@@ -77,12 +77,28 @@ __global__ void encode_kernel(uint32_t ni, uint32_t na, const uint32_t* __restri
 // ---------------------------------------------------------------------------
 // K2: symmetric CSR (src/encode.cpp:14-31)
 // ---------------------------------------------------------------------------
+// Warp-aggregated counter increments: the lanes of a warp that hit the same
+// counter (an AIG's fan-out nodes -- a multiplier's primary inputs feed a
+// thousand partial products each -- make neighbouring edges share endpoints)
+// issue one atomic per distinct counter; each lane gets its own slot.
+__device__ __forceinline__ uint32_t warp_agg_add(uint32_t* cnt, uint32_t idx, bool want_slot) {
+  const uint32_t mask = __activemask();
+  const uint32_t peers = __match_any_sync(mask, idx);
+  const uint32_t lane = threadIdx.x & 31u;
+  const int leader = __ffs(peers) - 1;
+  uint32_t old = 0;
+  if (static_cast<int>(lane) == leader) old = atomicAdd(&cnt[idx], static_cast<uint32_t>(__popc(peers)));
+  if (!want_slot) return 0;
+  old = __shfl_sync(peers, old, leader);
+  return old + static_cast<uint32_t>(__popc(peers & ((1u << lane) - 1u)));
+}
+
 __global__ void degree_count_kernel(uint64_t ne, const uint2* __restrict__ e, uint32_t* cnt) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 uv = e[i];
-    atomicAdd(&cnt[uv.x], 1u);
-    atomicAdd(&cnt[uv.y], 1u);
+    warp_agg_add(cnt, uv.x, false);
+    warp_agg_add(cnt, uv.y, false);
   }
 }
 
@@ -91,8 +107,8 @@ __global__ void scatter_kernel(uint64_t ne, const uint2* __restrict__ e, uint32_
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 uv = e[i];
-    col[atomicAdd(&cursor[uv.x], 1u)] = uv.y;
-    col[atomicAdd(&cursor[uv.y], 1u)] = uv.x;
+    col[warp_agg_add(cursor, uv.x, true)] = uv.y;
+    col[warp_agg_add(cursor, uv.y, true)] = uv.x;
   }
 }
 
