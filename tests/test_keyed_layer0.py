@@ -233,3 +233,43 @@ def test_row_records_long_rows(api, seed, sparse):
         plain = with_env("GROOT_L0_KEYED", "0", lambda: api.forward(model, g))
         assert rel_err(plain, ref) <= 1e-5
         np.testing.assert_array_equal(with_env("GROOT_L1_XFORM", "0", lambda: api.forward(model, g)), plain)
+
+
+@pytest.mark.parametrize("threshold", ["256", "16"])
+def test_row_records_hd_threshold(threshold):
+    """Row records under other row-classifier thresholds (GROOT_HD_THRESHOLD,
+    read once per process): 256 makes rows of degree 128..255 LD rows (their
+    degree needs the record's eighth degree bit), 16 makes rows of degree >= 16
+    HD rows. Keyed (sparse features) and materialized forwards vs the oracle."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+from paper_2511_18297_b200 import api
+from oracle import pyoracle as O
+rng = np.random.default_rng(5)
+n = 5000
+e = [(int(u), v) for v in range(1, n) for u in rng.integers(max(0, v - 40), v, rng.integers(1, 4))]
+for hub in range(10, n - 128, 640):  # a few rows of degree ~190 with in-tile neighbours (repeated edges)
+    e += [(hub, int(v)) for v in rng.integers(hub + 1, hub + 110, 190)]
+rp, ci = O.build_csr(n, np.array(e, np.uint32))
+deg = np.diff(rp.astype(np.int64))
+assert deg.max() >= 150 and deg.max() < 256, deg.max()
+for sparse in (True, False):
+    feat = (rng.random((n, 4)) < 0.5).astype(np.uint8)
+    if sparse:
+        feat[:] = 0
+        feat[::11, 1] = 1
+    g = api.EdaGraph.from_host(n, rp, ci, feat, np.zeros(n, np.uint8))
+    prm = O.init_model(4)
+    lg = api.forward(api.Model.from_params(prm), g)
+    h = O.HostGraph(n, rp, ci, feat, np.zeros(n, np.uint8), deg.astype(np.uint32), np.zeros((0, 2), np.uint32))
+    ref = O.forward(h, prm)
+    err = (np.abs(lg - ref).max(1) / np.maximum(np.abs(ref).max(1), 1e-6)).max()
+    assert err <= 1e-5, (sparse, err)
+print("ok")
+"""
+    env = dict(os.environ, GROOT_HD_THRESHOLD=threshold, GROOT_L0_KEYED_MIN_ROWS="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
