@@ -1,6 +1,7 @@
 // tile_plan.cu — builds the per-tile gather plan (tile_plan.cuh) on the device.
 //
-// One warp per 128-row tile, one pass, no global scans:
+// One warp per 128-row tile, no global scans (tile_plan_kernel below has the
+// details: the tile's slot segment staged in shared memory, nonzero-parallel):
 //   * LD degree of each row (degree < threshold; HD rows are flagged and
 //     skipped) -> row offsets into the tile's lcol segment (lrp);
 //   * each LD nonzero re-indexed to its local slot, stored at its own CSR
@@ -45,18 +46,61 @@ __device__ __forceinline__ uint32_t hash_find(const uint32_t* hk, uint32_t c) {
   return h;
 }
 
+// Warp-wide bitonic sort of 256 keys held 8 per lane (index lane*8 + k),
+// ascending: in-register compare-exchanges below distance 8, shuffles above.
+__device__ __forceinline__ void warp_sort256(uint32_t (&v)[8], uint32_t lane) {
+#pragma unroll
+  for (uint32_t s = 2; s <= 256; s <<= 1) {
+#pragma unroll
+    for (uint32_t d = s >> 1; d > 0; d >>= 1) {
+      if (d >= 8) {
+        const uint32_t lb = d >> 3;
+        const bool lower = (lane & lb) == 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          const uint32_t p = __shfl_xor_sync(0xffffffffu, v[k], lb);
+          const bool up = ((lane * 8 + k) & s) == 0;
+          v[k] = (lower == up) ? min(v[k], p) : max(v[k], p);
+        }
+      } else {
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          if (k & d) continue;
+          const bool up = ((lane * 8 + k) & s) == 0;
+          const uint32_t x = v[k], y = v[k ^ d];
+          if ((x > y) == up) {
+            v[k] = y;
+            v[k ^ d] = x;
+          }
+        }
+      }
+    }
+  }
+}
+
+// One warp per tile, nonzero-parallel over the tile's staged slot segment:
+// the segment [loff, loff + lcnt) of col_idx is copied to shared memory once
+// (coalesced); each lane takes nonzeros lane, lane + 32, ...: in-tile columns
+// get their slot, out-of-tile columns go into a shared-memory hash set; the
+// set is compacted and sorted in registers (the halo list); a second pass over
+// the staged segment gives out-of-tile nonzeros their rank. HD rows' nonzeros
+// are masked out (a bitmap over the segment). Row records from the staged slots.
 __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, const uint32_t* __restrict__ rp,
                                                                   const uint32_t* __restrict__ col, uint32_t thr,
                                                                   uint32_t halo_cap, TileMeta* meta, uint16_t* lrp,
                                                                   uint16_t* lcol, uint32_t* halo,
                                                                   unsigned long long* rec, uint32_t* slow_count) {
-  __shared__ uint32_t hk_all[kTpWarps][kHashSlots];    // set of out-of-tile columns
-  __shared__ uint16_t hv_all[kTpWarps][kHashSlots];    // their rank in the sorted halo list
-  __shared__ uint32_t uniq_all[kTpWarps][256];          // sorted halo list (padded to a power of 2)
+  __shared__ uint32_t hk_all[kTpWarps][kHashSlots];      // set of out-of-tile columns
+  __shared__ uint16_t hv_all[kTpWarps][kHashSlots];      // their rank in the sorted halo list
+  __shared__ __align__(16) uint32_t seg_all[kTpWarps][kTpColCap];  // the tile's slot segment of col_idx
+  __shared__ uint16_t sl_all[kTpWarps][kTpColCap];       // local slot of every staged nonzero
+  __shared__ uint32_t hdm_all[kTpWarps][kTpColCap / 32];  // staged nonzeros of HD rows (bitmap)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* hk = hk_all[wib];
   uint16_t* hv = hv_all[wib];
-  uint32_t* uniq = uniq_all[wib];
+  uint32_t* seg = seg_all[wib];
+  uint16_t* sl = sl_all[wib];
+  uint32_t* hdm = hdm_all[wib];
   const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
   for (uint32_t t = blockIdx.x * kTpWarps + wib; t < ntiles; t += gridDim.x * kTpWarps) {
     const uint32_t row0 = t * kTpRows;
@@ -73,68 +117,74 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
     const uint32_t end = rp[min(row0 + kTpRows, n)];
     const uint32_t loff = base & ~7u;
     const uint32_t lcnt = (end - loff + 7u) & ~7u;
+    const uint32_t k0 = base - loff, k1 = end - loff;  // this tile's nonzeros in the segment
     bool slow = lcnt > kTpColCap;
     uint32_t H = 0;
+    uint32_t hsorted[8];
     if (!slow) {
-      // out-of-tile references; more than half the set's slots -> slow tile
-      uint32_t outs = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (!hd[i])
-          for (uint32_t k = 0; k < d[i]; ++k) outs += col[b[i] + k] - row0 >= kTpRows;
-      slow = __reduce_add_sync(0xffffffffu, outs) > kHashSlots / 2;
-    }
-    if (!slow) {
+      // stage the segment (16-B loads: loff is a multiple of 8 entries) and the HD mask
+      for (uint32_t i = lane; i < lcnt / 4; i += 32)
+        reinterpret_cast<uint4*>(seg)[i] = __ldg(reinterpret_cast<const uint4*>(col + loff) + i);
+      for (uint32_t i = lane; i < kTpColCap / 32; i += 32) hdm[i] = 0u;
 #pragma unroll
       for (uint32_t i = lane; i < kHashSlots; i += 32) hk[i] = kEmpty;
       __syncwarp();
-      // in-tile neighbours get their slot now; out-of-tile columns go into the set
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (hd[i]) continue;
-        for (uint32_t k = 0; k < d[i]; ++k) {
-          const uint32_t c = col[b[i] + k];
-          if (c - row0 < kTpRows) lcol[b[i] + k] = static_cast<uint16_t>(c - row0);
-          else hash_insert(hk, c);
-        }
-      }
+      for (int i = 0; i < 4; ++i)
+        if (hd[i] && d[i])
+          for (uint32_t k = b[i] - loff; k < b[i] - loff + d[i] && k < kTpColCap; ++k) atomicOr(&hdm[k >> 5], 1u << (k & 31));
       __syncwarp();
-      // compact the set (slot order), then sort it: the halo list
-#pragma unroll
-      for (uint32_t i0 = 0; i0 < kHashSlots; i0 += 32) {
-        const uint32_t c = hk[i0 + lane];
-        const uint32_t m = __ballot_sync(0xffffffffu, c != kEmpty);
-        const uint32_t at = H + __popc(m & ((1u << lane) - 1u));
-        if (c != kEmpty && at < kTpHaloCap) uniq[at] = c;
-        H += __popc(m);
+      // pass 1: in-tile slots; out-of-tile columns into the set (more than half
+      // the set's slots of out-of-tile references -> slow tile)
+      uint32_t outs = 0;
+      for (uint32_t k = k0 + lane; k < k1; k += 32) {
+        if ((hdm[k >> 5] >> (k & 31)) & 1u) continue;
+        const uint32_t c = seg[k];
+        if (c - row0 < kTpRows) sl[k] = static_cast<uint16_t>(c - row0);
+        else ++outs;
       }
-      slow = H > halo_cap;
+      slow = __reduce_add_sync(0xffffffffu, outs) > kHashSlots / 2;
       if (!slow) {
-        uint32_t P = 32;
-        while (P < H) P <<= 1;
-        for (uint32_t i = H + lane; i < P; i += 32) uniq[i] = kEmpty;
+        for (uint32_t k = k0 + lane; k < k1; k += 32) {
+          if ((hdm[k >> 5] >> (k & 31)) & 1u) continue;
+          const uint32_t c = seg[k];
+          if (c - row0 >= kTpRows) hash_insert(hk, c);
+        }
         __syncwarp();
-        for (uint32_t k = 2; k <= P; k <<= 1)
-          for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-            for (uint32_t x = lane; x < P / 2; x += 32) {
-              const uint32_t i = ((x & ~(jj - 1u)) << 1) | (x & (jj - 1u)), q = i + jj;  // jj is a power of 2
-              const uint32_t u = uniq[i], v = uniq[q];
-              if ((u > v) == ((i & k) == 0)) {
-                uniq[i] = v;
-                uniq[q] = u;
-              }
-            }
-            __syncwarp();
-          }
-        for (uint32_t i = lane; i < H; i += 32) hv[hash_find(hk, uniq[i])] = static_cast<uint16_t>(i);
-        __syncwarp();
+        // compact the set into registers (lane*8 + k), then sort: the halo list
+        uint32_t* uq = reinterpret_cast<uint32_t*>(hv);  // (hv is rewritten below) 512 u16 = 256 u32 scratch
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (hd[i]) continue;
-          for (uint32_t k = 0; k < d[i]; ++k) {
-            const uint32_t c = col[b[i] + k];
-            if (c - row0 >= kTpRows) lcol[b[i] + k] = static_cast<uint16_t>(kTpRows + hv[hash_find(hk, c)]);
+        for (uint32_t i0 = 0; i0 < kHashSlots; i0 += 32) {
+          const uint32_t c = hk[i0 + lane];
+          const uint32_t m = __ballot_sync(0xffffffffu, c != kEmpty);
+          const uint32_t at = H + __popc(m & ((1u << lane) - 1u));
+          if (c != kEmpty && at < 256) uq[at] = c;
+          H += __popc(m);
+        }
+        slow = H > halo_cap;
+        if (!slow) {
+          __syncwarp();
+#pragma unroll
+          for (uint32_t k = 0; k < 8; ++k) hsorted[k] = lane * 8 + k < H ? uq[lane * 8 + k] : kEmpty;
+          __syncwarp();
+          warp_sort256(hsorted, lane);
+#pragma unroll
+          for (uint32_t k = 0; k < 8; ++k)
+            if (lane * 8 + k < H) hv[hash_find(hk, hsorted[k])] = static_cast<uint16_t>(lane * 8 + k);
+          __syncwarp();
+          // pass 2: out-of-tile nonzeros get 128 + their rank; every slot to lcol
+          for (uint32_t k = k0 + lane; k < k1; k += 32) {
+            if ((hdm[k >> 5] >> (k & 31)) & 1u) continue;
+            const uint32_t c = seg[k];
+            uint32_t v;
+            if (c - row0 < kTpRows) v = c - row0;
+            else {
+              v = kTpRows + hv[hash_find(hk, c)];
+              sl[k] = static_cast<uint16_t>(v);
+            }
+            lcol[loff + k] = static_cast<uint16_t>(v);
           }
+          __syncwarp();
         }
       }
     }
@@ -153,15 +203,24 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
 #pragma unroll
       for (int i = 0; i < 4; ++i) lr[32 * i + lane] = static_cast<uint16_t>((b[i] - loff) | (hd[i] ? kTpHdBit : 0u));
       if (lane < kTpLrp - kTpRows) lr[kTpRows + lane] = static_cast<uint16_t>(end - loff);
-      for (uint32_t i = lane; i < ((H + 3u) & ~3u); i += 32) halo[t * kTpHaloCap + i] = uniq[min(i, H - 1)];
-      // row records: the first kTpRecSlots slots of each row (this lane wrote them
-      // above), unused fields -> the zero slot
+      // halo list: sorted element i lives in lane i / 8, register i % 8 (padded to a multiple of 4)
+      const uint32_t hp = (H + 3u) & ~3u;
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t i = lane * 8 + k;
+        if (i < H) halo[t * kTpHaloCap + i] = hsorted[k];
+      }
+      if (H & 3u) {  // padding entries repeat the last row (read, never used)
+        const uint32_t last = __shfl_sync(0xffffffffu, hsorted[(H - 1) & 7], (H - 1) >> 3);
+        for (uint32_t i = H + lane; i < hp; i += 32) halo[t * kTpHaloCap + i] = last;
+      }
+      // row records: the first kTpRecSlots slots of each row, unused fields -> the zero slot
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t f[kTpRecSlots];
 #pragma unroll
         for (uint32_t k = 0; k < kTpRecSlots; ++k)
-          f[k] = (!hd[i] && k < d[i] ? static_cast<uint32_t>(lcol[b[i] + k]) : kTpZeroSlot) << 7;
+          f[k] = (!hd[i] && k < d[i] ? static_cast<uint32_t>(sl[b[i] - loff + k]) : kTpZeroSlot) << 7;
         const uint32_t dl = hd[i] ? 0u : d[i];  // LD degree < thr <= 256
         f[0] |= dl & 0x7Fu;
         f[1] |= (hd[i] ? 1u : 0u) | (dl > kTpRecSlots ? 2u : 0u) | ((dl >> 7) << 2);
