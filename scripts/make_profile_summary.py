@@ -90,7 +90,7 @@ def main(rnd, out, reports):
             per.setdefault(name, []).append((rd or 0) + (wr or 0))
     mean = {k: sum(v) / len(v) for k, v in per.items()}
     scopes = {
-        "l0_keys": ["hd_key_kernel", "l0_key_kernel", "dict_finalize_kernel", "l0_xlat_kernel", "l0_ids_kernel",
+        "l0_keys": ["hd_key_kernel", "l0_key_kernel", "l0_key_tile_kernel", "dict_finalize_kernel", "l0_xlat_kernel", "l0_ids_kernel",
                     "l0_halo_ids_kernel", "l0_hd_ids_kernel"],
         "hd_mean32": ["hd_chunk_kernel", "hd_reduce_kernel"],
         "spmm_mean32": ["spmm_mean32", "hd_chunk_kernel", "hd_reduce_kernel"],
