@@ -5,13 +5,15 @@
 //
 // Per layer l >= 1 (32 -> 32) one persistent, warp-specialised kernel per SM
 // (sage_tile_kernel) walks 128-row tiles with the tile plan of tile_plan.cuh:
-//   loader warp   plan records (row offsets, u16 local neighbour slots, halo
-//                 list) by bulk copy, the tile's 128 feature rows by one TMA box
+//   loader warp   plan records (row records, halo list; row offsets and slot
+//                 list for tiles with rows of degree > 4) by bulk copy, the
+//                 tile's 128 feature rows by one TMA box
 //   copier warps  the tile's halo rows (out-of-tile neighbours) by cp.async,
 //                 into the stage right behind the tile rows
-//   8 producers   per row: neighbour rows from shared memory, sum in nonzero
-//                 order, x 1/deg, TF32 hi/lo split of [h | mean(h_N)] written
-//                 straight into tensor memory (tcgen05.st)
+//   8 producers   per row: one row record (its first four neighbour slots,
+//                 tile_plan.cuh), the neighbour rows from shared memory, sum in
+//                 nonzero order, x 1/deg, TF32 hi/lo split of [h | mean(h_N)]
+//                 written straight into tensor memory (tcgen05.st)
 //   MMA warp      tcgen05.mma kind::tf32, A from TMEM, W from smem, 3 products
 //                 (hi*hi + hi*lo + lo*hi) into a double-buffered accumulator
 //   4 epilogue    tcgen05.ld, + bias, ReLU, 256-bit stores of whole rows (or, in
@@ -21,7 +23,7 @@
 // in L2-ordered chunks with a fixed-order reduction (hd_chunk_kernel).
 // Layer 0 (4 -> 32, inputs in {0,1}^4) is keyed by default: per row an exact
 // integer record, a dictionary of the distinct records, their 4 -> 32 rows and
-// a u8 entry id per row (l0_key_kernel ...); layer 1 then reads entry ids
+// a u8 entry id per row (l0_key_tile_kernel ...); layer 1 then reads entry ids
 // instead of layer-0 rows and, when more layers follow, runs transform-first
 // (kModeXform). Graphs that are not keyable use sage_layer0_kernel.
 #include <cub/cub.cuh>
@@ -248,9 +250,9 @@ constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8
 #define GROOT_ROW_STAGES 4
 #endif
 // Shared-memory plan per variant: staged-row kernels spend it on the row ring,
-// keyed kernels stage no rows (their ring only sequences the copiers' slot
-// rewrite) and hold the entry table. (5 row stages fit only with the plan lead
-// cut to 3 tiles: measured 2 % slower.)
+// keyed kernels stage no rows (no row ring: the copier warps translate the
+// plan's row records into entry-row offsets) and hold the entry tables. (5 row
+// stages fit only with the plan lead cut to 3 tiles: measured 2 % slower.)
 #ifndef GROOT_KEYED_META
 #define GROOT_KEYED_META 8
 #endif
