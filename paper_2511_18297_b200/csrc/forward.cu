@@ -138,6 +138,34 @@ struct HeadW {
 // group; lane j holds features 8j..8j+7 of each) into tensor memory: hi = x with
 // the low 13 mantissa bits cleared (an exact TF32 value), lo = x - hi (exact,
 // Sterbenz). Register 4i+2h+e of the 16x256b store is feature 2i+e of row h.
+__device__ __forceinline__ void split_regs(const float4 (&x)[2][2], uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float f[4] = {x[h][c].x, x[h][c].y, x[h][c].z, x[h][c].w};
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int idx = 4 * (2 * c + p) + 2 * h;  // features 4c+2p, 4c+2p+1
+        const float h0 = __uint_as_float(__float_as_uint(f[2 * p]) & 0xFFFFE000u);
+        const float h1 = __uint_as_float(__float_as_uint(f[2 * p + 1]) & 0xFFFFE000u);
+        const float2 l = ptx::fsub2(make_float2(f[2 * p], f[2 * p + 1]), make_float2(h0, h1));
+        hi[idx] = __float_as_uint(h0);
+        hi[idx + 1] = __float_as_uint(h1);
+        lo[idx] = __float_as_uint(l.x);
+        lo[idx + 1] = __float_as_uint(l.y);
+      }
+    }
+}
+// Both operand halves of a row pair at once: [h | m] hi into columns 0..63, lo
+// into 64..127, two 64-column stores.
+__device__ __forceinline__ void tmem_store_split2(uint32_t taddr, const float4 (&hs)[2][2], const float4 (&mm)[2][2]) {
+  uint32_t hi[32], lo[32];
+  split_regs(hs, reinterpret_cast<uint32_t(&)[16]>(hi[0]), reinterpret_cast<uint32_t(&)[16]>(lo[0]));
+  split_regs(mm, reinterpret_cast<uint32_t(&)[16]>(hi[16]), reinterpret_cast<uint32_t(&)[16]>(lo[16]));
+  ptx::tmem_st_16x256b_x8(taddr, hi);
+  ptx::tmem_st_16x256b_x8(taddr + 64, lo);
+}
 __device__ __forceinline__ void tmem_store_split(uint32_t taddr, const float4 (&x)[2][2]) {
   uint32_t hi[16], lo[16];
 #pragma unroll
@@ -246,6 +274,9 @@ constexpr uint32_t kTkMetaBytes = ((kTkRecOff + kTpRows * 8u + 127u) / 128u) * 1
 constexpr uint32_t kTileRing = 32;     // tile ids of the CTA's iterations (dynamic scheduler)
 constexpr uint32_t kEndTile = 0xFFFFFFFFu;
 constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8)
+#ifndef GROOT_ST_X8
+#define GROOT_ST_X8 1  // producers store [h | m] hi and lo with two 64-column tcgen05.st (x8) instead of four x4
+#endif
 #ifndef GROOT_ROW_STAGES
 #define GROOT_ROW_STAGES 4
 #endif
@@ -828,8 +859,12 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if (kTraceOn) wt3 = clock64();
         ptx::tc_fence_after();
         const uint32_t ta = tmem_base + (lbase << 16) + s * kStageCols;
+#if GROOT_ST_X8
+        tmem_store_split2(ta, hs, mm);  // columns 0..31 / 32..63 (hi: self, mean), 64..95 / 96..127 (lo)
+#else
         tmem_store_split(ta, hs);       // columns 0..31 (hi), 64..95 (lo): self features
         tmem_store_split(ta + 32, mm);  // columns 32..63 (hi), 96..127 (lo): neighbour mean
+#endif
         pend = s;                       // handed over after the next tile's gather
         tstamp(tr, it, 7);
         if (kTraceOn) {
