@@ -212,7 +212,7 @@ struct LayerArgs {
   uint32_t period_rows;       //      and its halo rows shift by (t / period) * period_rows
   uint32_t* tile_counter;     // dynamic tile scheduler (zeroed before the launch); null: static b + i*G
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
-  const float* ktable_self;   // kModeXform: Ts (entry rows . W_self)
+  const float* ktable_self;   // kModeXform: Ts (entry rows . W_self + b)
   const uint32_t* hbimg;      // kModeLast: 4 KB W_out image (hi/lo), K permuted by kcol_feature, N padded to 16
   const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused; tiles x 128), see l0_key_kernel
   const uint8_t* hids;        //                entry ids of the halo rows (tiles x kTpHaloCap, as the halo list)
@@ -840,12 +840,13 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if (kMode == kModeSpmm) {
           if (r < n && !hd[h]) ptx::stg_f8(a.spmm_out + static_cast<size_t>(r) * kF + 8 * j, mm[h][0], mm[h][1]);
         } else if (kXform) {
-          if (r < n) {
-            const float* bj = sBias + 8 * j;
-            const float4 o0 = make_float4(fmaxf((hs[h][0].x + mm[h][0].x) + bj[0], 0.f), fmaxf((hs[h][0].y + mm[h][0].y) + bj[1], 0.f),
-                                          fmaxf((hs[h][0].z + mm[h][0].z) + bj[2], 0.f), fmaxf((hs[h][0].w + mm[h][0].w) + bj[3], 0.f));
-            const float4 o1 = make_float4(fmaxf((hs[h][1].x + mm[h][1].x) + bj[4], 0.f), fmaxf((hs[h][1].y + mm[h][1].y) + bj[5], 0.f),
-                                          fmaxf((hs[h][1].z + mm[h][1].z) + bj[6], 0.f), fmaxf((hs[h][1].w + mm[h][1].w) + bj[7], 0.f));
+          if (r < n) {  // relu(Ts[id] + b + mean Tn): the bias is in the self table (l1_xform_kernel)
+            const float2 s0 = ptx::fadd2(make_float2(hs[h][0].x, hs[h][0].y), make_float2(mm[h][0].x, mm[h][0].y));
+            const float2 s1 = ptx::fadd2(make_float2(hs[h][0].z, hs[h][0].w), make_float2(mm[h][0].z, mm[h][0].w));
+            const float2 s2 = ptx::fadd2(make_float2(hs[h][1].x, hs[h][1].y), make_float2(mm[h][1].x, mm[h][1].y));
+            const float2 s3 = ptx::fadd2(make_float2(hs[h][1].z, hs[h][1].w), make_float2(mm[h][1].z, mm[h][1].w));
+            const float4 o0 = make_float4(fmaxf(s0.x, 0.f), fmaxf(s0.y, 0.f), fmaxf(s1.x, 0.f), fmaxf(s1.y, 0.f));
+            const float4 o1 = make_float4(fmaxf(s2.x, 0.f), fmaxf(s2.y, 0.f), fmaxf(s3.x, 0.f), fmaxf(s3.y, 0.f));
             ptx::stg_f8(a.hout + static_cast<size_t>(r) * kF + 8 * j, o0, o1);
           }
         } else if (r >= n) {
@@ -1641,13 +1642,16 @@ __global__ void __launch_bounds__(256) l0_halo_ids_kernel(uint32_t ntiles, const
 
 // kModeXform tables: Tn[k] = table[k] . W_neigh, Ts[k] = table[k] . W_self
 // (fp64 accumulation, rounded once), CTA per entry, thread per output.
+// Tn = table . W_neigh and Ts = table . W_self + b (the layer bias folded into
+// the self table, so the layer adds one table row to the neighbour mean), fp64.
 __global__ void __launch_bounds__(64) l1_xform_kernel(const float* __restrict__ table, const float* __restrict__ ws,
-                                                      const float* __restrict__ wn, const uint32_t* __restrict__ flags,
-                                                      float* __restrict__ tn, float* __restrict__ ts) {
+                                                      const float* __restrict__ wn, const float* __restrict__ bias,
+                                                      const uint32_t* __restrict__ flags, float* __restrict__ tn,
+                                                      float* __restrict__ ts) {
   const uint32_t k = blockIdx.x, o = threadIdx.x & 31;
   if (flags[0] || k >= flags[1]) return;
   const float* W = threadIdx.x < 32 ? wn : ws;
-  double acc = 0.0;
+  double acc = threadIdx.x < 32 ? 0.0 : static_cast<double>(bias[o]);
   for (uint32_t i = 0; i < kF; ++i) acc = fma(static_cast<double>(table[k * kF + i]), static_cast<double>(W[i * kF + o]), acc);
   (threadIdx.x < 32 ? tn : ts)[k * kF + o] = static_cast<float>(acc);
 }
@@ -2123,7 +2127,8 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
     g->l0_xtab.zero();
     const float* w1 = m->naive_w.p + (2 * m->in_dim * kF + kF);  // layer 1: W_self, W_neigh, b
     ProfScope ps("l1_xform");
-    GROOT_LAUNCH(l1_xform_kernel, kTkTableRows, 64, 0, g->l0_table.p, w1, w1 + kF * kF, g->l0_flags.p, g->l0_xtab.p,
+    GROOT_LAUNCH(l1_xform_kernel, kTkTableRows, 64, 0, g->l0_table.p, w1, w1 + kF * kF, w1 + 2 * kF * kF, g->l0_flags.p,
+                 g->l0_xtab.p,
                  g->l0_xtab.p + kTkTableRows * kF);
   }
   const float* hd_src = xform ? g->l0_xtab.p : hin;  // (xform: HD means of Tn rows)
