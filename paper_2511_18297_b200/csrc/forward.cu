@@ -277,6 +277,9 @@ constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8
 #ifndef GROOT_ST_X8
 #define GROOT_ST_X8 1  // producers store [h | m] hi and lo with two 64-column tcgen05.st (x8) instead of four x4
 #endif
+#ifndef GROOT_XFORM_SELF_PARITY
+#define GROOT_XFORM_SELF_PARITY 1  // transform-first layer: self (Ts) rows in lane-group parity order (-1 %)
+#endif
 #ifndef GROOT_ROW_STAGES
 #define GROOT_ROW_STAGES 4
 #endif
@@ -740,10 +743,18 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         if (kMma || kXform) {
           const uint8_t* sself = kXform ? sTable + kTkTableRows * 128 : sTable;  // Ts, or the entry rows
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // natural half order (no parity swap; rows li, li + 1 share banks: 2-way)
+          for (int h = 0; h < 2; ++h) {
             const uint8_t* rowp = kKeyed ? sself + sp[kTkKidOff + li + 8 * h] * 128u : st + (li + 8 * h) * 128u;
-            hs[h][0] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j);
-            hs[h][1] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j + 16u);
+            if (kXform && GROOT_XFORM_SELF_PARITY) {
+              // lane-group parity order (conflict-free like the neighbour reads), swapped back
+              const float4 f0 = ptx::lds_f4(ptx::smem_addr(rowp) + off0);
+              const float4 f1 = ptx::lds_f4(ptx::smem_addr(rowp) + off1);
+              hs[h][0] = gp ? f1 : f0;
+              hs[h][1] = gp ? f0 : f1;
+            } else {  // natural half order (rows li, li + 1 share banks: 2-way)
+              hs[h][0] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j);
+              hs[h][1] = ptx::lds_f4(ptx::smem_addr(rowp) + 32u * j + 16u);
+            }
           }
         }
         {
