@@ -1416,25 +1416,78 @@ __global__ void __launch_bounds__(256) l0_key_tile_kernel(uint32_t n, const uint
   const int lane = threadIdx.x & 31;
   uint32_t* sF = sF_all[threadIdx.x >> 5];
   const uint32_t ntiles = (n + kTpRows - 1) / kTpRows;
-  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t pt = p.period ? t % p.period : t;
-    const uint32_t shift = p.period ? (t / p.period) * p.period_rows : 0u;
-    const uint4 meta = __ldg(p.tmeta + pt);
+  // The warp's tiles t0, t0 + S, ... go through a three-stage pipeline of
+  // global loads, so a tile's dependent chain (plan meta -> records, features,
+  // halo list -> halo features) is in flight behind the previous tiles' work:
+  //   meta of tile t + 2S | records, tile features, halo list of t + S |
+  //   halo features of t (issued at the end of the previous iteration).
+  constexpr uint32_t kPer = (kTpHaloCap + 31) / 32;  // halo entries per lane
+  const uint32_t S = gridDim.x * (blockDim.x >> 5);
+  struct Stage {
+    uint32_t t;
+    uint4 meta;
+    unsigned long long r[kTpRows / 32];
+    uint4 f;
+    uint32_t h[kPer];  // halo row ids, then their feature words
+  };
+  auto meta_of = [&](uint32_t t) -> uint4 {
+    return t < ntiles ? __ldg(p.tmeta + (p.period ? t % p.period : t)) : make_uint4(0, 0, 0, kTpSlow);
+  };
+  auto load_rows = [&](Stage& st) {  // records, tile features, halo list (needs st.meta)
+    if (st.t >= ntiles || (st.meta.w & kTpSlow)) return;
+    const uint32_t pt = p.period ? st.t % p.period : st.t;
+    const uint32_t row0 = st.t * kTpRows;
+#pragma unroll
+    for (uint32_t i = 0; i < kTpRows / 32; ++i) st.r[i] = __ldg(p.rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
+    if (row0 + kTpRows <= n) {
+      st.f = __ldg(reinterpret_cast<const uint4*>(feat + row0) + lane);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i) w[i] = row0 + 4 * lane + i < n ? __ldg(feat + row0 + 4 * lane + i) : 0u;
+      st.f = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) st.h[u] = lane + 32 * u < st.meta.w ? __ldg(p.halo + st.meta.y + lane + 32 * u) : 0u;
+  };
+  auto load_halo = [&](Stage& st) {  // halo feature words (needs the halo list)
+    if (st.t >= ntiles || (st.meta.w & kTpSlow)) return;
+    const uint32_t shift = p.period ? (st.t / p.period) * p.period_rows : 0u;
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) st.h[u] = lane + 32 * u < st.meta.w ? __ldg(feat + shift + st.h[u]) : 0u;
+  };
+  const uint32_t t0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  Stage cur, nx1;
+  uint4 nx2_meta;
+  cur.t = t0;
+  cur.meta = meta_of(cur.t);
+  load_rows(cur);
+  load_halo(cur);
+  nx1.t = t0 + S;
+  nx1.meta = meta_of(nx1.t);
+  load_rows(nx1);
+  nx2_meta = meta_of(t0 + 2 * S);
+  for (uint32_t t = t0; t < ntiles; t += S) {
+    const uint4 meta = cur.meta;
     const bool slow = (meta.w & kTpSlow) != 0;
     const uint32_t row0 = t * kTpRows;
     unsigned long long r[kTpRows / 32];
     if (!slow) {
 #pragma unroll
-      for (uint32_t i = 0; i < kTpRows / 32; ++i) r[i] = __ldg(p.rec + static_cast<size_t>(pt) * kTpRows + 32 * i + lane);
-      if (row0 + kTpRows <= n) {
-        reinterpret_cast<uint4*>(sF)[lane] = __ldg(reinterpret_cast<const uint4*>(feat + row0) + lane);
-      } else {
+      for (uint32_t i = 0; i < kTpRows / 32; ++i) r[i] = cur.r[i];
+      reinterpret_cast<uint4*>(sF)[lane] = cur.f;
 #pragma unroll
-        for (uint32_t i = 0; i < 4; ++i) sF[4 * lane + i] = row0 + 4 * lane + i < n ? __ldg(feat + row0 + 4 * lane + i) : 0u;
-      }
-      for (uint32_t i = lane; i < meta.w; i += 32) sF[kTpRows + i] = __ldg(feat + shift + __ldg(p.halo + meta.y + i));
+      for (uint32_t u = 0; u < kPer; ++u)
+        if (lane + 32 * u < meta.w) sF[kTpRows + lane + 32 * u] = cur.h[u];
       if (lane == 0) sF[kTpZeroSlot] = 0u;
     }
+    // advance the pipeline: the next tiles' loads go out before this tile's work
+    cur = nx1;
+    load_halo(cur);
+    nx1.t = t + 2 * S;
+    nx1.meta = nx2_meta;
+    load_rows(nx1);
+    nx2_meta = meta_of(t + 3 * S);
     __syncwarp();
 #pragma unroll
     for (uint32_t i = 0; i < kTpRows / 32; ++i) {

@@ -1,15 +1,16 @@
 """Per-role breakdown of one kernel's ncu source page (SASS): instructions
 executed per tile and warp-stall samples, by execution-count class.
 
-usage: python scripts/sass_regions.py REPORT KERNEL_INDEX TILES [listing.txt]
-(KERNEL_INDEX counts launches of regex 'sage_tile' in the report, from 1.)
+usage: python scripts/sass_regions.py REPORT KERNEL_INDEX TILES [listing.txt] [kernel regex, default sage_tile]
+(KERNEL_INDEX counts launches matching the regex in the report, from 1.)
 """
 import csv, io, subprocess, sys
 from collections import defaultdict
 
 rep, k, T = sys.argv[1], sys.argv[2], float(sys.argv[3])
+kre = sys.argv[5] if len(sys.argv) > 5 else "sage_tile"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                      "--kernel-id", f"::regex:sage_tile:{k}"], capture_output=True, text=True).stdout
+                      "--kernel-id", f"::regex:{kre}:{k}"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 data = []
