@@ -94,6 +94,14 @@ class Aig {
     if (driver.node >= num_nodes()) throw std::invalid_argument("Aig::add_output: driver references unknown node");
     outputs_.push_back(driver);
   }
+  // Flips the inversion flag of one fanin of an AND node (inc/aig.hpp:57, src/aig.cpp:24-29):
+  // the verifier's mutated-multiplier tests.
+  void flip_and_fanin(std::uint32_t node, bool right_side) {
+    if (!is_and(node)) throw std::invalid_argument("Aig::flip_and_fanin: not an AND node");
+    AndNode& a = ands_[node - first_and()];
+    Literal& l = right_side ? a.right : a.left;
+    l.inverted = !l.inverted;
+  }
   // Flat AIGER literal arrays for the C ABI.
   std::vector<std::uint32_t> and_lits() const {
     std::vector<std::uint32_t> v(2 * ands_.size());
@@ -144,6 +152,12 @@ inline void write_aiger(const Aig& g, std::ostream& out) {  // src/aig.cpp:96-11
   for (const Literal& d : g.outputs()) out << encode_lit(d) << '\n';
   for (std::uint32_t n = 0; n < a; ++n)
     out << 2 * (i + 1 + n) << ' ' << encode_lit(g.and_nodes()[n].left) << ' ' << encode_lit(g.and_nodes()[n].right) << '\n';
+}
+
+inline void write_aiger_file(const Aig& g, const std::string& path) {  // inc/aig.hpp:73, src/aig.cpp:109-113
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write AIGER file: " + path);
+  write_aiger(g, out);
 }
 
 // ---- inc/circuitgen.hpp ---------------------------------------------------------

@@ -5,7 +5,9 @@
 #include <cassert>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <sstream>
 
 #include "groot_aigsage.hpp"
@@ -38,6 +40,42 @@ int main(int argc, char** argv) {
     parse_aiger(bad);
   } catch (const std::runtime_error& e) {
     threw = std::string(e.what()).find("latches unsupported") != std::string::npos;
+  }
+  CHECK(threw);
+  // file forms (inc/aig.hpp:73, inc/circuitgen.hpp): AIGER, labels, supports round trips
+  const std::string tmp = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") + "/groot_api_" +
+                          std::to_string(static_cast<long>(std::time(nullptr)) % 100000);
+  write_aiger_file(c.aig, tmp + ".aag");
+  CHECK(parse_aiger_file(tmp + ".aag") == c.aig);
+  write_labels(tmp + ".lab", c.gt.labels);
+  CHECK(load_labels(tmp + ".lab", c.gt.labels.size()) == c.gt.labels);
+  threw = false;
+  try {
+    load_labels(tmp + ".lab", c.gt.labels.size() + 1);  // node 19 missing
+  } catch (const std::runtime_error& e) {
+    threw = std::string(e.what()).find("missing node 19") != std::string::npos;
+  }
+  CHECK(threw);
+  CsaCircuit c4 = gen_csa_multiplier(4);
+  CHECK(!c4.gt.supports.empty());
+  write_supports(tmp + ".sup", c4.gt.supports);
+  CHECK(load_supports(tmp + ".sup") == c4.gt.supports);
+  std::remove((tmp + ".aag").c_str());
+  std::remove((tmp + ".lab").c_str());
+  std::remove((tmp + ".sup").c_str());
+  // flip_and_fanin (src/aig.cpp:24-29): toggles one fanin's inversion, twice restores
+  Aig flipped = c.aig;
+  const std::uint32_t v = flipped.first_and() + 3;
+  flipped.flip_and_fanin(v, true);
+  CHECK(flipped.and_node(v).right.inverted != c.aig.and_node(v).right.inverted &&
+        flipped.and_node(v).left == c.aig.and_node(v).left && !(flipped == c.aig));
+  flipped.flip_and_fanin(v, true);
+  CHECK(flipped == c.aig);
+  threw = false;
+  try {
+    flipped.flip_and_fanin(1, false);  // an input, not an AND node
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()) == "Aig::flip_and_fanin: not an AND node";
   }
   CHECK(threw);
   threw = false;
