@@ -59,16 +59,20 @@ __global__ void encode_kernel(uint32_t ni, uint32_t na, const uint32_t* __restri
     if (v > ni && v < nodes) {
       const uint32_t a = v - 1 - ni;
       const uint2 lr = reinterpret_cast<const uint2*>(ands)[a];
-      if ((lr.x >> 1) >= v || (lr.y >> 1) >= v) atomicMin(bad, v);
+      const bool ok = (lr.x >> 1) < v && (lr.y >> 1) < v;
+      if (!ok) atomicMin(bad, v);
       f = 0x0101u | ((lr.x & 1u) << 16) | ((lr.y & 1u) << 24);
-      edges[2 * a] = make_uint2(lr.x >> 1, v);
-      edges[2 * a + 1] = make_uint2(lr.y >> 1, v);
+      // (an invalid fanin is reported after the CSR build; its edges point at
+      // node 0 meanwhile so the build stays in bounds)
+      edges[2 * a] = make_uint2(ok ? lr.x >> 1 : 0u, v);
+      edges[2 * a + 1] = make_uint2(ok ? lr.y >> 1 : 0u, v);
     } else if (v >= nodes) {
       const uint32_t k = v - nodes;
       const uint32_t d = outs[k];
-      if ((d >> 1) >= nodes) atomicMin(bad, v);
+      const bool ok = (d >> 1) < nodes;
+      if (!ok) atomicMin(bad, v);
       f = ((d & 1u) << 8) | 0x01010000u;
-      edges[2ull * na + k] = make_uint2(d >> 1, v);
+      edges[2ull * na + k] = make_uint2(ok ? d >> 1 : 0u, v);
     }
     feat[v] = f;
   }
@@ -524,11 +528,14 @@ groot_graph* encode(uint32_t ni, uint32_t na, const uint32_t* h_ands, uint32_t n
     const auto t1 = now();
     GROOT_LAUNCH(encode_kernel, blocks_for(n, 256), 256, 0, ni, na, ands.p, no, outs.p,
                  reinterpret_cast<uint32_t*>(g->feat.p), reinterpret_cast<uint2*>(g->edges.p), bad.p);
-    const uint32_t b = read_scalar(bad.p);
-    if (b != none) fail(GROOT_EINVAL, "Aig::add_and: fanin index must be strictly below the new node");
     const auto t2 = now();
     build_csr(n, ne, g->edges.p, g->rp.p, g->col.p);
+    uint32_t b = none;  // the validity flag, read with the build's final synchronisation
+    bad.download(&b, 1);
     stream_sync();
+    if (b != none)  // the first offending node: an AND node's fanin, or an output's driver (src/aig.cpp:10-22)
+      fail(GROOT_EINVAL, b < 1ull + ni + na ? "Aig::add_and: fanin index must be strictly below the new node"
+                                            : "Aig::add_output: driver references unknown node");
     if (host_timing)
       std::fprintf(stderr, "[encode] upload %.2f ms, encode %.2f ms, csr %.2f ms\n", ms(t0, t1), ms(t1, t2),
                    ms(t2, now()));

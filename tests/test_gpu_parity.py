@@ -517,3 +517,22 @@ def test_exact_halo_mode_device(api, circuit, width, k):
     for r in range(k):
         got[parts[r].core_nodes] = hs[r][: plans[r].num_core].cpu().numpy()
     check_logits(got, ref, f"mode X {circuit}{width} k{k}")
+
+
+def test_encode_rejects_bad_fanins(api):
+    """encode's device validation (src/aig.cpp:10-16 semantics): a fanin at or
+    above its AND node, or an output driver past the last node, is rejected
+    with the reference's message after an in-bounds CSR build; a valid AIG
+    encoded right after still matches the oracle."""
+    from paper_2511_18297_b200._lib import GrootInvalidArgument
+    ands = np.array([[2, 4], [6, 12]], np.uint32)  # node 4 = AND(1, 2); node 5 = AND(3, node 6: forward reference)
+    with pytest.raises(GrootInvalidArgument, match="fanin index must be strictly below the new node"):
+        api.encode(api.Aig(3, ands, np.array([10], np.uint32)))
+    ands_ok = np.array([[2, 4], [6, 8]], np.uint32)
+    with pytest.raises(GrootInvalidArgument, match="driver references unknown node"):
+        api.encode(api.Aig(3, ands_ok, np.array([40], np.uint32)))  # output driver 20 > last node
+    c = api.gen_csa_multiplier(8)
+    got = api.encode(c.aig, c.labels).copy_out()
+    ref = O.encode(O.gen_csa(8))
+    for f in ("row_ptr", "col_idx", "features", "fwd_edges"):
+        assert np.array_equal(got[f], getattr(ref, f)), f
