@@ -1914,7 +1914,7 @@ void classify_rows(groot_graph* g, uint32_t thr) {
     GROOT_CUDA(cudaMemcpyAsync(g->hd_rows.p, out.p, num * 4ull, cudaMemcpyDeviceToDevice, stream()));
   g->hd_mean.alloc(static_cast<size_t>(num) * kF);
   g->hd_threshold = thr;
-  stream_sync();
+  // (no synchronisation: the temporaries return to the stream-ordered pool)
 }
 
 void build_tile_plan(groot_graph* g, uint32_t thr);
@@ -1967,7 +1967,6 @@ static void build_hd_plan(groot_graph* g) {
                                              stream()));
   g->hdp_partial.alloc(static_cast<size_t>(nunits) * kF);
   g->hdp_nunits = nunits;
-  stream_sync();
   g->hdp_valid = true;
 }
 

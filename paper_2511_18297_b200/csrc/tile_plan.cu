@@ -261,9 +261,7 @@ void build_tile_plan(groot_graph* g, uint32_t thr) {
   const unsigned grid = std::min<uint32_t>((ntiles + kTpWarps - 1) / kTpWarps, static_cast<uint32_t>(num_sms()) * 16u);
   GROOT_LAUNCH(tile_plan_kernel, grid, kTpWarps * 32, 0, n, g->rp.p, g->col.p, thr, cap,
                reinterpret_cast<TileMeta*>(g->tp_meta.p), g->tp_lrp.p, g->tp_lcol.p, g->tp_halo.p, g->tp_rec.p, slow.p);
-  slow.download(&g->tp_slow, 1);
-  stream_sync();
-  g->tp_threshold = thr;
+  g->tp_threshold = thr;  // (the slow-tile count stays on the device: no host synchronisation)
   g->tp_halo_cap = cap;
 }
 
