@@ -283,6 +283,9 @@ constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8
 #ifndef GROOT_ROW_STAGES
 #define GROOT_ROW_STAGES 4
 #endif
+#ifndef GROOT_LAST_PIPE
+#define GROOT_LAST_PIPE 1  // last layer: head of tile i drained behind the split of tile i + 1
+#endif
 // Shared-memory plan per variant: staged-row kernels spend it on the row ring,
 // keyed kernels stage no rows (no row ring: the copier warps translate the
 // plan's row records into entry-row offsets) and hold the entry tables. (5 row
@@ -601,12 +604,9 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     // stay in uniform registers), one elected lane issues =====
     constexpr uint32_t idesc = ptx::idesc_tf32<kTileM, kF>();
     const uint32_t b0s = ptx::smem_addr(sB);
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      const uint32_t acc = kAccBufs == 2 ? (it & 1) : 0u, aph = kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1);
-      if (kMode == kModeLast && it > 0) {
-        // the previous tile's 32 -> classes head, once the epilogue has put its
-        // A operand (relu(acc + b) split into TF32 hi / lo) into TMEM
+    // the previous tile's 32 -> classes head, once the epilogue has put its A
+    // operand (relu(acc + b) split into TF32 hi / lo) into TMEM
+    auto issue_head = [&](uint32_t it) {
         ptx::mbar_wait(hready, (it - 1) & 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
@@ -623,11 +623,19 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           ptx::mma_commit(hdone);
         }
         __syncwarp();
-      }
+    };
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+      const uint32_t acc = kAccBufs == 2 ? (it & 1) : 0u, aph = kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1);
+      // GROOT_LAST_PIPE: tile it's layer MMAs go first (the accumulator is free
+      // once the epilogue has loaded tile it-1), the head of it-1 after them,
+      // while the epilogue works on the split
+      if (kMode == kModeLast && !GROOT_LAST_PIPE && it > 0) issue_head(it);
       ptx::mbar_wait(&full[s], ph);
       if (lane == 0) tstamp(a.trace, it, 8);
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
       if (sTile[it % kTileRing] == kEndTile) {  // producers' end hand-over: wake the epilogue and stop
+        if (kMode == kModeLast && GROOT_LAST_PIPE && it > 0) issue_head(it);
         if (lane == 0) ptx::mbar_arrive(&tfull[acc]);
         break;
       }
@@ -652,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         ptx::mma_commit(&tfull[acc]);
       }
       __syncwarp();
+      if (kMode == kModeLast && GROOT_LAST_PIPE && it > 0) issue_head(it);
       if (lane == 0) tstamp(a.trace, it, 10);
     }
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
@@ -899,12 +908,36 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
     float b8[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) b8[k] = sBias[8 * j + k];
+    // last layer: each lane's row's logits -> first maximum (and the logits)
+    auto head_out = [&](uint32_t row, const float (&lg)[8]) {
+      float best = 0.f;
+      uint32_t arg = 0;
+#pragma unroll
+      for (int cl = 0; cl < kMaxClasses; ++cl) {
+        if (cl < static_cast<int>(a.classes)) {
+          const float sc = lg[cl] + hw.b[cl];
+          if (cl == 0 || sc > best) { best = sc; arg = cl; }
+          if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + cl] = sc;
+        }
+      }
+      if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
+    };
+    uint32_t prev_row = 0;  // GROOT_LAST_PIPE: this lane's row of the tile whose head is in flight
     for (uint32_t e = 0;; ++e) {
       const uint32_t acc = kAccBufs == 2 ? (e & 1) : 0u, ph = kAccBufs == 2 ? ((e >> 1) & 1) : (e & 1);
       if (GROOT_EPI_POLL_NS) ptx::mbar_wait_poll(&tfull[acc], ph, GROOT_EPI_POLL_NS);
       else ptx::mbar_wait_sleep(&tfull[acc], ph, 200);
       const uint32_t t = sTile[e % kTileRing];
-      if (t == kEndTile) break;
+      if (t == kEndTile) {
+        if (kMode == kModeLast && GROOT_LAST_PIPE && e > 0) {  // the last tile's head
+          ptx::mbar_wait(hdone, (e - 1) & 1);
+          ptx::tc_fence_after();
+          float lg[8];
+          ptx::tmem_ld_32x32b_x8(tmem_base + kHeadDCol + ((q * 32u) << 16), lg);
+          head_out(prev_row, lg);
+        }
+        break;
+      }
       if (warp == 0 && lane == 0) tstamp(a.trace, e, 11);
       ptx::tc_fence_after();
       const uint32_t tq = tmem_base + kAccCol0 + acc * kAccCols + ((q * 32u) << 16);
@@ -955,6 +988,23 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           lo[c] = __float_as_uint(l.x);
           lo[c + 1] = __float_as_uint(l.y);
         }
+#if GROOT_LAST_PIPE
+        // the previous tile's logits leave the head's columns before this tile's
+        // head A operand is published (its MMA overwrites them)
+        float lg[8];
+        if (e > 0) {
+          ptx::mbar_wait(hdone, (e - 1) & 1);
+          ptx::tc_fence_after();
+          ptx::tmem_ld_32x32b_x8(tmem_base + kHeadDCol + ((q * 32u) << 16), lg);
+        }
+        ptx::tmem_st_32x32b_x32(tmem_base + kHeadHiCol + ((q * 32u) << 16), hi);
+        ptx::tmem_st_32x32b_x32(tmem_base + kHeadLoCol + ((q * 32u) << 16), lo);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(hready);
+        if (e > 0) head_out(prev_row, lg);
+        prev_row = row0 + lane;
+#else
         ptx::tmem_st_32x32b_x32(tmem_base + kHeadHiCol + ((q * 32u) << 16), hi);
         ptx::tmem_st_32x32b_x32(tmem_base + kHeadLoCol + ((q * 32u) << 16), lo);
         ptx::tmem_wait_st();
@@ -977,6 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
           }
         }
         if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
+#endif
       }
       if (warp == 0 && lane == 0) tstamp(a.trace, e, 12);
     }
