@@ -62,16 +62,40 @@ constexpr uint32_t kTmemCols = 512;
 static_assert(kAccCol0 + 2 * kAccCols <= kTmemCols, "tensor memory budget");
 constexpr uint32_t kBBytes = 4 * 4096;            // W_self hi/lo, W_neigh hi/lo (32 x 32 each)
 constexpr int kMaxClasses = 8;
-// Last layer: the 32 -> classes head runs on the tensor core too. The last
-// layer keeps ONE accumulator (the epilogue frees it right after loading it)
-// and uses the second accumulator's columns for the head's A operand: the
-// epilogue writes relu(acc + b) split into TF32 hi (kHeadHiCol) and lo
-// (kHeadLoCol); one MMA group of N = 16 (classes zero-padded) leaves the
-// logits in kHeadDCol.
+// Last layer: the 32 -> classes head runs on the tensor core too: the epilogue
+// writes its A operand into TMEM (kHeadHiCol), one MMA group of N = 16
+// (classes zero-padded) leaves the logits in kHeadDCol. Without the certified
+// head (GROOT_HEAD_CERT=0) the A operand is relu(acc + b) split into TF32 hi
+// and lo (kHeadLoCol), and the last layer keeps ONE accumulator (freed right
+// after the epilogue loads it) to make room.
 constexpr uint32_t kHeadN = 16;
-constexpr uint32_t kHeadHiCol = kAccCol0 + kAccCols;      // 416 (the unused second accumulator)
-constexpr uint32_t kHeadLoCol = kAccCol0 + 2 * kAccCols;  // 448
-constexpr uint32_t kHeadDCol = kHeadLoCol + kAccCols;     // 480
+// Last layer, classes only (no logits requested): certified single-operand head.
+// The epilogue stores relu(acc + b) once (no TF32 hi/lo split); the head MMA
+// forms x.W (W hi + lo) and, in columns 8.., S_c = x.|W_c|, with x taken at
+// TF32 by the tensor core (|x - tf32(x)| <= 2^-10 tf32(x)), so every logit is
+// within 2^-10 S_c of x.W. A row whose top-2 margin exceeds the two bounds has
+// the class of the exact logits; any other row (and every row when logits are
+// requested) recomputes its head in fp32 FFMA from x in registers.
+#ifndef GROOT_HEAD_CERT
+#define GROOT_HEAD_CERT 1
+#endif
+#ifndef GROOT_LAST_PIPE
+#define GROOT_LAST_PIPE (!GROOT_HEAD_CERT)  // last layer: head of tile i drained behind the split of tile i + 1
+#endif
+// GROOT_LAST_ACC2 (certified head only): its A operand needs 32 columns, not
+// 64, so the last layer can keep both accumulators (head A at 448, logits at
+// 480) with the MMA warp issuing tile i's head after tile i + 1's layer MMAs.
+// Measured +1.5 % against one accumulator (two A/B pairs), so off.
+#ifndef GROOT_LAST_ACC2
+#define GROOT_LAST_ACC2 0
+#endif
+static_assert(!(GROOT_HEAD_CERT && GROOT_LAST_PIPE), "the certified head keeps its row's x in registers");
+static_assert(!GROOT_LAST_ACC2 || GROOT_HEAD_CERT, "two accumulators leave room for the certified head only");
+// the MMA warp issues tile i's head after tile i + 1's layer MMAs
+#define GROOT_HEAD_AFTER_MMA (GROOT_LAST_PIPE || GROOT_LAST_ACC2)
+constexpr uint32_t kHeadHiCol = kAccCol0 + (GROOT_LAST_ACC2 ? 2 : 1) * kAccCols;  // 448 (ACC2) / 416 (the unused second accumulator)
+constexpr uint32_t kHeadLoCol = kAccCol0 + 2 * kAccCols;  // 448 (not with the certified head)
+constexpr uint32_t kHeadDCol = kAccCol0 + 3 * kAccCols;   // 480
 static_assert(kHeadDCol + kHeadN <= kTmemCols, "tensor memory budget (head)");
 constexpr uint32_t kHeadBBytes = 2 * kHeadN * 128;        // W_out hi/lo, K-major SW128, N = 16 rows
 // Column c (0..31) of an A block in tensor memory holds input feature
@@ -214,6 +238,7 @@ struct LayerArgs {
   uint32_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
   const float* ktable_self;   // kModeXform: Ts (entry rows . W_self + b)
   const uint32_t* hbimg;      // kModeLast: 4 KB W_out image (hi/lo), K permuted by kcol_feature, N padded to 16
+  float head_cert;            // kModeLast, GROOT_HEAD_CERT: scale of the margin bound (1; huge = every row exact)
   const uint8_t* keys;        // keyed layer 1: u8 entry id per row (hin unused; tiles x 128), see l0_key_kernel
   const uint8_t* hids;        //                entry ids of the halo rows (tiles x kTpHaloCap, as the halo list)
   const float* ktable;        //                kTkTableRows x 32 rows of the entries
@@ -283,9 +308,7 @@ constexpr uint32_t kTkTableRows = 256;  // keyed layer 1: entry rows (ids are u8
 #ifndef GROOT_ROW_STAGES
 #define GROOT_ROW_STAGES 4
 #endif
-#ifndef GROOT_LAST_PIPE
-#define GROOT_LAST_PIPE 1  // last layer: head of tile i drained behind the split of tile i + 1
-#endif
+
 // Shared-memory plan per variant: staged-row kernels spend it on the row ring,
 // keyed kernels stage no rows (no row ring: the copier warps translate the
 // plan's row records into entry-row offsets) and hold the entry tables. (5 row
@@ -336,7 +359,7 @@ template <int kMode, bool kKeyed = false>
 __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs a, const HeadW hw,
                                                                 const __grid_constant__ CUtensorMap tmap_in) {
   constexpr bool kMma = kMode == kModeLayer || kMode == kModeLast;
-  constexpr uint32_t kAccBufs = kMode == kModeLast ? 1u : 2u;  // last layer: see kHeadHiCol
+  constexpr uint32_t kAccBufs = kMode == kModeLast && !GROOT_LAST_ACC2 ? 1u : 2u;  // last layer: see kHeadHiCol
   constexpr bool kXform = kMode == kModeXform;
   static_assert(!kXform || kKeyed, "transform-first mode reads the entry tables");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -618,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
             const uint64_t bhi = ptx::umma_desc_sw128(hb + kk * 32), blo = ptx::umma_desc_sw128(hb + kHeadN * 128 + kk * 32);
             ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, bhi, hdesc, kk != 0);
             ptx::mma_tf32_ts(tmem_base + kHeadDCol, ahi + kk * 8, blo, hdesc, 1);
-            ptx::mma_tf32_ts(tmem_base + kHeadDCol, alo + kk * 8, bhi, hdesc, 1);
+            if (!GROOT_HEAD_CERT) ptx::mma_tf32_ts(tmem_base + kHeadDCol, alo + kk * 8, bhi, hdesc, 1);
           }
           ptx::mma_commit(hdone);
         }
@@ -630,12 +653,12 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
       // GROOT_LAST_PIPE: tile it's layer MMAs go first (the accumulator is free
       // once the epilogue has loaded tile it-1), the head of it-1 after them,
       // while the epilogue works on the split
-      if (kMode == kModeLast && !GROOT_LAST_PIPE && it > 0) issue_head(it);
+      if (kMode == kModeLast && !GROOT_HEAD_AFTER_MMA && it > 0) issue_head(it);
       ptx::mbar_wait(&full[s], ph);
       if (lane == 0) tstamp(a.trace, it, 8);
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
       if (sTile[it % kTileRing] == kEndTile) {  // producers' end hand-over: wake the epilogue and stop
-        if (kMode == kModeLast && GROOT_LAST_PIPE && it > 0) issue_head(it);
+        if (kMode == kModeLast && GROOT_HEAD_AFTER_MMA && it > 0) issue_head(it);
         if (lane == 0) ptx::mbar_arrive(&tfull[acc]);
         break;
       }
@@ -660,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         ptx::mma_commit(&tfull[acc]);
       }
       __syncwarp();
-      if (kMode == kModeLast && GROOT_LAST_PIPE && it > 0) issue_head(it);
+      if (kMode == kModeLast && GROOT_HEAD_AFTER_MMA && it > 0) issue_head(it);
       if (lane == 0) tstamp(a.trace, it, 10);
     }
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
@@ -976,6 +999,69 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         ptx::tmem_ld_32x32b_x32(tq, r);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
+#if GROOT_HEAD_CERT
+        float x[32];
+        uint32_t xs[32];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {  // column c holds output feature kcol_feature(c); pairs: FADD2
+          const float2 z = ptx::fadd2(make_float2(r[c], r[c + 1]),
+                                      make_float2(hw.bias[kcol_feature(c)], hw.bias[kcol_feature(c + 1)]));
+          x[c] = fmaxf(z.x, 0.0f);
+          x[c + 1] = fmaxf(z.y, 0.0f);
+          xs[c] = __float_as_uint(x[c]);
+          xs[c + 1] = __float_as_uint(x[c + 1]);
+        }
+        ptx::tmem_st_32x32b_x32(tmem_base + kHeadHiCol + ((q * 32u) << 16), xs);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(hready);  // the MMA warp issues the head
+        ptx::mbar_wait(hdone, e & 1);
+        ptx::tc_fence_after();
+        float lg[16];
+        ptx::tmem_ld_32x32b_x16(tmem_base + kHeadDCol + ((q * 32u) << 16), lg);
+        const uint32_t row = row0 + lane;
+        float best = 0.f, second = -INFINITY, smax = 0.f;
+        uint32_t arg = 0;
+#pragma unroll
+        for (int cl = 0; cl < kMaxClasses; ++cl) {
+          if (cl < static_cast<int>(a.classes)) {
+            const float sc = lg[cl] + hw.b[cl];
+            smax = fmaxf(smax, lg[8 + cl]);
+            if (cl == 0) {
+              best = sc;
+            } else if (sc > best) {
+              second = fmaxf(second, best);
+              best = sc;
+              arg = cl;
+            } else {
+              second = fmaxf(second, sc);
+            }
+          }
+        }
+        // |logit - x.W| <= 2^-10 S_c (operand) + accumulation; margin must beat both bounds
+        const float bound =
+            a.head_cert * (smax * (2.0f * 1.125f / 1024.0f) + 1e-6f * (fabsf(best) + fabsf(second)) + 1e-30f);
+        if (a.logits || !(best - second > bound)) {  // exact fp32 head from x (rare without logits)
+          float l[kMaxClasses];
+#pragma unroll
+          for (int cl = 0; cl < kMaxClasses; ++cl) l[cl] = hw.b[cl];
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+#pragma unroll
+            for (int cl = 0; cl < kMaxClasses; ++cl)
+              if (cl < static_cast<int>(a.classes)) l[cl] = fmaf(x[c], hw.w[kcol_feature(c)][cl], l[cl]);
+          best = l[0];
+          arg = 0;
+#pragma unroll
+          for (int cl = 0; cl < kMaxClasses; ++cl) {
+            if (cl < static_cast<int>(a.classes)) {
+              if (cl > 0 && l[cl] > best) { best = l[cl]; arg = cl; }
+              if (a.logits && row < n) a.logits[static_cast<size_t>(row) * a.classes + cl] = l[cl];
+            }
+          }
+        }
+        if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
+#else
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {  // column c holds output feature kcol_feature(c); pairs: FADD2
@@ -1028,6 +1114,7 @@ __global__ void __launch_bounds__(kThreads, 1) sage_tile_kernel(const LayerArgs 
         }
         if (row < n) a.cls[row] = static_cast<uint8_t>(arg);
 #endif
+#endif  // GROOT_HEAD_CERT
       }
       if (warp == 0 && lane == 0) tstamp(a.trace, e, 12);
     }
@@ -2262,6 +2349,10 @@ void layer_device(const groot_model* m, groot_graph* g, uint32_t l, const float*
   a.hout = hout;
   a.bimg = m->bimg.p + static_cast<size_t>(l - 1) * (kBBytes / 4);
   a.hbimg = m->hbimg.p;
+  {
+    const char* hc = std::getenv("GROOT_HEAD_CERT_SCALE");  // test knob: route rows to the exact head
+    a.head_cert = hc ? static_cast<float>(std::atof(hc)) : 1.0f;
+  }
   a.classes = m->classes;
   a.cls = cls;
   a.logits = logits;
@@ -2577,7 +2668,9 @@ void model_upload(groot_model* m) {
   std::vector<uint32_t> himg(kHeadBBytes / 4, 0);
   for (uint32_t nn = 0; nn < kHeadN; ++nn)
     for (uint32_t k = 0; k < 32; ++k) {
-      const float v = nn < C ? head[kcol_feature(k) * C + nn] : 0.0f;
+      // rows 8 + c: |W_c| (the certified head's bound sums, GROOT_HEAD_CERT)
+      const float v = nn < C ? head[kcol_feature(k) * C + nn]
+                             : (nn >= 8 && nn - 8 < C ? std::fabs(head[kcol_feature(k) * C + nn - 8]) : 0.0f);
       const float hi = tf32_rna_host(v), lo = v - hi;
       const uint32_t o = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
       std::memcpy(reinterpret_cast<uint8_t*>(himg.data()) + o, &hi, 4);

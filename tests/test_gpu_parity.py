@@ -536,3 +536,46 @@ def test_encode_rejects_bad_fanins(api):
     ref = O.encode(O.gen_csa(8))
     for f in ("row_ptr", "col_idx", "features", "fwd_edges"):
         assert np.array_equal(got[f], getattr(ref, f)), f
+
+
+@pytest.mark.parametrize("width,copies,trained", [(64, 2, True), (256, 1, False), (64, 1, False)])
+def test_certified_head(api, golden_dir, width, copies, trained):
+    """Last layer without logits (GROOT_HEAD_CERT): classes from the single-operand
+    tensor-core head where its margin bound certifies them, the exact fp32 head
+    elsewhere. Default, all-exact (bound scale 1e30) and the oracle must agree
+    off fp64 near-ties; with logits requested every row takes the exact head."""
+    from helpers import near_ties, with_env
+    g = dev_graph(api, width, copies)
+    h = ora_graph(width, copies)
+    prm = trained_params(golden_dir) if trained else O.init_model(5)
+    model = api.Model.from_params(prm)
+    ref = O.forward(h, prm)
+    dflt = api.predict_full(model, g)
+    exact = with_env("GROOT_HEAD_CERT_SCALE", "1e30", lambda: api.predict_full(model, g))
+    check_classes(dflt.labels, ref, "certified head")
+    check_classes(exact.labels, ref, "exact head")
+    assert_same = (dflt.labels != exact.labels) & ~near_ties(ref)
+    assert not assert_same.any()
+    check_logits(api.forward(model, g), ref, "logits (exact head)")
+
+
+def test_certified_head_ties_take_first_max(api):
+    """Two identical class columns: their logits tie exactly, the margin test
+    fails, the exact head keeps the first maximum (class 0, never class 1),
+    as Eigen's maxCoeff in the reference (src/gnn.cpp:293-300)."""
+    g = dev_graph(api, 64, 2)
+    h = ora_graph(64, 2)
+    prm = O.init_model(7).copy()
+    wo = prm.shape[0] - (32 * 5 + 5)
+    W = prm[wo:wo + 160].reshape(32, 5)
+    W[:, 1] = W[:, 0]
+    prm[wo + 160 + 1] = prm[wo + 160]
+    model = api.Model.from_params(prm)
+    ref = O.forward(h, prm)
+    pred = api.predict_full(model, g)
+    from helpers import near_ties
+    assert not (pred.labels == 1).any()
+    check_classes(pred.labels, ref, "tied columns")
+    sure = (np.argmax(ref, axis=1) == 0) & ~near_ties(np.delete(ref, 1, axis=1))
+    assert sure.sum() > 0
+    assert (pred.labels[sure] == 0).all()
