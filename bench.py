@@ -67,6 +67,20 @@ def parse():
 # ---------------------------------------------------------------------------
 # helpers
 # ---------------------------------------------------------------------------
+def init_nccl(local, world):
+    """One NCCL communicator over all ranks; NCCL's INIT log (stderr) stays on so
+    the communicator's nranks and transport can be checked from the run log."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()} on cuda:{local} "
+          f"({torch.cuda.get_device_name(local)}), NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}",
+          file=sys.stderr, flush=True)
+    assert dist.get_world_size() == world
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -262,7 +276,7 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_nccl(local, world)
     from paper_2511_18297_b200 import api
     from paper_2511_18297_b200._lib import check, lib
     import ctypes as C
@@ -607,7 +621,7 @@ def run_halo(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_nccl(local, world)
     stream = torch.cuda.current_stream()
     api.set_stream(stream.cuda_stream)
     circ = (api.gen_booth_multiplier if args.circuit == "booth" else api.gen_csa_multiplier)(args.width)
