@@ -1539,7 +1539,12 @@ struct L0KeyPlan {
   uint32_t period, period_rows;
 };
 
-__global__ void __launch_bounds__(256) l0_key_tile_kernel(uint32_t n, const uint32_t* __restrict__ rp,
+#ifdef GROOT_L0_KEY_MINB  // experiment knob: min CTAs per SM (register cap) of the key pass
+#define GROOT_L0_KEY_BOUNDS __launch_bounds__(256, GROOT_L0_KEY_MINB)
+#else
+#define GROOT_L0_KEY_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void GROOT_L0_KEY_BOUNDS l0_key_tile_kernel(uint32_t n, const uint32_t* __restrict__ rp,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ feat, uint32_t thr,
                                                           const L0KeyPlan p, uint16_t* __restrict__ lslot,
@@ -1682,10 +1687,18 @@ __global__ void __launch_bounds__(256) hd_key_kernel(const uint32_t* __restrict_
   for (uint32_t slot = blockIdx.x; slot < count; slot += gridDim.x) {
     const uint32_t r = hd_rows[slot], b = rp[r], d = rp[r + 1] - b;
     uint32_t c[4] = {0, 0, 0, 0};
-    for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) {
-      const uint32_t x = __ldg(feat + __ldg(col + b + e));
+    // four neighbours per thread in flight: column loads, then the feature gathers
+    constexpr uint32_t kU = 4;
+    for (uint32_t e0 = threadIdx.x; e0 < d; e0 += kU * blockDim.x) {
+      uint32_t ci[kU];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) c[k] += (x >> (8 * k)) & 0xFFu;
+      for (uint32_t u = 0; u < kU; ++u) ci[u] = e0 + u * blockDim.x < d ? __ldg(col + b + e0 + u * blockDim.x) : 0u;
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t x = e0 + u * blockDim.x < d ? __ldg(feat + ci[u]) : 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] += (x >> (8 * k)) & 0xFFu;
+      }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -1786,20 +1799,34 @@ __global__ void __launch_bounds__(256) l0_ids_kernel(uint32_t n, uint32_t key_wa
                                                      const uint32_t* __restrict__ flags, uint8_t* __restrict__ ids) {
   if (flags[0]) return;
   const uint32_t quads = (n + 3) / 4;
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
-    const uint32_t cta = (((4 * q) / rows_per_group) % key_warps) >> 3;  // the 4 rows share a row group
-    const uint8_t* xl = xlat + static_cast<size_t>(cta) * kDictLocal;
-    uint32_t out = 0;
-    if (4 * q + 3 < n) {
-      const uint2 sl = *reinterpret_cast<const uint2*>(lslot + 4 * q);
-      const uint32_t s4[4] = {sl.x & 0xFFFFu, sl.x >> 16, sl.y & 0xFFFFu, sl.y >> 16};
+  // kU independent quads per thread and iteration: their slot loads are in
+  // flight together (one DRAM round trip per kU quads, not per quad)
+  constexpr uint32_t kU = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t qb = blockIdx.x * blockDim.x + threadIdx.x; qb < quads; qb += stride * kU) {
+    uint2 sl[kU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) out |= static_cast<uint32_t>(s4[u] < kDictLocal ? __ldg(xl + s4[u]) : 0u) << (8 * u);
-      reinterpret_cast<uint32_t*>(ids)[q] = out;
-    } else {
-      for (uint32_t r = 4 * q; r < n; ++r) {
-        const uint32_t sl = lslot[r];
-        ids[r] = sl < kDictLocal ? __ldg(xl + sl) : 0u;
+    for (uint32_t i = 0; i < kU; ++i) {
+      const uint32_t q = qb + i * stride;
+      sl[i] = q < quads && 4 * q + 3 < n ? *reinterpret_cast<const uint2*>(lslot + 4 * q) : make_uint2(~0u, ~0u);
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < kU; ++i) {
+      const uint32_t q = qb + i * stride;
+      if (q >= quads) break;
+      const uint32_t cta = (((4 * q) / rows_per_group) % key_warps) >> 3;  // the 4 rows share a row group
+      const uint8_t* xl = xlat + static_cast<size_t>(cta) * kDictLocal;
+      if (4 * q + 3 < n) {
+        const uint32_t s4[4] = {sl[i].x & 0xFFFFu, sl[i].x >> 16, sl[i].y & 0xFFFFu, sl[i].y >> 16};
+        uint32_t out = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) out |= static_cast<uint32_t>(s4[u] < kDictLocal ? __ldg(xl + s4[u]) : 0u) << (8 * u);
+        reinterpret_cast<uint32_t*>(ids)[q] = out;
+      } else {
+        for (uint32_t r = 4 * q; r < n; ++r) {
+          const uint32_t s1 = lslot[r];
+          ids[r] = s1 < kDictLocal ? __ldg(xl + s1) : 0u;
+        }
       }
     }
   }
@@ -2237,7 +2264,8 @@ static bool layer0_keyed(const groot_model* m, groot_graph* g) {
   const unsigned sms = static_cast<unsigned>(num_sms());
   static const bool tiled_env = env_u32("GROOT_L0_KEY_TILED", 1) != 0;
   const bool key_tiled = tiled_env && g->tp_meta.p && g->tp_rec.p && g->tp_threshold == g->hd_threshold;
-  const unsigned key_ctas = key_tiled ? blocks_for(ntiles, 8, sms * 8)  // a warp per tile
+  static const uint32_t key_per_sm = env_u32("GROOT_L0_KEY_CTAS_PER_SM", 8);
+  const unsigned key_ctas = key_tiled ? blocks_for(ntiles, 8, sms * key_per_sm)  // a warp per tile
                                       : blocks_for((n + kL0KeyRows - 1) / kL0KeyRows, 256, sms * 8);
   if (g->l0_slot.n < n) g->l0_slot.alloc(n);
   if (g->l0_id.n < static_cast<size_t>(ntiles) * kTileM) g->l0_id.alloc(static_cast<size_t>(ntiles) * kTileM);
