@@ -2480,38 +2480,44 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
     ~Ev() { if (e) cudaEventDestroy(e); }
   } evh, evs;
   cudaEvent_t ev_half = evh.e, ev_side = evs.e;
-  // the last layer in kReadbackParts tile ranges: the classes of the copies a
-  // range completes go to the host on the side stream while the next computes
-  constexpr uint32_t kReadbackParts = 8;
-  uint32_t k1 = 0;
+  // the last layer in tile ranges of shrinking size: the classes of the rows a
+  // range completes go to the host on the side stream while the next ranges
+  // compute, so only the last (3 %) range's classes are read after the layer.
+  // Row r of copy k (device row k*P + r) is host row k*n1 + r.
+  constexpr uint32_t kReadbackParts = 9;
+  static constexpr uint16_t kEnd[kReadbackParts] = {250, 450, 600, 720, 820, 890, 940, 970, 1000};  // per mille of tiles
+  auto readback = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {  // device rows [r0, r1), padding rows skipped
+    for (uint64_t k = r0 / P; k < copies && k * P < r1; ++k) {
+      const uint64_t a = std::max<uint64_t>(r0, k * P), b = std::min<uint64_t>(r1, k * P + n1);
+      if (a < b)
+        GROOT_CUDA(cudaMemcpyAsync(labels_out + k * n1 + (a - k * P), cls + a, b - a, cudaMemcpyDeviceToHost, st));
+    }
+  };
+  uint64_t done = 0;  // device rows whose classes are on their way to the host
   if (D == 1) {
     layer_device(m, g, 0, nullptr, g->act[0].p, cls, nullptr, 0, ~0u, true, false);
   } else {
     const float* hin = g->act[(D - 2) & 1].p;
     const uint32_t ntiles = (g->n + kTileM - 1) / kTileM;
+    bool first = true;  // the first launch also computes the layer's HD-row means
     for (uint32_t part = 0; part < kReadbackParts; ++part) {
-      const uint32_t tb = static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * part / kReadbackParts);
-      const uint32_t te = part + 1 == kReadbackParts ? ~0u : static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * (part + 1) / kReadbackParts);
-      layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, tb, te, part == 0, keyed);
+      const uint32_t tb = part ? static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * kEnd[part - 1] / 1000) : 0u;
+      const uint32_t te = part + 1 == kReadbackParts ? ~0u : static_cast<uint32_t>(static_cast<uint64_t>(ntiles) * kEnd[part] / 1000);
+      if (te != ~0u && te <= tb) continue;  // empty range (small graphs)
+      layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, tb, te, first, keyed);
+      first = false;
       if (part + 1 == kReadbackParts || !labels_out) continue;
-      const uint64_t rows_done = static_cast<uint64_t>(te) * kTileM;
-      const uint32_t k0 = k1;
-      while (k1 < copies && static_cast<uint64_t>(k1) * P + n1 <= rows_done) ++k1;
-      if (k1 > k0) {
-        GROOT_CUDA(cudaEventRecord(ev_half, stream()));
-        GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
-        for (uint32_t k = k0; k < k1; ++k)
-          GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
-                                     cudaMemcpyDeviceToHost, side));
-      }
+      const uint64_t rows_done = std::min<uint64_t>(static_cast<uint64_t>(te) * kTileM, g->n);
+      GROOT_CUDA(cudaEventRecord(ev_half, stream()));
+      GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
+      readback(done, rows_done, side);
+      done = rows_done;
     }
-    if (k1) GROOT_CUDA(cudaEventRecord(ev_side, side));
+    if (done) GROOT_CUDA(cudaEventRecord(ev_side, side));
   }
   if (labels_out) {
-    for (uint32_t k = k1; k < copies; ++k)
-      GROOT_CUDA(cudaMemcpyAsync(labels_out + static_cast<size_t>(k) * n1, cls + static_cast<size_t>(k) * P, n1,
-                                 cudaMemcpyDeviceToHost, stream()));
-    if (k1) GROOT_CUDA(cudaStreamWaitEvent(stream(), ev_side, 0));
+    readback(done, g->n, stream());
+    if (done) GROOT_CUDA(cudaStreamWaitEvent(stream(), ev_side, 0));
   }
   if (confusion) {
     ProfScope ps("confusion");

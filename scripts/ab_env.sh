@@ -8,7 +8,7 @@ for spec in "$@"; do
   tag=$1; v=$2; shift 2
   lib=paper_2511_18297_b200/libgroot_b200.so
   [ "$v" != base ] && lib=paper_2511_18297_b200/libgroot_b200_$v.so
-  env GROOT_LIB=$PWD/$lib "$@" timeout 150 python bench.py --no-cpu-baseline --no-side --steps 10 --e2e-steps 3 \
+  env GROOT_LIB=$PWD/$lib "$@" timeout 150 python bench.py --no-cpu-baseline --no-side --steps 10 --e2e-steps ${E2E_STEPS:-3} \
     > gpurun_out/abe_$tag.json 2> gpurun_out/abe_$tag.err
   python -c "
 import json
