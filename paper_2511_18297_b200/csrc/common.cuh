@@ -39,6 +39,18 @@ constexpr int kMaxDevices = 64;
 int current_device();
 // The library stream of the calling thread's current device (groot_set_stream).
 cudaStream_t stream();
+// A second (copy) stream of the current device (forward.cu).
+cudaStream_t side_stream();
+// Timing-free CUDA event owned by a scope.
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() { GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+};
 
 // Makes `dev` the current device for a scope (restored on exit): entry points
 // taking a handle run on the device that owns it.

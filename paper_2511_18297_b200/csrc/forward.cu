@@ -2453,6 +2453,17 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
 // as kReadbackParts launches over consecutive tile ranges, and the classes of
 // the copies each range completes go to the host on a side stream while the
 // next range computes. labels_out is in the reference's numbering (k*n1 + v).
+// Copy stream of the current device (created once, non-blocking): class
+// read-back of the e2e call and encode's label upload overlap the main stream.
+cudaStream_t side_stream() {
+  static std::mutex side_mu;
+  static cudaStream_t side_of[kMaxDevices] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(side_mu);
+  if (!side_of[dev]) GROOT_CUDA(cudaStreamCreateWithFlags(&side_of[dev], cudaStreamNonBlocking));
+  return side_of[dev];
+}
+
 void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls, unsigned long long* confusion,
                               uint32_t copies, uint32_t n1, uint32_t P, uint8_t* labels_out) {
   require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
@@ -2465,24 +2476,13 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
     layer_device(m, g, l, l ? g->act[(l - 1) & 1].p : nullptr, g->act[l & 1].p, cls, nullptr, 0, ~0u, true, keyed);
   // read-back stream: one per device (created once); events per call, so
   // concurrent calls on different devices or threads share nothing
-  static std::mutex side_mu;
-  static cudaStream_t side_of[kMaxDevices] = {};
-  cudaStream_t side;
-  {
-    const int dev = current_device();
-    std::lock_guard<std::mutex> lk(side_mu);
-    if (!side_of[dev]) GROOT_CUDA(cudaStreamCreateWithFlags(&side_of[dev], cudaStreamNonBlocking));
-    side = side_of[dev];
-  }
-  struct Ev {
-    cudaEvent_t e = nullptr;
-    Ev() { GROOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
-    ~Ev() { if (e) cudaEventDestroy(e); }
-  } evh, evs;
+  cudaStream_t side = side_stream();
+  Event evh, evs;
   cudaEvent_t ev_half = evh.e, ev_side = evs.e;
   // the last layer in tile ranges of shrinking size: the classes of the rows a
   // range completes go to the host on the side stream while the next ranges
-  // compute, so only the last (3 %) range's classes are read after the layer.
+  // compute, so only the last (3 %) range's classes are read after the layer
+  // (beside the confusion count).
   // Row r of copy k (device row k*P + r) is host row k*n1 + r.
   constexpr uint32_t kReadbackParts = 9;
   static constexpr uint16_t kEnd[kReadbackParts] = {250, 450, 600, 720, 820, 890, 940, 970, 1000};  // per mille of tiles
@@ -2506,8 +2506,9 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
       if (te != ~0u && te <= tb) continue;  // empty range (small graphs)
       layer_device(m, g, D - 1, hin, nullptr, cls, nullptr, tb, te, first, keyed);
       first = false;
-      if (part + 1 == kReadbackParts || !labels_out) continue;
-      const uint64_t rows_done = std::min<uint64_t>(static_cast<uint64_t>(te) * kTileM, g->n);
+      if (!labels_out) continue;
+      const uint64_t rows_done =
+          part + 1 == kReadbackParts ? g->n : std::min<uint64_t>(static_cast<uint64_t>(te) * kTileM, g->n);
       GROOT_CUDA(cudaEventRecord(ev_half, stream()));
       GROOT_CUDA(cudaStreamWaitEvent(side, ev_half, 0));
       readback(done, rows_done, side);
@@ -2515,15 +2516,13 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
     }
     if (done) GROOT_CUDA(cudaEventRecord(ev_side, side));
   }
-  if (labels_out) {
-    readback(done, g->n, stream());
-    if (done) GROOT_CUDA(cudaStreamWaitEvent(stream(), ev_side, 0));
-  }
-  if (confusion) {
+  if (labels_out && done < g->n) readback(done, g->n, stream());  // depth 1: one launch
+  if (confusion) {  // overlaps the read-back of the last range
     ProfScope ps("confusion");
     GROOT_LAUNCH(confusion_kernel, blocks_for(g->n / 16 + 1, 256, static_cast<unsigned>(num_sms()) * 8), 256, 0, g->n, cls,
                  g->labels.p, confusion);
   }
+  if (done) GROOT_CUDA(cudaStreamWaitEvent(stream(), ev_side, 0));
 }
 
 // confusion[truth][pred] += over rows (device counts; labels >= 5 are skipped)

@@ -523,13 +523,24 @@ groot_graph* encode(uint32_t ni, uint32_t na, const uint32_t* h_ands, uint32_t n
     outs.upload(h_outs, no);
     const uint32_t none = 0xFFFFFFFFu;
     bad.upload(&none, 1);
-    if (h_labels) g->labels.upload(h_labels, n); else g->labels.zero();
+    // labels (only the confusion reads them) go up on the copy stream behind the
+    // AIG, under the encode and CSR kernels; the main stream waits for them below
+    Event lab_up, lab_done;
+    if (h_labels) {
+      GROOT_CUDA(cudaEventRecord(lab_up.e, stream()));
+      GROOT_CUDA(cudaStreamWaitEvent(side_stream(), lab_up.e, 0));
+      GROOT_CUDA(cudaMemcpyAsync(g->labels.p, h_labels, n, cudaMemcpyHostToDevice, side_stream()));
+      GROOT_CUDA(cudaEventRecord(lab_done.e, side_stream()));
+    } else {
+      g->labels.zero();
+    }
     if (host_timing) stream_sync();
     const auto t1 = now();
     GROOT_LAUNCH(encode_kernel, blocks_for(n, 256), 256, 0, ni, na, ands.p, no, outs.p,
                  reinterpret_cast<uint32_t*>(g->feat.p), reinterpret_cast<uint2*>(g->edges.p), bad.p);
     const auto t2 = now();
     build_csr(n, ne, g->edges.p, g->rp.p, g->col.p);
+    if (h_labels) GROOT_CUDA(cudaStreamWaitEvent(stream(), lab_done.e, 0));
     uint32_t b = none;  // the validity flag, read with the build's final synchronisation
     bad.download(&b, 1);
     stream_sync();
