@@ -46,28 +46,29 @@ __device__ __forceinline__ uint32_t hash_find(const uint32_t* hk, uint32_t c) {
   return h;
 }
 
-// Warp-wide bitonic sort of 256 keys held 8 per lane (index lane*8 + k),
-// ascending: in-register compare-exchanges below distance 8, shuffles above.
-__device__ __forceinline__ void warp_sort256(uint32_t (&v)[8], uint32_t lane) {
+// Warp-wide bitonic sort of 32*PER keys held PER per lane (index lane*PER + k),
+// ascending: in-register compare-exchanges below distance PER, shuffles above.
+template <uint32_t PER>
+__device__ __forceinline__ void warp_sort(uint32_t (&v)[PER], uint32_t lane) {
 #pragma unroll
-  for (uint32_t s = 2; s <= 256; s <<= 1) {
+  for (uint32_t s = 2; s <= 32 * PER; s <<= 1) {
 #pragma unroll
     for (uint32_t d = s >> 1; d > 0; d >>= 1) {
-      if (d >= 8) {
-        const uint32_t lb = d >> 3;
+      if (d >= PER) {
+        const uint32_t lb = d / PER;
         const bool lower = (lane & lb) == 0;
 #pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
+        for (uint32_t k = 0; k < PER; ++k) {
           const uint32_t p = __shfl_xor_sync(0xffffffffu, v[k], lb);
-          const bool up = ((lane * 8 + k) & s) == 0;
+          const bool up = ((lane * PER + k) & s) == 0;
           v[k] = (lower == up) ? min(v[k], p) : max(v[k], p);
         }
       } else {
 #pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
+        for (uint32_t k = 0; k < PER; ++k) {
           if (k & d) continue;
-          const bool up = ((lane * 8 + k) & s) == 0;
           const uint32_t x = v[k], y = v[k ^ d];
+          const bool up = ((lane * PER + k) & s) == 0;
           if ((x > y) == up) {
             v[k] = y;
             v[k ^ d] = x;
@@ -164,10 +165,23 @@ __global__ void __launch_bounds__(kTpWarps * 32) tile_plan_kernel(uint32_t n, co
         slow = H > halo_cap;
         if (!slow) {
           __syncwarp();
+          if (H <= 128) {  // the usual halo (~120 rows on CSA tiles): a 128-key sort, 4 per lane
+            uint32_t h4[4];
 #pragma unroll
-          for (uint32_t k = 0; k < 8; ++k) hsorted[k] = lane * 8 + k < H ? uq[lane * 8 + k] : kEmpty;
-          __syncwarp();
-          warp_sort256(hsorted, lane);
+            for (uint32_t k = 0; k < 4; ++k) h4[k] = lane * 4 + k < H ? uq[lane * 4 + k] : kEmpty;
+            __syncwarp();
+            warp_sort<4>(h4, lane);
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) {  // to the 8-per-lane layout: element lane*8+k
+              const uint32_t x = __shfl_sync(0xffffffffu, h4[k & 3], (2 * lane + (k >> 2)) & 31);
+              hsorted[k] = lane < 16 ? x : kEmpty;
+            }
+          } else {
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) hsorted[k] = lane * 8 + k < H ? uq[lane * 8 + k] : kEmpty;
+            __syncwarp();
+            warp_sort<8>(hsorted, lane);
+          }
 #pragma unroll
           for (uint32_t k = 0; k < 8; ++k)
             if (lane * 8 + k < H) hv[hash_find(hk, hsorted[k])] = static_cast<uint16_t>(lane * 8 + k);
