@@ -576,7 +576,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if strong and world > 1 else "weak",
-            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate)",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate; certified TF32 head)",
             "data": f"synthetic (deterministic {args.circuit.upper()} multiplier generator; trained 8-bit ASG1 weights)",
             "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {global_batch} "
                                    f"(4-layer GraphSAGE 4-32-32-32-32 + 32->5 head, predict_full)",
@@ -674,7 +674,7 @@ def run_halo(args):
         print(json.dumps({
             "metric": METRIC, "value": E / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate)",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05 transform, fp32 accumulate; certified TF32 head)",
             "data": f"synthetic (deterministic {args.circuit.upper()} multiplier generator; trained 8-bit ASG1 weights)",
             "config": {"workload": f"{args.width}-bit {args.circuit.upper()} multiplier AIG, batch {args.batch}, "
                                    f"{world} partitions (partition_multilevel), exact halo (mode X)",
