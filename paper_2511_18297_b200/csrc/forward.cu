@@ -17,7 +17,9 @@
 //   MMA warp      tcgen05.mma kind::tf32, A from TMEM, W from smem, 3 products
 //                 (hi*hi + hi*lo + lo*hi) into a double-buffered accumulator
 //   4 epilogue    tcgen05.ld, + bias, ReLU, 256-bit stores of whole rows (or, in
-//                 the last layer, the 32 -> classes head + first-max argmax)
+//                 the last layer, the 32 -> classes head on the tensor core +
+//                 first-max argmax; classes-only calls certify each row's class
+//                 from a single-operand head with a margin bound, GROOT_HEAD_CERT)
 // The same kernel without the MMA is the standalone LD SpMM. High-degree rows
 // (the row classifier's HD band; the PIs of a multiplier) are aggregated first
 // in L2-ordered chunks with a fixed-order reduction (hd_chunk_kernel).
