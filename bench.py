@@ -68,17 +68,20 @@ def parse():
 # helpers
 # ---------------------------------------------------------------------------
 def init_nccl(local, world):
-    """One NCCL communicator over all ranks; NCCL's INIT log (stderr) stays on so
-    the communicator's nranks and transport can be checked from the run log."""
+    """One NCCL communicator over all ranks. Each rank reports its device, the
+    NCCL version and the communicator's size (an all-reduce of ones) on stderr;
+    NCCL_DEBUG stays unset because NCCL logs to stdout, which carries only the
+    JSON line."""
     import torch
     import torch.distributed as dist
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
-    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t = torch.ones(1, device="cuda")
+    dist.all_reduce(t)
+    torch.cuda.synchronize()
     print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()} on cuda:{local} "
-          f"({torch.cuda.get_device_name(local)}), NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}",
-          file=sys.stderr, flush=True)
-    assert dist.get_world_size() == world
+          f"({torch.cuda.get_device_name(local)}), NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, "
+          f"communicator size {int(t.item())}", file=sys.stderr, flush=True)
+    assert dist.get_world_size() == world and int(t.item()) == world
 
 
 def dist_env():
