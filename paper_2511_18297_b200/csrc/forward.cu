@@ -2450,11 +2450,6 @@ void forward_device(const groot_model* m, groot_graph* g, uint8_t* cls, float* l
   }
 }
 
-// Forward + classify of a tile-aligned batch (batch_padded: copy k at rows
-// k*P .. k*P + n1) with the class read-back overlapped: the last layer runs
-// as kReadbackParts launches over consecutive tile ranges, and the classes of
-// the copies each range completes go to the host on a side stream while the
-// next range computes. labels_out is in the reference's numbering (k*n1 + v).
 // Copy stream of the current device (created once, non-blocking): class
 // read-back of the e2e call and encode's label upload overlap the main stream.
 cudaStream_t side_stream() {
@@ -2466,6 +2461,11 @@ cudaStream_t side_stream() {
   return side_of[dev];
 }
 
+// Forward + classify of a tile-aligned batch (batch_padded: copy k at rows
+// k*P .. k*P + n1) with the class read-back overlapped: the last layer runs
+// as kReadbackParts launches over consecutive tile ranges, and the classes of
+// the rows each range completes go to the host on a side stream while the
+// next range computes. labels_out is in the reference's numbering (k*n1 + v).
 void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls, unsigned long long* confusion,
                               uint32_t copies, uint32_t n1, uint32_t P, uint8_t* labels_out) {
   require(m->in_dim == 4 && m->hidden == kF, "forward: model shape unsupported (in_dim 4, hidden 32)");
