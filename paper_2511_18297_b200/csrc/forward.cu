@@ -94,7 +94,9 @@ constexpr uint32_t kHeadN = 16;
 static_assert(!(GROOT_HEAD_CERT && GROOT_LAST_PIPE), "the certified head keeps its row's x in registers");
 static_assert(!GROOT_LAST_ACC2 || GROOT_HEAD_CERT, "two accumulators leave room for the certified head only");
 // the MMA warp issues tile i's head after tile i + 1's layer MMAs
+#ifndef GROOT_HEAD_AFTER_MMA
 #define GROOT_HEAD_AFTER_MMA (GROOT_LAST_PIPE || GROOT_LAST_ACC2)
+#endif
 constexpr uint32_t kHeadHiCol = kAccCol0 + (GROOT_LAST_ACC2 ? 2 : 1) * kAccCols;  // 448 (ACC2) / 416 (the unused second accumulator)
 constexpr uint32_t kHeadLoCol = kAccCol0 + 2 * kAccCols;  // 448 (not with the certified head)
 constexpr uint32_t kHeadDCol = kAccCol0 + 3 * kAccCols;   // 480
