@@ -1092,7 +1092,9 @@ int groot_classify_aig(const groot_model* m, uint32_t ni, uint32_t na, const uin
       if (copies > 1) {
         const uint32_t Pa = (n1 + 127u) / 128u * 128u;
         groot_graph* gp = batch_padded(g1, copies, Pa);
-        if (m->depth > 1 && replicate_forward_plan(g1, gp, copies, Pa)) {
+        static const bool periodic = std::getenv("GROOT_E2E_PERIODIC") == nullptr ||
+                                     std::atoi(std::getenv("GROOT_E2E_PERIODIC")) != 0;  // experiment knob
+        if (periodic && m->depth > 1 && replicate_forward_plan(g1, gp, copies, Pa)) {
           g = gp;
           P = Pa;
         } else {

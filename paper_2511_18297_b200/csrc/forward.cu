@@ -2488,8 +2488,10 @@ void forward_classify_to_host(const groot_model* m, groot_graph* g, uint8_t* cls
   // compute, so only the last (3 %) range's classes are read after the layer
   // (beside the confusion count).
   // Row r of copy k (device row k*P + r) is host row k*n1 + r.
-  constexpr uint32_t kReadbackParts = 9;
-  static constexpr uint16_t kEnd[kReadbackParts] = {250, 450, 600, 720, 820, 890, 940, 970, 1000};  // per mille of tiles
+  static const uint32_t single = env_u32("GROOT_READBACK_SINGLE", 0);  // experiment: one launch, read-back after it
+  const uint32_t kReadbackParts = single ? 1u : 9u;
+  static constexpr uint16_t kEnd9[9] = {250, 450, 600, 720, 820, 890, 940, 970, 1000};  // per mille of tiles
+  const uint16_t* kEnd = single ? kEnd9 + 8 : kEnd9;
   auto readback = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {  // device rows [r0, r1), padding rows skipped
     for (uint64_t k = r0 / P; k < copies && k * P < r1; ++k) {
       const uint64_t a = std::max<uint64_t>(r0, k * P), b = std::min<uint64_t>(r1, k * P + n1);
